@@ -1,0 +1,168 @@
+/*
+ * mqo_gpu.h -- the C ABI of the B200-native mQO inner loop
+ * (libmqo_b200.so, built from paper_2605_06921_b200/csrc).
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (/root/reference/proj/core/include/mqo/).  Plain pointers, sizes and POD
+ * structs only: no torch or C++ types, no exceptions cross it.  Every entry
+ * point returns MQO_OK (0) or an error code, with mqo_last_error() holding a
+ * thread-local message; MQO_ERR_INVALID / MQO_ERR_LOGIC correspond to the
+ * reference's std::invalid_argument / std::logic_error (and carry the same
+ * messages), so a C++ facade can rethrow them unchanged.
+ *
+ * Each declaration cites the reference interface it replaces (file:line,
+ * relative to /root/reference/proj/core/).  Layouts: a "batch" holds B
+ * chains (independent trajectories) of one graph on one device.  Host
+ * state buffers are chain-major, B rows of n doubles -- chain b is exactly
+ * the reference's std::vector<double> RelaxedState::x (objectives.hpp:45-48).
+ * On the device the batch is stored vertex-major (X[v][B_pad]) so that a
+ * neighbour gather of all chains is one coalesced row read.
+ */
+#ifndef MQO_GPU_H
+#define MQO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status --------------------------------------------------------- */
+enum {
+  MQO_OK = 0,
+  MQO_ERR_INVALID = 1, /* std::invalid_argument in the reference */
+  MQO_ERR_LOGIC = 2,   /* std::logic_error in the reference */
+  MQO_ERR_CUDA = 3,
+  MQO_ERR_NCCL = 4,
+  MQO_ERR_OTHER = 5
+};
+
+/* Thread-local message of the last failing call on this thread. */
+const char* mqo_last_error(void);
+/* Library identification, e.g. "mqo_b200 0.1 sm_100a". */
+const char* mqo_version(void);
+
+/* ---- enums mirroring the reference ------------------------------------ */
+/* ObjectiveSpec alternatives, objectives.hpp:22-35 (variant index order). */
+enum {
+  MQO_MIS_QUBO = 0,
+  MQO_LAPLACIAN = 1,
+  MQO_PERTURBED_LAPLACIAN = 2,
+  MQO_ADJACENCY = 3,
+  MQO_PERTURBED_BIAS = 4
+};
+/* Problem, objectives.hpp:12. */
+enum { MQO_PROBLEM_MIS = 0, MQO_PROBLEM_MAXCUT = 1 };
+/* StopReason, pga.hpp:23. */
+enum { MQO_CONVERGED = 0, MQO_CHECKER_ACCEPTED = 1, MQO_ITER_CAP = 2 };
+
+/* ObjectiveSpec (objectives.hpp:22-35): kind + gamma/lambda. */
+typedef struct {
+  int32_t kind;
+  double param; /* MisQubo::gamma, PerturbedLaplacian/PerturbedBias::lambda */
+} mqo_objective;
+
+/* OptimizerConfig (pga.hpp:13-19). */
+typedef struct {
+  double alpha;
+  double beta;
+  int32_t max_iters;
+  double conv_tol;
+  int32_t check_every;
+} mqo_optimizer;
+
+/* ---- graph store (graph.hpp:20-63) ------------------------------------
+ * Uploads an immutable CSR (int64 offsets[n+1], int32 neighbours[2m], rows
+ * strictly ascending, no self loops) to `device`.  The invariants of
+ * Graph::check_invariants (graph.cpp:44-56) are verified on the host first
+ * and a violation returns MQO_ERR_LOGIC with the reference's message.
+
+ * device < 0 keeps a host-only graph (CSR readable, no batches).
+ * Replaces: Graph storage + Graph::from_edges's output (graph.cpp:8-42). */
+typedef struct mqo_graph mqo_graph;
+int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t* neighbors,
+                     int32_t device, mqo_graph** out);
+int mqo_graph_free(mqo_graph* g);
+int mqo_graph_info(const mqo_graph* g, int32_t* n, int64_t* m, int32_t* max_degree);
+/* Copies the canonical CSR back (offsets[n+1], neighbors[2m]). */
+int mqo_graph_csr(const mqo_graph* g, int64_t* offsets, int32_t* neighbors);
+
+/* Graph::from_edges (graph.hpp:26, graph.cpp:8-42): edges in any order and
+ * orientation, duplicates collapsed, self loops rejected
+ * (MQO_ERR_INVALID, reference messages); canonical CSR uploaded. */
+int mqo_graph_from_edges(int32_t n, int64_t num_edges, const int32_t* eu, const int32_t* ev,
+                         int32_t device, mqo_graph** out);
+
+/* GraphGenSpec (graph.hpp:67-91) and generate() (graph.cpp:169-178):
+ * bit-identical graphs to the reference for the same (spec, seed). */
+enum { MQO_GEN_ER = 0, MQO_GEN_BA = 1, MQO_GEN_SBM = 2 };
+typedef struct {
+  int32_t kind;
+  int32_t n;
+  double p;         /* ErSpec::p */
+  int32_t m_attach; /* BaSpec::m_attach */
+  int32_t k;        /* SbmSpec::k */
+  double p_in, p_out;
+  uint64_t seed;
+} mqo_gen_spec;
+int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph** out);
+
+/* ---- chain batch -------------------------------------------------------
+ * A batch of `chains` relaxed states (RelaxedState, objectives.hpp:45-48)
+ * plus velocities, the per-chain xoshiro streams and control words, on the
+ * graph's device, with its own CUDA stream. */
+typedef struct mqo_batch mqo_batch;
+int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out);
+int mqo_batch_free(mqo_batch* b);
+int mqo_batch_chains(const mqo_batch* b, int32_t* chains, int32_t* padded);
+/* The cudaStream_t the batch launches on (for event timing by callers). */
+int mqo_batch_stream(const mqo_batch* b, void** stream);
+/* Blocks until all work queued on the batch stream has finished. */
+int mqo_batch_sync(mqo_batch* b);
+
+/* Host <-> device state copies.  x / v are chain-major [chains][n]
+ * doubles (chain b = the reference's std::vector<double>). */
+int mqo_batch_set_x(mqo_batch* b, const double* x);
+int mqo_batch_get_x(mqo_batch* b, double* x);
+int mqo_batch_set_v(mqo_batch* b, const double* v);
+int mqo_batch_get_v(mqo_batch* b, double* v);
+/* Zeroes every velocity (the fresh `velocity` of run_trajectory,
+ * pga.cpp:75). */
+int mqo_batch_zero_v(mqo_batch* b);
+
+/* project() on every chain (pga.cpp:47-49, clamp pga.cpp:31-34). */
+int mqo_project(mqo_batch* b, int32_t problem);
+
+/* gradient() of every chain at its current x, written chain-major to the
+ * host buffer `out` [chains][n] (objectives.cpp:101-134; the dominant SpMV
+ * is Graph::adjacency_apply / laplacian_apply, graph.cpp:63-88). */
+int mqo_gradient(mqo_batch* b, const mqo_objective* obj, double* out);
+
+/* step() on every chain, in place on the device state: v = beta v + grad,
+ * x = clamp(x + alpha v) (pga.cpp:51-61).  Asynchronous on the batch
+ * stream; bit-identical to the reference for every chain. */
+int mqo_step(mqo_batch* b, const mqo_objective* obj, const mqo_optimizer* opt);
+
+/* run_trajectory() on every chain from its current x (pga.cpp:63-111):
+ * projects, zeroes the velocity, iterates the fused step with the MIS
+ * fixed-point checker (pga.cpp:91-98,113-135) or the MaxCut ||dx||_inf stop
+ * (pga.cpp:99-102) until each chain stops.  `deadline_secs` is an absolute
+ * CLOCK_MONOTONIC time (<0: none) polled every 256 iterations like
+ * pga.cpp:104-107.  On return the device x of chain b is its
+ * TrajectoryOutcome::state; iterations[b] / reasons[b] (host arrays, may be
+ * NULL) receive TrajectoryOutcome::iterations / reason. */
+int mqo_run_trajectories(mqo_batch* b, const mqo_objective* obj, const mqo_optimizer* opt,
+                         double deadline_secs, int32_t* iterations, int32_t* reasons);
+
+/* mis_fixed_point_check() on every chain's current (binary) x
+ * (pga.cpp:113-135).  fixed[b] in {0,1}.  Returns MQO_ERR_INVALID with the
+ * reference message when a state is not binary or gamma/alpha are out of
+ * range. */
+int mqo_mis_fixed_point_check(mqo_batch* b, double gamma, double alpha, int32_t* fixed);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MQO_GPU_H */

@@ -1,0 +1,360 @@
+"""Python mirror of the reference's public C++ API for the mQO hot path.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/core/include/mqo/ (graph.hpp, objectives.hpp, pga.hpp,
+solver.hpp); every call goes through the C ABI of include/mqo_gpu.h into
+libmqo_b200.so.  ``std::invalid_argument`` surfaces as
+:class:`InvalidArgument` (a ``ValueError``), ``std::logic_error`` as
+:class:`LogicError`.
+
+The batched entry points (:class:`ChainBatch`) are the B200-native shape of
+the API: B independent chains of one graph advance together on the device.
+The single-chain functions (``step``, ``run_trajectory`` ...) are the
+reference signatures, implemented as a batch of one.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (ADJACENCY, CHECKER_ACCEPTED, CONVERGED, ITER_CAP, LAPLACIAN, MIS_QUBO,
+                   PERTURBED_BIAS, PERTURBED_LAPLACIAN, PROBLEM_MAXCUT, PROBLEM_MIS,
+                   InvalidArgument, LogicError, MqoError, Objective, Optimizer, check, lib)
+
+__all__ = [
+    "Graph", "ErSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
+    "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
+    "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
+    "InvalidArgument", "LogicError", "MqoError",
+]
+
+
+def _ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+_D = C.POINTER(C.c_double)
+_I32 = C.POINTER(C.c_int32)
+_I64 = C.POINTER(C.c_int64)
+_U8 = C.POINTER(C.c_uint8)
+
+
+class StopReason:  # pga.hpp:23
+    Converged, CheckerAccepted, IterCap = CONVERGED, CHECKER_ACCEPTED, ITER_CAP
+    names = {CONVERGED: "converged", CHECKER_ACCEPTED: "checker-accepted", ITER_CAP: "iter-cap"}
+
+
+# ------------------------------------------------------------- objectives
+@dataclass(frozen=True)
+class MisQubo:  # objectives.hpp:22-24
+    gamma: float = 2.0
+    kind = MIS_QUBO
+
+    @property
+    def param(self):
+        return self.gamma
+
+
+@dataclass(frozen=True)
+class Laplacian:
+    kind = LAPLACIAN
+    param = 0.0
+
+
+@dataclass(frozen=True)
+class PerturbedLaplacian:
+    lam: float = 0.001
+    kind = PERTURBED_LAPLACIAN
+
+    @property
+    def param(self):
+        return self.lam
+
+
+@dataclass(frozen=True)
+class Adjacency:
+    kind = ADJACENCY
+    param = 0.0
+
+
+@dataclass(frozen=True)
+class PerturbedBias:  # the paper's new MaxCut objective f_B
+    lam: float = 0.001
+    kind = PERTURBED_BIAS
+
+    @property
+    def param(self):
+        return self.lam
+
+
+def problem_of(spec) -> int:  # objectives.cpp:8-10
+    return PROBLEM_MIS if spec.kind == MIS_QUBO else PROBLEM_MAXCUT
+
+
+def _obj(spec) -> Objective:
+    return Objective(spec.kind, float(spec.param))
+
+
+@dataclass
+class OptimizerConfig:  # pga.hpp:13-19
+    alpha: float = 0.8
+    beta: float = 0.0
+    max_iters: int = 5000
+    conv_tol: float = 1e-6
+    check_every: int = 1
+
+    def to_c(self) -> Optimizer:
+        return Optimizer(self.alpha, self.beta, self.max_iters, self.conv_tol, self.check_every)
+
+
+# ------------------------------------------------------------------ graph
+@dataclass(frozen=True)
+class ErSpec:  # graph.hpp:67-70
+    n: int
+    p: float
+
+
+@dataclass(frozen=True)
+class BaSpec:  # graph.hpp:72-75
+    n: int
+    m_attach: int = 1
+
+
+@dataclass(frozen=True)
+class SbmSpec:  # graph.hpp:77-82
+    n: int
+    k: int = 2
+    p_in: float = 0.0
+    p_out: float = 0.0
+
+
+class _GenSpec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int32), ("p", C.c_double),
+                ("m_attach", C.c_int32), ("k", C.c_int32), ("p_in", C.c_double),
+                ("p_out", C.c_double), ("seed", C.c_uint64)]
+
+
+lib.mqo_generate.argtypes = [C.POINTER(_GenSpec), C.c_int32, C.POINTER(C.c_void_p)]
+lib.mqo_generate.restype = C.c_int
+lib.mqo_graph_from_edges.argtypes = [C.c_int32, C.c_int64, _I32, _I32, C.c_int32,
+                                     C.POINTER(C.c_void_p)]
+lib.mqo_graph_from_edges.restype = C.c_int
+lib.mqo_graph_csr.argtypes = [C.c_void_p, _I64, _I32]
+lib.mqo_graph_csr.restype = C.c_int
+
+
+class Graph:
+    """Immutable CSR graph (graph.hpp:20-63), resident in HBM on ``device``
+    (``device=-1`` keeps a host-only graph: CSR readable, no chain batches)."""
+
+    def __init__(self, handle: C.c_void_p, device: int):
+        self._h = handle
+        self.device = device
+        n, m, d = C.c_int32(), C.c_int64(), C.c_int32()
+        check(lib.mqo_graph_info(handle, C.byref(n), C.byref(m), C.byref(d)))
+        self._n, self._m, self._dmax = n.value, m.value, d.value
+        self._csr = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mqo_graph_free(h)
+            self._h = None
+
+    # construction ---------------------------------------------------------
+    @staticmethod
+    def from_edges(n: int, edges, device: int = 0) -> "Graph":
+        e = np.asarray(edges, dtype=np.int32).reshape(-1, 2)
+        u = np.ascontiguousarray(e[:, 0])
+        v = np.ascontiguousarray(e[:, 1])
+        h = C.c_void_p()
+        check(lib.mqo_graph_from_edges(n, len(u), _ptr(u, _I32), _ptr(v, _I32), device,
+                                       C.byref(h)))
+        return Graph(h, device)
+
+    @staticmethod
+    def from_csr(offsets, neighbors, device: int = 0) -> "Graph":
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.int32)
+        if nbr.size == 0:
+            nbr = np.zeros(1, np.int32)
+        h = C.c_void_p()
+        check(lib.mqo_graph_upload(len(off) - 1, _ptr(off, _I64), _ptr(nbr, _I32), device,
+                                   C.byref(h)))
+        return Graph(h, device)
+
+    # accessors ------------------------------------------------------------
+    def n(self) -> int:
+        return self._n
+
+    def m(self) -> int:
+        return self._m
+
+    def max_degree(self) -> int:
+        return self._dmax
+
+    def csr(self):
+        if self._csr is None:
+            off = np.empty(self._n + 1, np.int64)
+            nbr = np.empty(max(2 * self._m, 1), np.int32)
+            check(lib.mqo_graph_csr(self._h, _ptr(off, _I64), _ptr(nbr, _I32)))
+            self._csr = (off, nbr[: 2 * self._m].copy())
+        return self._csr
+
+    def degree(self, v: int) -> int:
+        off, _ = self.csr()
+        return int(off[v + 1] - off[v])
+
+    def neighbors(self, v: int) -> np.ndarray:
+        off, nbr = self.csr()
+        return nbr[off[v]:off[v + 1]]
+
+
+def generate(spec, seed: int, device: int = 0) -> Graph:
+    """generate(GraphGenSpec) (graph.cpp:169-178), bit-identical graphs."""
+    s = _GenSpec()
+    s.seed = seed
+    if isinstance(spec, ErSpec):
+        s.kind, s.n, s.p = 0, spec.n, spec.p
+    elif isinstance(spec, BaSpec):
+        s.kind, s.n, s.m_attach = 1, spec.n, spec.m_attach
+    elif isinstance(spec, SbmSpec):
+        s.kind, s.n, s.k, s.p_in, s.p_out = 2, spec.n, spec.k, spec.p_in, spec.p_out
+    else:
+        raise InvalidArgument(1, "generate: unknown spec")
+    h = C.c_void_p()
+    check(lib.mqo_generate(C.byref(s), device, C.byref(h)))
+    return Graph(h, device)
+
+
+# ------------------------------------------------------------ chain batch
+class ChainBatch:
+    """B chains (relaxed states + velocities) of one graph on its device."""
+
+    def __init__(self, g: Graph, chains: int):
+        self.g = g
+        self.chains = chains
+        h = C.c_void_p()
+        check(lib.mqo_batch_create(g._h, chains, C.byref(h)))
+        self._h = h
+        pad = C.c_int32()
+        check(lib.mqo_batch_chains(h, None, C.byref(pad)))
+        self.padded = pad.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mqo_batch_free(h)
+            self._h = None
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(lib.mqo_batch_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def sync(self) -> None:
+        check(lib.mqo_batch_sync(self._h))
+
+    def _shape_in(self, a) -> np.ndarray:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if a.shape != (self.chains, self.g.n()):
+            a = a.reshape(self.chains, self.g.n())
+        return a
+
+    def set_x(self, x) -> None:
+        x = self._shape_in(x)
+        check(lib.mqo_batch_set_x(self._h, _ptr(x, _D)))
+
+    def get_x(self, out: np.ndarray | None = None) -> np.ndarray:
+        out = np.empty((self.chains, self.g.n()), np.float64) if out is None else out
+        check(lib.mqo_batch_get_x(self._h, _ptr(out, _D)))
+        return out
+
+    def set_v(self, v) -> None:
+        v = self._shape_in(v)
+        check(lib.mqo_batch_set_v(self._h, _ptr(v, _D)))
+
+    def get_v(self) -> np.ndarray:
+        out = np.empty((self.chains, self.g.n()), np.float64)
+        check(lib.mqo_batch_get_v(self._h, _ptr(out, _D)))
+        return out
+
+    def zero_v(self) -> None:
+        check(lib.mqo_batch_zero_v(self._h))
+
+    def project(self, problem: int) -> None:
+        check(lib.mqo_project(self._h, problem))
+
+    def gradient(self, spec) -> np.ndarray:
+        out = np.empty((self.chains, self.g.n()), np.float64)
+        o = _obj(spec)
+        check(lib.mqo_gradient(self._h, C.byref(o), _ptr(out, _D)))
+        return out
+
+    def step(self, spec, cfg: OptimizerConfig) -> None:
+        """One fused PGA step of every chain (asynchronous)."""
+        o, c = _obj(spec), cfg.to_c()
+        check(lib.mqo_step(self._h, C.byref(o), C.byref(c)))
+
+    def run_trajectories(self, spec, cfg: OptimizerConfig, deadline: float = -1.0):
+        o, c = _obj(spec), cfg.to_c()
+        it = np.zeros(self.chains, np.int32)
+        rs = np.zeros(self.chains, np.int32)
+        check(lib.mqo_run_trajectories(self._h, C.byref(o), C.byref(c), deadline,
+                                       _ptr(it, _I32), _ptr(rs, _I32)))
+        return it, rs
+
+    def mis_fixed_point_check(self, gamma: float, alpha: float) -> np.ndarray:
+        f = np.zeros(self.chains, np.int32)
+        check(lib.mqo_mis_fixed_point_check(self._h, gamma, alpha, _ptr(f, _I32)))
+        return f.astype(bool)
+
+
+# ------------------------------------------- single-chain reference calls
+@dataclass
+class RelaxedState:  # objectives.hpp:45-48
+    x: np.ndarray
+    problem: int = PROBLEM_MIS
+
+
+@dataclass
+class TrajectoryOutcome:  # pga.hpp:26-30
+    state: np.ndarray
+    iterations: int = 0
+    reason: int = ITER_CAP
+    extra: dict = field(default_factory=dict)
+
+
+def gradient(spec, g: Graph, x) -> np.ndarray:
+    b = ChainBatch(g, 1)
+    b.set_x(np.asarray(x, np.float64)[None, :])
+    return b.gradient(spec)[0]
+
+
+def step(spec, g: Graph, x, velocity, cfg: OptimizerConfig):
+    """pga.hpp:36-37 -- returns (x, velocity) after one step."""
+    b = ChainBatch(g, 1)
+    b.set_x(np.asarray(x, np.float64)[None, :])
+    v = np.zeros(g.n()) if velocity is None or len(velocity) == 0 else velocity
+    b.set_v(np.asarray(v, np.float64)[None, :])
+    b.step(spec, cfg)
+    return b.get_x()[0], b.get_v()[0]
+
+
+def run_trajectory(spec, g: Graph, init, cfg: OptimizerConfig,
+                   deadline: float | None = None) -> TrajectoryOutcome:
+    """pga.hpp:47-49 on one chain."""
+    b = ChainBatch(g, 1)
+    b.set_x(np.asarray(init, np.float64)[None, :])
+    it, rs = b.run_trajectories(spec, cfg, -1.0 if deadline is None else deadline)
+    return TrajectoryOutcome(b.get_x()[0], int(it[0]), int(rs[0]))
+
+
+def mis_fixed_point_check(g: Graph, x, gamma: float, alpha: float) -> bool:
+    b = ChainBatch(g, 1)
+    b.set_x(np.asarray(x, np.float64)[None, :])
+    return bool(b.mis_fixed_point_check(gamma, alpha)[0])

@@ -1,0 +1,123 @@
+// common.cuh -- shared internals of libmqo_b200.so: error plumbing for the C
+// ABI (include/mqo_gpu.h), the graph / batch handle layouts, and the exact
+// (no-FMA) fp64 helpers every kernel uses so results stay bit-identical to
+// the reference's `-O3 -ffp-contract=off`-style scalar code.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mqo_gpu.h"
+
+namespace mqo_b200 {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define MQO_CUDA(expr)                                                           \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess)                                                       \
+      throw ::mqo_b200::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Runs `f`, mapping the reference's exception types onto the ABI codes.
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return MQO_OK;
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return MQO_ERR_INVALID;
+  } catch (const std::logic_error& e) {
+    set_error(e.what());
+    return MQO_ERR_LOGIC;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    return MQO_ERR_CUDA;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return MQO_ERR_OTHER;
+  }
+}
+
+// ------------------------------------------------------ exact fp64 helpers
+// The reference evaluates every expression as separately rounded IEEE
+// operations (no contraction).  These intrinsics pin that on the device
+// regardless of --fmad.
+__device__ __forceinline__ double ex_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ex_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double ex_mul(double a, double b) { return __dmul_rn(a, b); }
+
+// clamp_to (pga.cpp:31-34): std::min(1.0, std::max(lo, t)) with the
+// std::max/min tie rules spelled out (signed zeros, NaN behave identically).
+__device__ __forceinline__ double clamp_box(double t, double lo) {
+  const double a = lo < t ? t : lo;
+  return a < 1.0 ? a : 1.0;
+}
+
+// ----------------------------------------------------------------- layout
+// Chains per lane of the fused kernels: 4 (one 32-byte sector of X per
+// lane per neighbour) for B >= 4, else 1.
+inline int chains_per_lane(int B) { return B >= 4 ? 4 : 1; }
+
+// Quads (lane work units) per row, padded so a row group is warp-aligned:
+// a power of two <= 32, or a multiple of 32.
+inline int quads_per_row(int B, int cpl) {
+  int q = (B + cpl - 1) / cpl;
+  if (q >= 32) return (q + 31) / 32 * 32;
+  int p = 1;
+  while (p < q) p <<= 1;
+  return p;
+}
+
+// Per-chain trajectory control word (K2 state).
+struct ChainCtl {
+  int32_t active;
+  int32_t iterations;
+  int32_t reason;
+  int32_t final_buf;
+};
+
+}  // namespace mqo_b200
+
+// ------------------------------------------------------------- handles
+struct mqo_graph {
+  int device = 0;
+  int32_t n = 0;
+  int64_t m = 0;
+  int32_t max_degree = 0;
+  int64_t* d_off = nullptr;   // n+1
+  int32_t* d_nbr = nullptr;   // 2m
+  int32_t* d_order = nullptr; // rows by degree descending (stable by id)
+  std::vector<int64_t> h_off;
+  std::vector<int32_t> h_nbr;
+};
+
+struct mqo_batch {
+  mqo_graph* g = nullptr;
+  int32_t B = 0;    // chains
+  int32_t cpl = 1;  // chains per lane
+  int32_t Q = 1;    // quads (lane units) per row
+  int32_t Bp = 0;   // padded chain stride = Q * cpl
+  cudaStream_t stream = nullptr;
+  double* d_x[2] = {nullptr, nullptr};  // vertex-major [n][Bp], double buffered
+  double* d_v = nullptr;                // [n][Bp]
+  double* d_aux = nullptr;              // [n][Bp] staging / gradient output (lazy)
+  int cur = 0;                          // buffer holding the current x
+  mqo_b200::ChainCtl* d_ctl = nullptr;  // [Bp]
+  uint32_t* d_viol = nullptr;           // [3][Bp] MIS checker accumulators
+  unsigned long long* d_chg = nullptr;  // [3][Bp] max |dx| accumulators (bits)
+  int32_t* d_flag = nullptr;            // misc device flags [4]
+  int32_t* h_flag = nullptr;            // pinned mirror [4]
+  int coop_blocks = 0;                  // resident CTAs for the persistent kernel
+};

@@ -1,0 +1,167 @@
+// graph_build.cu -- host-side graph construction behind the C ABI:
+// Graph::from_edges (graph.cpp:8-42) and the seeded generators
+// (graph.cpp:107-178).  Same algorithms and the same xoshiro draws as the
+// reference, so a (spec, seed) pair yields the identical CSR; the result is
+// uploaded to HBM by mqo_graph_upload.
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+using namespace mqo_b200;
+
+namespace {
+
+// Canonical CSR from (u<v)-normalised packed keys: sort, unique, count,
+// prefix sum, fill, per-row sort (graph.cpp:16-37).
+void csr_from_keys(int32_t n, std::vector<uint64_t>& keys, std::vector<int64_t>& off,
+                   std::vector<int32_t>& nbr) {
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  const int64_t m = static_cast<int64_t>(keys.size());
+  off.assign(static_cast<size_t>(n) + 1, 0);
+  for (uint64_t k : keys) {
+    ++off[(k >> 32) + 1];
+    ++off[(k & 0xffffffffu) + 1];
+  }
+  for (int32_t v = 0; v < n; ++v) off[v + 1] += off[v];
+  nbr.resize(static_cast<size_t>(2 * m));
+  std::vector<int64_t> cursor(off.begin(), off.end() - 1);
+  // keys are sorted by (u, v).  First give every row its smaller
+  // neighbours (for fixed v the keys with second == v arrive in ascending
+  // u), then its larger ones (ascending v for fixed u): each row comes out
+  // strictly ascending without the per-row sort of graph.cpp:35-37.
+  for (uint64_t k : keys) {
+    const int32_t u = static_cast<int32_t>(k >> 32), v = static_cast<int32_t>(k & 0xffffffffu);
+    nbr[cursor[v]++] = u;
+  }
+  for (uint64_t k : keys) {
+    const int32_t u = static_cast<int32_t>(k >> 32), v = static_cast<int32_t>(k & 0xffffffffu);
+    nbr[cursor[u]++] = v;
+  }
+}
+
+inline uint64_t key_of(int32_t u, int32_t v) {
+  if (u > v) std::swap(u, v);
+  return (static_cast<uint64_t>(static_cast<uint32_t>(u)) << 32) | static_cast<uint32_t>(v);
+}
+
+void build_from_edges(int32_t n, int64_t ne, const int32_t* eu, const int32_t* ev,
+                      std::vector<int64_t>& off, std::vector<int32_t>& nbr) {
+  if (n < 0) throw std::invalid_argument("graph: negative vertex count");
+  std::vector<uint64_t> keys(static_cast<size_t>(ne));
+  for (int64_t i = 0; i < ne; ++i) {
+    const int32_t u = eu[i], v = ev[i];
+    if (u < 0 || u >= n || v < 0 || v >= n)
+      throw std::invalid_argument("graph: vertex index out of range");
+    if (u == v) throw std::invalid_argument("graph: self-loop rejected");
+    keys[i] = key_of(u, v);
+  }
+  csr_from_keys(n, keys, off, nbr);
+}
+
+void generate_er(int32_t n, double p, uint64_t seed, std::vector<int64_t>& off,
+                 std::vector<int32_t>& nbr) {  // graph.cpp:107-116
+  if (n < 0) throw std::invalid_argument("er: negative n");
+  if (p < 0.0 || p > 1.0) throw std::invalid_argument("er: p outside [0,1]");
+  Xoshiro r = xoshiro_seed(derive_seed(seed, 0x45521ULL));
+  std::vector<uint64_t> keys;
+  const double expect = 0.5 * static_cast<double>(n) * (n - 1.0) * p;
+  keys.reserve(static_cast<size_t>(expect * 1.05 + 16));
+  for (int32_t u = 0; u < n; ++u)
+    for (int32_t v = u + 1; v < n; ++v)
+      if (u01_of(xoshiro_next(r)) < p) keys.push_back(key_of(u, v));
+  csr_from_keys(n, keys, off, nbr);
+}
+
+void generate_ba(int32_t n, int32_t m_attach, uint64_t seed, std::vector<int64_t>& off,
+                 std::vector<int32_t>& nbr) {  // graph.cpp:118-146
+  if (m_attach < 1) throw std::invalid_argument("ba: m_attach must be >= 1");
+  if (m_attach >= n) throw std::invalid_argument("ba: m_attach must be < n");
+  Xoshiro r = xoshiro_seed(derive_seed(seed, 0xBAULL));
+  std::vector<uint64_t> keys;
+  std::vector<int32_t> endpoints;
+  keys.reserve(static_cast<size_t>(m_attach) * n);
+  endpoints.reserve(static_cast<size_t>(2) * m_attach * n);
+  for (int32_t v = 1; v <= m_attach; ++v) {
+    keys.push_back(key_of(0, v));
+    endpoints.push_back(0);
+    endpoints.push_back(v);
+  }
+  std::vector<int32_t> targets;
+  for (int32_t v = m_attach + 1; v < n; ++v) {
+    targets.clear();
+    while (static_cast<int32_t>(targets.size()) < m_attach) {
+      const int32_t t = endpoints[xoshiro_index(r, endpoints.size())];
+      if (std::find(targets.begin(), targets.end(), t) == targets.end()) targets.push_back(t);
+    }
+    for (int32_t t : targets) {
+      keys.push_back(key_of(t, v));
+      endpoints.push_back(t);
+      endpoints.push_back(v);
+    }
+  }
+  csr_from_keys(n, keys, off, nbr);
+}
+
+void generate_sbm(int32_t n, int32_t k, double p_in, double p_out, uint64_t seed,
+                  std::vector<int64_t>& off, std::vector<int32_t>& nbr) {  // graph.cpp:148-165
+  if (k < 1) throw std::invalid_argument("sbm: k must be >= 1");
+  if (p_in < 0.0 || p_in > 1.0 || p_out < 0.0 || p_out > 1.0)
+    throw std::invalid_argument("sbm: probabilities outside [0,1]");
+  if (p_in <= p_out) throw std::invalid_argument("sbm: requires p_in > p_out");
+  Xoshiro r = xoshiro_seed(derive_seed(seed, 0x5B3ULL));
+  std::vector<uint64_t> keys;
+  for (int32_t u = 0; u < n; ++u) {
+    const int bu = static_cast<int>((static_cast<int64_t>(u) * k) / n);
+    for (int32_t v = u + 1; v < n; ++v) {
+      const int bv = static_cast<int>((static_cast<int64_t>(v) * k) / n);
+      if (u01_of(xoshiro_next(r)) < (bu == bv ? p_in : p_out)) keys.push_back(key_of(u, v));
+    }
+  }
+  csr_from_keys(n, keys, off, nbr);
+}
+
+}  // namespace
+
+extern "C" int mqo_graph_from_edges(int32_t n, int64_t num_edges, const int32_t* eu,
+                                    const int32_t* ev, int32_t device, mqo_graph** out) {
+  std::vector<int64_t> off;
+  std::vector<int32_t> nbr;
+  const int rc = guard([&] {
+    if (num_edges < 0 || (num_edges > 0 && (!eu || !ev)))
+      throw std::invalid_argument("mqo_graph_from_edges: bad edge arrays");
+    build_from_edges(n, num_edges, eu, ev, off, nbr);
+  });
+  if (rc) return rc;
+  return mqo_graph_upload(n, off.data(), nbr.data(), device, out);
+}
+
+extern "C" int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph** out) {
+  std::vector<int64_t> off;
+  std::vector<int32_t> nbr;
+  int32_t n = 0;
+  const int rc = guard([&] {
+    if (!spec) throw std::invalid_argument("mqo_generate: null spec");
+    n = spec->n;
+    switch (spec->kind) {
+      case MQO_GEN_ER: generate_er(spec->n, spec->p, spec->seed, off, nbr); break;
+      case MQO_GEN_BA: generate_ba(spec->n, spec->m_attach, spec->seed, off, nbr); break;
+      case MQO_GEN_SBM:
+        generate_sbm(spec->n, spec->k, spec->p_in, spec->p_out, spec->seed, off, nbr);
+        break;
+      default: throw std::invalid_argument("mqo_generate: unknown generator kind");
+    }
+  });
+  if (rc) return rc;
+  return mqo_graph_upload(n, off.data(), nbr.data(), device, out);
+}
+
+extern "C" int mqo_graph_csr(const mqo_graph* g, int64_t* offsets, int32_t* neighbors) {
+  return guard([&] {
+    if (!g) throw std::invalid_argument("mqo_graph_csr: null graph");
+    if (offsets) std::memcpy(offsets, g->h_off.data(), sizeof(int64_t) * g->h_off.size());
+    if (neighbors) std::memcpy(neighbors, g->h_nbr.data(), sizeof(int32_t) * g->h_nbr.size());
+  });
+}

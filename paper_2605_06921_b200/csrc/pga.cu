@@ -1,0 +1,668 @@
+// pga.cu -- K1 `pga_step_fused` and K2 trajectory control: the hot path.
+//
+// Reference path replaced (relative to /root/reference/proj/core/):
+//   Graph::adjacency_apply / laplacian_apply   graph.cpp:63-88   (the SpMV)
+//   gradient epilogues                         objectives.cpp:101-134
+//   step / run_trajectory loop body            pga.cpp:51-61, 79-88
+//   MIS binarize + mis_fixed_point_check       pga.cpp:91-98, 113-135
+//   MaxCut ||dx||_inf stop, deadline poll      pga.cpp:99-107
+//
+// One pass = one PGA iteration of every active chain.  Work unit = (row v,
+// quad q): a lane owns CPL (4) consecutive chains of row v and gathers
+// X[u][4q..4q+3] (one 32-byte sector) for every neighbour u of v, in CSR
+// order, accumulating each chain sequentially -- the exact summation order
+// of adjacency_apply, so every fp64 result is bit-identical.  Parallelism
+// comes from rows x chains, never from splitting a row's sum.  The MIS
+// fixed-point check of the previous iterate x_{t-1} is fused into the same
+// gather (count of neighbours with x_u > 0.5), so it costs no extra bytes
+// instead of the reference's second SpMV.  The MaxCut max|dx| is reduced
+// per chain in the epilogue.
+//
+// Trajectories run as a cooperative persistent kernel: passes separated by
+// grid.sync(); every CTA takes the (identical, redundant) per-chain stop
+// decision after the barrier, CTA 0 records it.  Per-chain accumulators are
+// triple-buffered by pass so no extra barrier is needed to reset them.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <ctime>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+using namespace mqo_b200;
+
+namespace mqo_b200 {
+double* aux_buffer(mqo_batch* b);
+void upload_chain_major(mqo_batch* b, const double* host, double* dst);
+void download_chain_major(mqo_batch* b, const double* src, double* host);
+void launch_project(mqo_batch* b, double* x, int32_t problem);
+}  // namespace mqo_b200
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+enum Mode : int { kStep = 0, kGrad = 1, kCheck = 2, kTraj = 3 };
+
+struct PassArgs {
+  const int64_t* __restrict__ off;
+  const int32_t* __restrict__ nbr;
+  const int32_t* __restrict__ order;
+  int32_t n, B, Bp, Q;
+  double* x[2];
+  double* v;
+  double* gout;
+  double param, alpha, beta, lo;
+  ChainCtl* ctl;
+  uint32_t* viol;            // [3][Bp]
+  unsigned long long* chg;   // [3][Bp]
+  int32_t* flag;             // [0] active count, [1] non-binary flag
+  int32_t base;              // buffer index holding x_0 (kTraj) / current x
+  int32_t p_begin, p_end;    // passes [p_begin, p_end)
+  int32_t T;                 // last iterate of the trajectory
+  int32_t check_every;
+  double conv_tol;
+  int32_t is_mis;
+};
+
+template <int CPL>
+__device__ __forceinline__ void ldx(const double* p, double (&o)[CPL]) {
+  if constexpr (CPL == 4) {
+    const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x;
+    o[1] = a.y;
+    o[2] = b.x;
+    o[3] = b.y;
+  } else {
+    o[0] = __ldcg(p);
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void stx(double* p, const double (&o)[CPL], unsigned mask) {
+  if constexpr (CPL == 4) {
+    if (mask == 0xF) {
+      __stcg(reinterpret_cast<double2*>(p), make_double2(o[0], o[1]));
+      __stcg(reinterpret_cast<double2*>(p) + 1, make_double2(o[2], o[3]));
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (mask & (1u << c)) __stcg(p + c, o[c]);
+    }
+  } else {
+    if (mask & 1u) __stcg(p, o[0]);
+  }
+}
+
+// Gradient epilogues, objectives.cpp:109-133, operation by operation.
+template <int KIND>
+__device__ __forceinline__ double grad_epi(double acc, double x, double deg, double param) {
+  if constexpr (KIND == MQO_MIS_QUBO) return ex_sub(1.0, ex_mul(param, acc));
+  if constexpr (KIND == MQO_LAPLACIAN) return ex_mul(acc, 0.5);
+  if constexpr (KIND == MQO_PERTURBED_LAPLACIAN)
+    return ex_mul(2.0, ex_add(ex_sub(ex_mul(deg, x), acc), ex_mul(param, x)));
+  if constexpr (KIND == MQO_ADJACENCY) return ex_mul(acc, -2.0);
+  return ex_sub(ex_mul(-2.0, acc), param);  // PerturbedBias
+}
+
+// Per-thread accumulators of one pass (this thread's fixed quad).
+template <int CPL>
+struct Acc {
+  unsigned viol = 0;     // bit c: chain c of the quad violates the MIS check
+  double chg[CPL];       // max |x_new - x_old|
+  unsigned nonbin = 0;   // kCheck: a state not in {0,1}
+  __device__ Acc() {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) chg[c] = 0.0;
+  }
+};
+
+// One (row, quad) work unit.
+template <int KIND, int CPL, int MODE, bool CHECK>
+__device__ __forceinline__ void row_unit(const PassArgs& a, const double* __restrict__ X,
+                                         double* __restrict__ Xo, int32_t v, int32_t col,
+                                         unsigned amask, bool write, Acc<CPL>& acc) {
+  constexpr int U = CPL == 4 ? 8 : 16;
+  const int64_t e0 = __ldg(a.off + v), e1 = __ldg(a.off + v + 1);
+  const int64_t rowbase = static_cast<int64_t>(v) * a.Bp + col;
+  double xv[CPL];
+  ldx<CPL>(X + rowbase, xv);
+  double s[CPL];
+  int cnt[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    s[c] = 0.0;
+    cnt[c] = 0;
+  }
+  for (int64_t e = e0; e < e1; e += U) {
+    int32_t us[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) us[j] = (e + j < e1) ? __ldg(a.nbr + e + j) : -1;
+    double val[U][CPL];
+#pragma unroll
+    for (int j = 0; j < U; ++j)
+      if (us[j] >= 0) ldx<CPL>(X + static_cast<int64_t>(us[j]) * a.Bp + col, val[j]);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (us[j] < 0) break;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        if constexpr (KIND == MQO_LAPLACIAN)
+          s[c] = ex_add(s[c], ex_sub(xv[c], val[j][c]));  // graph.cpp:85
+        else
+          s[c] = ex_add(s[c], val[j][c]);               // graph.cpp:68
+        if constexpr (CHECK) cnt[c] += val[j][c] > 0.5 ? 1 : 0;
+      }
+    }
+  }
+  if constexpr (CHECK) {
+    // pga.cpp:125-133 on binarize(x) (pga.cpp:93): selected vertices must
+    // have no selected neighbour, unselected ones at least one.
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const bool sel = xv[c] > 0.5;
+      const bool bad = sel ? (cnt[c] > 0) : (cnt[c] < 1);
+      if (bad && (amask & (1u << c))) acc.viol |= 1u << c;
+      if constexpr (MODE == kCheck)
+        if (xv[c] != 0.0 && xv[c] != 1.0 && (amask & (1u << c))) acc.nonbin = 1;
+    }
+  }
+  if constexpr (MODE == kCheck) return;
+  const double deg = static_cast<double>(e1 - e0);
+  double g[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) g[c] = grad_epi<KIND>(s[c], xv[c], deg, a.param);
+  if constexpr (MODE == kGrad) {
+    stx<CPL>(a.gout + rowbase, g, amask);
+    return;
+  }
+  if (!write) return;
+  double vv[CPL], xn[CPL];
+  ldx<CPL>(a.v + rowbase, vv);
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    // pga.cpp:82-85: v = beta v + g ; next = clamp(x + alpha v)
+    vv[c] = ex_add(ex_mul(a.beta, vv[c]), g[c]);
+    xn[c] = clamp_box(ex_add(xv[c], ex_mul(a.alpha, vv[c])), a.lo);
+    const double d = fabs(ex_sub(xn[c], xv[c]));
+    acc.chg[c] = acc.chg[c] < d ? d : acc.chg[c];  // std::max(max_change, d)
+  }
+  stx<CPL>(a.v + rowbase, vv, amask);
+  stx<CPL>(Xo + rowbase, xn, amask);
+}
+
+// Walks this thread's (row, quad) units for one pass.  Thread -> quad is
+// fixed for the whole launch so per-chain accumulators live in registers.
+template <int KIND, int CPL, int MODE, bool CHECK>
+__device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, double* Xo,
+                                          const uint8_t* qmask, bool write, Acc<CPL>& acc,
+                                          int32_t& my_q) {
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int32_t q, r0, rstep;
+  if (a.Q >= 32) {
+    const int wpr = a.Q >> 5;
+    q = (gwarp % wpr) * 32 + lane;
+    r0 = gwarp / wpr;
+    rstep = nwarps / wpr;
+  } else {
+    const int rpw = 32 / a.Q;
+    q = lane & (a.Q - 1);
+    r0 = gwarp * rpw + lane / a.Q;
+    rstep = nwarps * rpw;
+  }
+  my_q = q;
+  const int32_t col = q * CPL;
+  unsigned amask;
+  if (qmask) {
+    amask = qmask[q];
+  } else {  // all real chains of the quad (padding chains skipped)
+    const int real = a.B - col;
+    amask = real >= CPL ? (1u << CPL) - 1u : (real > 0 ? (1u << real) - 1u : 0u);
+  }
+  if (!amask) return;
+  for (int32_t r = r0; r < a.n; r += rstep)
+    row_unit<KIND, CPL, MODE, CHECK>(a, X, Xo, __ldg(a.order + r), col, amask, write, acc);
+}
+
+// Folds thread accumulators into shared per-chain slots.
+template <int CPL>
+__device__ __forceinline__ void fold_to_smem(const Acc<CPL>& acc, int32_t q, uint32_t* s_viol,
+                                             unsigned long long* s_chg, bool chg) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    if (acc.viol & (1u << c)) atomicOr(s_viol + q * CPL + c, 1u);
+    if (chg && acc.chg[c] > 0.0)
+      atomicMax(s_chg + q * CPL + c, static_cast<unsigned long long>(__double_as_longlong(acc.chg[c])));
+  }
+}
+
+// Single-pass kernels: step / gradient / fixed-point check.
+template <int KIND, int CPL, int MODE>
+__global__ void __launch_bounds__(kThreads) k_pass(PassArgs a) {
+  constexpr bool CHECK = MODE == kCheck;
+  Acc<CPL> acc;
+  int32_t q = 0;
+  const double* X = a.x[a.base];
+  double* Xo = a.x[a.base];  // kStep updates in place per unit: each unit
+                             // reads its own row + neighbours of the input
+  // kStep must not read rows another unit already updated, so it writes the
+  // other buffer; the host flips `cur` afterwards.
+  if constexpr (MODE == kStep) Xo = a.x[a.base ^ 1];
+  pass_rows<KIND, CPL, MODE, CHECK>(a, X, Xo, nullptr, true, acc, q);
+  if constexpr (CHECK) {
+    if (acc.viol) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        if (acc.viol & (1u << c)) atomicOr(a.viol + q * CPL + c, 1u);
+    }
+    if (acc.nonbin) atomicOr(reinterpret_cast<unsigned*>(a.flag + 1), 1u);
+  }
+}
+
+// Cooperative persistent trajectory kernel (K1 + K2).
+template <int KIND, int CPL>
+__global__ void __launch_bounds__(kThreads) k_traj(PassArgs a) {
+  constexpr bool MIS = KIND == MQO_MIS_QUBO;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned long long smem_u64[];
+  unsigned long long* s_chg = smem_u64;                              // [Bp]
+  uint32_t* s_viol = reinterpret_cast<uint32_t*>(s_chg + a.Bp);       // [Bp]
+  uint8_t* s_active = reinterpret_cast<uint8_t*>(s_viol + a.Bp);      // [Bp]
+  uint8_t* s_qmask = s_active + a.Bp;                                 // [Q]
+  __shared__ int s_count;
+
+  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x)
+    s_active[b] = (b < a.B && a.ctl[b].active) ? 1 : 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < a.Q; q += blockDim.x) {
+    unsigned m = 0;
+    for (int c = 0; c < CPL; ++c) m |= s_active[q * CPL + c] ? (1u << c) : 0u;
+    s_qmask[q] = static_cast<uint8_t>(m);
+  }
+
+  for (int32_t p = a.p_begin; p < a.p_end; ++p) {
+    const int slot = p % 3, next = (p + 1) % 3;
+    if (blockIdx.x == 0)
+      for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+        a.viol[next * a.Bp + b] = 0u;
+        a.chg[next * a.Bp + b] = 0ull;
+      }
+    for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+      s_viol[b] = 0u;
+      s_chg[b] = 0ull;
+    }
+    __syncthreads();
+
+    const double* X = a.x[(a.base + p - 1) & 1];
+    double* Xo = a.x[(a.base + p) & 1];
+    const bool write = !MIS || p <= a.T;  // pass T+1 is check-only (MIS)
+    Acc<CPL> acc;
+    int32_t q = 0;
+    pass_rows<KIND, CPL, kTraj, MIS>(a, X, Xo, s_qmask, write, acc, q);
+    fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
+    __syncthreads();
+    for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+      if (!s_active[b]) continue;
+      if (MIS) {
+        if (s_viol[b]) {
+          uint32_t* gv = a.viol + slot * a.Bp + b;
+          if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
+        }
+      } else if (s_chg[b]) {
+        unsigned long long* gc = a.chg + slot * a.Bp + b;
+        if (*reinterpret_cast<volatile unsigned long long*>(gc) < s_chg[b]) atomicMax(gc, s_chg[b]);
+      }
+    }
+    grid.sync();
+
+    // K2: identical stop decisions in every CTA (pga.cpp:89-102).
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    int local = 0;
+    for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+      if (!s_active[b]) continue;
+      bool stop = false;
+      ChainCtl c;
+      if (MIS) {
+        const int32_t t = p - 1;  // the iterate this pass checked
+        if (t >= 1 && t % a.check_every == 0 && __ldcg(a.viol + slot * a.Bp + b) == 0u) {
+          stop = true;
+          c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
+        }
+      } else {
+        const double ch = __longlong_as_double(
+            static_cast<long long>(__ldcg(a.chg + slot * a.Bp + b)));
+        if (ch <= a.conv_tol) {
+          stop = true;
+          c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
+        }
+      }
+      if (stop) {
+        s_active[b] = 0;
+        if (blockIdx.x == 0) a.ctl[b] = c;
+      } else {
+        ++local;
+      }
+    }
+    if (local) atomicAdd(&s_count, local);
+    __syncthreads();
+    for (int q2 = threadIdx.x; q2 < a.Q; q2 += blockDim.x) {
+      unsigned m = 0;
+      for (int c = 0; c < CPL; ++c) m |= s_active[q2 * CPL + c] ? (1u << c) : 0u;
+      s_qmask[q2] = static_cast<uint8_t>(m);
+    }
+    const int count = s_count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.flag[0] = count;
+    __syncthreads();
+    if (count == 0) break;
+  }
+}
+
+// Chains still running at the end: IterCap at iterate T (pga.cpp:109-110).
+__global__ void k_finalize(ChainCtl* ctl, int32_t B, int32_t T, int32_t base) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  if (ctl[b].active) ctl[b] = ChainCtl{0, T, MQO_ITER_CAP, (base + T) & 1};
+}
+
+__global__ void k_ctl_init(ChainCtl* ctl, int32_t B, int32_t Bp) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < Bp) ctl[b] = ChainCtl{b < B ? 1 : 0, 0, MQO_ITER_CAP, 0};
+}
+
+// Copies each chain's final iterate into buffer `dst` when it ended in the
+// other one.
+__global__ void k_gather_final(double* __restrict__ dst, const double* __restrict__ src,
+                               const ChainCtl* __restrict__ ctl, int32_t dst_index,
+                               int64_t count, int32_t Bp) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int b = static_cast<int>(i % Bp);
+    if (ctl[b].final_buf != dst_index) dst[i] = src[i];
+  }
+}
+
+// ----------------------------------------------------------- dispatch
+
+using PassFn = void (*)(PassArgs);
+
+template <int MODE>
+PassFn pass_fn(int kind, int cpl) {
+#define MQO_K(K)                                              \
+  case K:                                                     \
+    return cpl == 4 ? k_pass<K, 4, MODE> : k_pass<K, 1, MODE>;
+  switch (kind) {
+    MQO_K(MQO_MIS_QUBO)
+    MQO_K(MQO_LAPLACIAN)
+    MQO_K(MQO_PERTURBED_LAPLACIAN)
+    MQO_K(MQO_ADJACENCY)
+    MQO_K(MQO_PERTURBED_BIAS)
+  }
+#undef MQO_K
+  throw std::invalid_argument("objective: unknown kind");
+}
+
+PassFn traj_fn(int kind, int cpl) {
+#define MQO_K(K) \
+  case K:        \
+    return cpl == 4 ? k_traj<K, 4> : k_traj<K, 1>;
+  switch (kind) {
+    MQO_K(MQO_MIS_QUBO)
+    MQO_K(MQO_LAPLACIAN)
+    MQO_K(MQO_PERTURBED_LAPLACIAN)
+    MQO_K(MQO_ADJACENCY)
+    MQO_K(MQO_PERTURBED_BIAS)
+  }
+#undef MQO_K
+  throw std::invalid_argument("objective: unknown kind");
+}
+
+int sm_count(int device) {
+  static int cached[64] = {0};
+  if (!cached[device]) MQO_CUDA(cudaDeviceGetAttribute(&cached[device], cudaDevAttrMultiProcessorCount, device));
+  return cached[device];
+}
+
+// Warps needed so every (row, quad) unit has a thread.
+int64_t warp_tasks(const mqo_batch* b) {
+  const int64_t n = b->g->n;
+  if (b->Q >= 32) return n * (b->Q / 32);
+  const int rpw = 32 / b->Q;
+  return (n + rpw - 1) / rpw;
+}
+
+// A row spans wpr = Q/32 warps; the thread -> quad map stays fixed only if
+// the total warp count is a multiple of wpr.
+int align_blocks(const mqo_batch* b, int64_t blocks) {
+  const int wpr = b->Q >= 32 ? b->Q / 32 : 1;
+  if (wpr > kWarps) {
+    const int per = wpr / kWarps;
+    blocks = std::max<int64_t>(per, blocks / per * per);
+  }
+  return static_cast<int>(blocks);
+}
+
+int pass_blocks(const mqo_batch* b) {
+  const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
+  // ~8 resident CTAs of 256 threads per SM is the register-limited ceiling;
+  // keep the grid a multiple of the SM count worth of waves.
+  const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * 8;
+  return align_blocks(b, std::max<int64_t>(1, std::min(need, cap)));
+}
+
+void validate_objective(const mqo_objective& o) {  // objectives.cpp:27-38
+  if (o.kind < 0 || o.kind > 4) throw std::invalid_argument("objective: unknown kind");
+  if (o.kind == MQO_MIS_QUBO && !(o.param > 1.0))
+    throw std::invalid_argument("mis-qubo: gamma must be > 1");
+  if (o.kind == MQO_PERTURBED_LAPLACIAN && !(o.param > 0.0))
+    throw std::invalid_argument("perturbed-laplacian: lambda must be > 0");
+  if (o.kind == MQO_PERTURBED_BIAS && !(o.param > 0.0 && o.param < 2.0))
+    throw std::invalid_argument("perturbed-bias: lambda must be in (0, 2)");
+}
+
+void validate_optimizer(const mqo_optimizer& c) {  // pga.cpp:9-18
+  if (!(c.alpha > 0.0)) throw std::invalid_argument("optimizer: alpha must be > 0");
+  if (c.beta < 0.0 || c.beta >= 1.0) throw std::invalid_argument("optimizer: beta must be in [0, 1)");
+  if (c.max_iters < 1) throw std::invalid_argument("optimizer: max_iters must be >= 1");
+  if (c.conv_tol < 0.0) throw std::invalid_argument("optimizer: conv_tol must be >= 0");
+  if (c.check_every < 1) throw std::invalid_argument("optimizer: check_every must be >= 1");
+}
+
+PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
+  PassArgs a{};
+  const mqo_graph* g = b->g;
+  a.off = g->d_off;
+  a.nbr = g->d_nbr;
+  a.order = g->d_order;
+  a.n = g->n;
+  a.B = b->B;
+  a.Bp = b->Bp;
+  a.Q = b->Q;
+  a.x[0] = b->d_x[0];
+  a.x[1] = b->d_x[1];
+  a.v = b->d_v;
+  a.param = obj.param;
+  a.lo = obj.kind == MQO_MIS_QUBO ? 0.0 : -1.0;
+  a.ctl = b->d_ctl;
+  a.viol = b->d_viol;
+  a.chg = b->d_chg;
+  a.flag = b->d_flag;
+  a.base = b->cur;
+  a.is_mis = obj.kind == MQO_MIS_QUBO;
+  return a;
+}
+
+double now_monotonic() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<double>(ts.tv_sec) + 1e-9 * static_cast<double>(ts.tv_nsec);
+}
+
+}  // namespace
+
+namespace mqo_b200 {
+
+// Enqueues one fused step on the batch stream (used by mqo_step and the
+// engine); flips the current buffer.
+void launch_step(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt) {
+  PassArgs a = make_args(b, obj);
+  a.alpha = opt.alpha;
+  a.beta = opt.beta;
+  if (b->g->n == 0) return;
+  pass_fn<kStep>(obj.kind, b->cpl)<<<pass_blocks(b), kThreads, 0, b->stream>>>(a);
+  MQO_CUDA(cudaGetLastError());
+  b->cur ^= 1;
+}
+
+// Runs trajectories of every chain from the current x (already projected
+// by the caller when required).  Returns with ctl[] filled and the final
+// states gathered into buffer b->cur.
+void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt,
+                      double deadline) {
+  mqo_graph* g = b->g;
+  const bool mis = obj.kind == MQO_MIS_QUBO;
+  k_ctl_init<<<(b->Bp + 255) / 256, 256, 0, b->stream>>>(b->d_ctl, b->B, b->Bp);
+  MQO_CUDA(cudaMemsetAsync(b->d_v, 0, sizeof(double) * int64_t(g->n) * b->Bp, b->stream));
+  int32_t T = opt.max_iters;
+  if (g->n == 0) {
+    k_finalize<<<(b->B + 255) / 256, 256, 0, b->stream>>>(b->d_ctl, b->B, T, b->cur);
+    return;
+  }
+  PassArgs a = make_args(b, obj);
+  a.alpha = opt.alpha;
+  a.beta = opt.beta;
+  a.check_every = opt.check_every;
+  a.conv_tol = opt.conv_tol;
+  a.T = T;
+
+  PassFn fn = traj_fn(obj.kind, b->cpl);
+  const size_t smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
+  int per_sm = 0;
+  MQO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn),
+                                                         kThreads, smem));
+  if (per_sm < 1) throw std::logic_error("trajectory kernel cannot be resident");
+  const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
+  const int blocks = align_blocks(
+      b, std::max<int64_t>(1, std::min<int64_t>(need, int64_t(per_sm) * sm_count(g->device))));
+
+  int32_t last = mis ? T + 1 : T;  // MIS needs one check-only pass for x_T
+  int32_t p = 1;
+  while (p <= last) {
+    // Chunks end on multiples of 256 so the deadline is polled where the
+    // reference polls it ((iter & 255) == 0, pga.cpp:104-107).
+    const int32_t chunk_end = std::min<int32_t>(last + 1, (p / 256 + 1) * 256 + 1);
+    MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * 3 * b->Bp, b->stream));
+    MQO_CUDA(cudaMemsetAsync(b->d_chg, 0, sizeof(unsigned long long) * 3 * b->Bp, b->stream));
+    a.p_begin = p;
+    a.p_end = chunk_end;
+    a.T = T;
+    void* args[] = {&a};
+    MQO_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), blocks, kThreads,
+                                         args, smem, b->stream));
+    MQO_CUDA(cudaMemcpyAsync(b->h_flag, b->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             b->stream));
+    MQO_CUDA(cudaStreamSynchronize(b->stream));
+    if (b->h_flag[0] == 0) break;
+    const int32_t done = chunk_end - 1;  // passes completed
+    if (deadline >= 0.0 && done <= T && (done & 255) == 0 && done < T &&
+        now_monotonic() >= deadline) {
+      T = done;  // IterCap at this iterate after (MIS) checking it
+      last = mis ? T + 1 : T;
+    }
+    p = chunk_end;
+  }
+  k_finalize<<<(b->B + 255) / 256, 256, 0, b->stream>>>(b->d_ctl, b->B, T, b->cur);
+  MQO_CUDA(cudaGetLastError());
+  // Gather every chain's final iterate into one buffer.
+  const int dst = (b->cur + T) & 1;
+  const int64_t count = int64_t(g->n) * b->Bp;
+  k_gather_final<<<std::min<int64_t>((count + 255) / 256, 148 * 32), 256, 0, b->stream>>>(
+      b->d_x[dst], b->d_x[dst ^ 1], b->d_ctl, dst, count, b->Bp);
+  MQO_CUDA(cudaGetLastError());
+  b->cur = dst;
+}
+
+void read_outcomes(mqo_batch* b, int32_t* iterations, int32_t* reasons) {
+  std::vector<ChainCtl> ctl(b->B);
+  MQO_CUDA(cudaMemcpyAsync(ctl.data(), b->d_ctl, sizeof(ChainCtl) * b->B, cudaMemcpyDeviceToHost,
+                           b->stream));
+  MQO_CUDA(cudaStreamSynchronize(b->stream));
+  for (int i = 0; i < b->B; ++i) {
+    if (iterations) iterations[i] = ctl[i].iterations;
+    if (reasons) reasons[i] = ctl[i].reason;
+  }
+}
+
+}  // namespace mqo_b200
+
+extern "C" int mqo_step(mqo_batch* b, const mqo_objective* obj, const mqo_optimizer* opt) {
+  return guard([&] {
+    if (!b || !obj || !opt) throw std::invalid_argument("mqo_step: null argument");
+    validate_objective(*obj);
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    launch_step(b, *obj, *opt);
+  });
+}
+
+extern "C" int mqo_gradient(mqo_batch* b, const mqo_objective* obj, double* out) {
+  return guard([&] {
+    if (!b || !obj || !out) throw std::invalid_argument("mqo_gradient: null argument");
+    validate_objective(*obj);
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    if (b->g->n == 0) return;
+    PassArgs a = make_args(b, *obj);
+    // gradient output goes to the idle X buffer, then out through aux
+    a.gout = b->d_x[b->cur ^ 1];
+    pass_fn<kGrad>(obj->kind, b->cpl)<<<pass_blocks(b), kThreads, 0, b->stream>>>(a);
+    MQO_CUDA(cudaGetLastError());
+    download_chain_major(b, a.gout, out);
+  });
+}
+
+extern "C" int mqo_run_trajectories(mqo_batch* b, const mqo_objective* obj,
+                                    const mqo_optimizer* opt, double deadline_secs,
+                                    int32_t* iterations, int32_t* reasons) {
+  return guard([&] {
+    if (!b || !obj || !opt) throw std::invalid_argument("mqo_run_trajectories: null argument");
+    validate_optimizer(*opt);  // run_trajectory validates cfg (pga.cpp:65)
+    if (obj->kind < 0 || obj->kind > 4) throw std::invalid_argument("objective: unknown kind");
+    if (obj->kind == MQO_MIS_QUBO && !(obj->param > 1.0))
+      throw std::invalid_argument("mis_fixed_point_check: gamma must be > 1");
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    launch_project(b, b->d_x[b->cur], obj->kind == MQO_MIS_QUBO ? MQO_PROBLEM_MIS
+                                                                 : MQO_PROBLEM_MAXCUT);
+    run_trajectories(b, *obj, *opt, deadline_secs);
+    read_outcomes(b, iterations, reasons);
+  });
+}
+
+extern "C" int mqo_mis_fixed_point_check(mqo_batch* b, double gamma, double alpha,
+                                         int32_t* fixed) {
+  return guard([&] {
+    if (!b || !fixed) throw std::invalid_argument("mqo_mis_fixed_point_check: null argument");
+    if (!(gamma > 1.0)) throw std::invalid_argument("mis_fixed_point_check: gamma must be > 1");
+    if (!(alpha > 0.0)) throw std::invalid_argument("mis_fixed_point_check: alpha must be > 0");
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * b->Bp, b->stream));
+    MQO_CUDA(cudaMemsetAsync(b->d_flag, 0, sizeof(int32_t) * 4, b->stream));
+    if (b->g->n) {
+      PassArgs a = make_args(b, mqo_objective{MQO_MIS_QUBO, gamma});
+      pass_fn<kCheck>(MQO_MIS_QUBO, b->cpl)<<<pass_blocks(b), kThreads, 0, b->stream>>>(a);
+      MQO_CUDA(cudaGetLastError());
+    }
+    std::vector<uint32_t> viol(b->Bp);
+    MQO_CUDA(cudaMemcpyAsync(viol.data(), b->d_viol, sizeof(uint32_t) * b->Bp,
+                             cudaMemcpyDeviceToHost, b->stream));
+    MQO_CUDA(cudaMemcpyAsync(b->h_flag, b->d_flag, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost,
+                             b->stream));
+    MQO_CUDA(cudaStreamSynchronize(b->stream));
+    if (b->h_flag[1]) throw std::invalid_argument("mis_fixed_point_check: state not binary");
+    for (int i = 0; i < b->B; ++i) fixed[i] = viol[i] ? 0 : 1;
+  });
+}

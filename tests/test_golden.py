@@ -1,0 +1,200 @@
+"""Pins the plain-C oracle against golden vectors produced by the reference
+itself (tests/golden/make_golden.py runs oracle/_ref), plus the reference's
+own recorded acceptance output (proj/test_output.txt:34,43).  Also checks the
+product's host-side graph builders (no GPU: device=-1) against the same
+goldens.  CPU only."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from oracle import (ADJACENCY, LAPLACIAN, MIS_QUBO, PERTURBED_BIAS, PERTURBED_LAPLACIAN)
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+KSEED = 20250801
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"), allow_pickle=False)
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def test_rng_streams(O):
+    z = load("rng")
+    for seed in (1, KSEED):
+        for b in range(1, 5):
+            r = O.rng(O.derive_seed(seed, b))
+            got = np.array([r.next_u64() for _ in range(256)], np.uint64)
+            assert (got == z[f"u64_{seed}_{b}"]).all()
+    r = O.rng(7)
+    got = np.array([r.normal(0.0, 1.0) for _ in range(257)])
+    assert (got.view(np.uint64) == z["normal_7"].view(np.uint64)).all()
+    r = O.rng(11)
+    got = np.array([r.uniform_index(n) for n in range(1, 300)], np.uint64)
+    assert (got == z["index_11"]).all()
+
+
+SPECS = {"er1000": ("er", 1000, 0.01, 1), "er2000": ("er", 2000, 6 / 2000, 1),
+         "ba10000": ("ba", 10000, 5, 1), "sbm300": ("sbm", 300, 3, 0.2, 0.01, 4),
+         "er100": ("er", 100, 0.0166, 2400)}
+
+
+def _gen(L, s):
+    if s[0] == "er":
+        return L.generate_er(s[1], s[2], s[3])
+    if s[0] == "ba":
+        return L.generate_ba(s[1], s[2], s[3])
+    return L.generate_sbm(*s[1:])
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_generators_oracle(O, name):
+    z = load("graphs")
+    g = _gen(O, SPECS[name])
+    off, nbr = g.csr()
+    assert [g.n, g.m, g.max_degree] == z[f"{name}_nm"].tolist()
+    assert sha(off, nbr) == str(z[f"{name}_sha"])
+
+
+@pytest.mark.parametrize("name", list(SPECS))
+def test_generators_product_host(name):
+    """The product's own C++ generators (graph_build.cu), host-only graph."""
+    from paper_2605_06921_b200 import BaSpec, ErSpec, SbmSpec, generate
+    z = load("graphs")
+    s = SPECS[name]
+    spec = {"er": lambda: ErSpec(s[1], s[2]), "ba": lambda: BaSpec(s[1], s[2]),
+            "sbm": lambda: SbmSpec(*s[1:5])}[s[0]]()
+    g = generate(spec, s[-1], device=-1)
+    off, nbr = g.csr()
+    assert [g.n(), g.m(), g.max_degree()] == z[f"{name}_nm"].tolist()
+    assert sha(off, nbr) == str(z[f"{name}_sha"])
+
+
+def test_from_edges_product_host():
+    from paper_2605_06921_b200 import Graph, InvalidArgument
+    z = load("graphs")
+    off, nbr = z["er1000_off"], z["er1000_nbr"]
+    edges = [(v, int(u)) for v in range(1000) for u in nbr[off[v]:off[v + 1]]]
+    rng = np.random.default_rng(3)
+    rng.shuffle(edges)
+    g = Graph.from_edges(1000, edges, device=-1)  # both orientations + shuffled
+    o2, n2 = g.csr()
+    assert (o2 == off).all() and (n2 == nbr).all()
+    with pytest.raises(InvalidArgument, match="self-loop"):
+        Graph.from_edges(3, [(1, 1)], device=-1)
+    with pytest.raises(InvalidArgument, match="out of range"):
+        Graph.from_edges(3, [(0, 3)], device=-1)
+
+
+def test_steps_and_trajectories(O):
+    z = load("steps")
+    g1 = O.generate_er(1000, 0.01, 1)
+    g2 = O.generate_er(2000, 6 / 2000, 1)
+    for gname, g, kinds in (("c1", g1, [(MIS_QUBO, 2.0)]),
+                            ("c2", g2, [(PERTURBED_BIAS, 0.001), (LAPLACIAN, 0.0),
+                                        (PERTURBED_LAPLACIAN, 0.001), (ADJACENCY, 0.0)])):
+        for kind, param in kinds:
+            x0 = z[f"{gname}_k{kind}_x0"]
+            gr = O.gradient(g, kind, param, x0)
+            assert (gr.view(np.uint64) == z[f"{gname}_k{kind}_grad"].view(np.uint64)).all()
+            alpha, beta = (0.8, 0.3) if kind == MIS_QUBO else (0.0025, 0.8)
+            x, v = x0.copy(), np.zeros(g.n)
+            for t in range(1, 101):
+                x, v = O.step(g, kind, param, x, v, alpha, beta)
+                if t in (1, 10, 100):
+                    assert (x.view(np.uint64) == z[f"{gname}_k{kind}_x{t}"].view(np.uint64)).all()
+                    assert (v.view(np.uint64) == z[f"{gname}_k{kind}_v{t}"].view(np.uint64)).all()
+            xt, it, rs = O.run_trajectory(g, kind, param, x0, alpha, beta)
+            assert [it, rs] == z[f"{gname}_k{kind}_traj_ir"].tolist()
+            assert (xt.view(np.uint64) == z[f"{gname}_k{kind}_traj"].view(np.uint64)).all()
+
+
+def test_solver_pieces(O):
+    z = load("pieces")
+    g1 = O.generate_er(1000, 0.01, 1)
+    g2 = O.generate_er(2000, 6 / 2000, 1)
+    for sig in (0.0, 0.15):
+        r = O.rng(O.derive_seed(1, 1))
+        x = O.init_state(g1, 0, sig, r)
+        assert (x.view(np.uint64) == z[f"init_mis_{sig}"].view(np.uint64)).all()
+        assert r.next_u64() == int(z[f"init_mis_{sig}_next"][0])
+        r = O.rng(O.derive_seed(1, 2))
+        x = O.init_state(g2, 1, sig, r)
+        assert (x.view(np.uint64) == z[f"init_cut_{sig}"].view(np.uint64)).all()
+    for n in (1000, 2001, 100000):
+        for rho in (0.5, 0.6, 0.8):
+            r = O.rng(O.derive_seed(n, int(rho * 10)))
+            x, chosen = O.global_reset(np.ones(n), rho, r)
+            key = f"reset_{n}_{rho}"
+            assert sha(chosen) == str(z[key + "_sha"])
+            assert r.next_u64() == int(z[key + "_next"][0])
+            assert (x == 0).sum() == int(np.floor(rho * n))
+    zs = load("steps")
+    body, score = O.extract_solution(g1, 0, zs["c1_k0_traj"])
+    assert (body == z["c1_harvest"]).all() and score == int(z["c1_harvest_score"][0])
+    assert O.is_independent(g1, body) == bool(z["c1_independent"][0])
+    ind, _ = O.greedy_maximalize(g1, body)
+    assert (ind == z["c1_greedy"]).all()
+    assert (O.one_two_swap(g1, ind)[0] == z["c1_swap"]).all()
+    ind, _ = O.greedy_maximalize(g1, np.zeros(1000, np.uint8))
+    assert (ind == z["c1_greedy_empty"]).all()
+    assert (O.one_two_swap(g1, ind)[0] == z["c1_swap_empty"]).all()
+    body, score = O.extract_solution(g2, 1, zs["c2_k4_traj"])
+    assert (body == z["c2_harvest"]).all() and score == int(z["c2_harvest_score"][0])
+    assert (O.build_gain_table(g2, body) == z["c2_tight"]).all()
+    s1, a = O.one_flip_pass(g2, body)
+    s2, b = O.two_flip_pass(g2, body)
+    s3, c = O.one_two_flip(g2, body)
+    assert (s1 == z["c2_oneflip"]).all() and (s2 == z["c2_twoflip"]).all()
+    assert (s3 == z["c2_onetwo"]).all() and [a, b, c] == z["c2_gains"].tolist()
+
+
+def test_acceptance_criterion5_recorded_output(O):
+    """proj/test_output.txt:34,43 -- the reference's recorded means 39.800
+    (f_P) and 70.600 (f_B) on the criterion-5 graphs."""
+    z = load("reports")
+    cuts = {PERTURBED_LAPLACIAN: [], PERTURBED_BIAS: [], LAPLACIAN: []}
+    for gi in range(10):
+        g = O.generate_er(100, 1.66 / 100.0, O.derive_seed(KSEED, 2400 + gi))
+        c = -1.0 + 2.0 * O.rng(O.derive_seed(KSEED, 2500 + gi)).uniform01()
+        for kind in cuts:
+            x, it, rs = O.run_trajectory(g, kind, 0.001, np.full(g.n, c), 0.1, 0.0)
+            cuts[kind].append(O.extract_solution(g, 1, x)[1])
+    for kind in cuts:
+        assert cuts[kind] == z[f"crit5_k{kind}"].tolist()
+    assert np.mean(cuts[PERTURBED_LAPLACIAN]) == pytest.approx(39.8)
+    assert np.mean(cuts[PERTURBED_BIAS]) == pytest.approx(70.6)
+    assert cuts[LAPLACIAN] == [0] * 10
+
+
+def _cfg(name):
+    if name == "c1_s1":
+        return orc.Cfg(objective=MIS_QUBO, param=2.0, alpha=0.8, beta=0.3, reset_fraction=0.7,
+                       reset_rounds=60, seed=1, time_budget_secs=600, max_outer_loops=1)
+    if name == "c1_s2_b4":
+        return orc.Cfg(objective=MIS_QUBO, param=2.0, alpha=0.8, beta=0.3, reset_fraction=0.7,
+                       reset_rounds=10, seed=2, time_budget_secs=600, max_outer_loops=2,
+                       pool_batch=4, pool_keep=3)
+    return orc.Cfg(objective=PERTURBED_BIAS, param=0.001, alpha=0.0025, beta=0.8,
+                   reset_fraction=0.8, reset_rounds=6, seed=1, time_budget_secs=600,
+                   max_outer_loops=1, pool_batch=4, pool_keep=3, max_iters=2000)
+
+
+@pytest.mark.parametrize("name", ["c1_s1", "c1_s2_b4", "c2_s1_b4"])
+def test_engine_reports(O, name):
+    z = load("reports")
+    g = {"c1_s1": lambda: O.generate_er(1000, 0.01, 1),
+         "c1_s2_b4": lambda: O.generate_er(1000, 0.01, 2),
+         "c2_s1_b4": lambda: O.generate_er(2000, 6 / 2000, 1)}[name]()
+    rep, body = O.solve_pooled(g, _cfg(name).to_c())
+    keys = [str(k) for k in z["report_keys"]]
+    assert [rep[k] for k in keys] == z[name + "_report"].tolist()
+    assert (body == z[name + "_body"]).all()
