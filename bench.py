@@ -88,6 +88,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()  # nvidia-smi needs a moment before its first row
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.05)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -257,7 +261,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     traffic = load_traffic()
 
     # e2e through the C-ABI with pinned host buffers
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = 3
     hx = torch.empty((B, n), dtype=torch.float64, pin_memory=True)
     hx.numpy()[:] = X
     hout = torch.empty((B, n), dtype=torch.float64, pin_memory=True)
@@ -329,10 +333,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--cpu-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

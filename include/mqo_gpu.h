@@ -161,6 +161,53 @@ int mqo_run_trajectories(mqo_batch* b, const mqo_objective* obj, const mqo_optim
  * range. */
 int mqo_mis_fixed_point_check(mqo_batch* b, double gamma, double alpha, int32_t* fixed);
 
+/* ---- per-chain random streams (rng.hpp:13-86) ---------------------------
+ * The complete state of an mqo::Rng: xoshiro256** words plus the cached
+ * Box-Muller spare.  Chain b of a batch owns one stream. */
+typedef struct {
+  uint64_t s[4];
+  double spare;
+  int32_t has_spare;
+  int32_t flags; /* internal */
+} mqo_rng_state;
+/* Chain b <- Rng(derive_seed(master_seed, first_stream + b)); the solver
+ * uses first_stream = 1 (solver.cpp:234-236). */
+int mqo_batch_seed_streams(mqo_batch* b, uint64_t master_seed, uint64_t first_stream);
+int mqo_batch_get_streams(mqo_batch* b, mqo_rng_state* out);
+int mqo_batch_set_streams(mqo_batch* b, const mqo_rng_state* in);
+
+/* ---- K3 init_state (solver.cpp:30-46) ----------------------------------
+ * x_b = Pi(d_base + N(0, sigma^2)) drawn from chain b's stream in vertex
+ * order (Box-Muller, rng.hpp:49-62), replayed segment-parallel on the
+ * device.  sigma == 0 draws nothing.  Box-Muller's log/sin/cos come from
+ * CUDA's libm: within 1 ulp of glibc, not bit-identical. */
+int mqo_init_states(mqo_batch* b, int32_t problem, double sigma);
+/* The init_constant path (solver.cpp:283-287): x = Pi(c 1), no draws. */
+int mqo_init_constant(mqo_batch* b, int32_t problem, double c);
+
+/* ---- K4 conditional reset -----------------------------------------------
+ * global_reset (solver.cpp:48-63) on every chain's current x: zeroes the
+ * floor(rho n) coordinates a partial Fisher-Yates over chain b's stream
+ * picks -- bit-identical draws and chosen sets, resolved in parallel. */
+int mqo_global_reset(mqo_batch* b, double rho);
+/* The device copy of the TopK pool: `count` packed bodies of
+ * ceil(n/64) words each (bit 63-(v%64) of word v/64 = vertex v). */
+int mqo_set_pool(mqo_batch* b, int32_t count, const uint64_t* packed);
+/* One reset round start (solver.cpp:301-303): chain b draws
+ * pool.at(uniform_index(pool.size())), encodes it (encode_solution,
+ * solver.cpp:147-160) and applies global_reset.  picks[b] (may be NULL)
+ * receives the drawn pool index. */
+int mqo_reset_from_pool(mqo_batch* b, int32_t problem, double rho, int32_t* picks);
+
+/* ---- K5/K6 harvest (solver.cpp:166-175) ---------------------------------
+ * extract_solution (objectives.cpp:143-161) of every chain's current x;
+ * MIS: is_independent (173-180) -> valid[b] = 0 when dependent (the
+ * reference discards it), else greedy_maximalize (localsearch.cpp:35-56);
+ * MaxCut: cut_value (163-171).  scores[b], valid[b] and the packed bodies
+ * [chains][ceil(n/64)] (each may be NULL) are written to host memory. */
+int mqo_harvest(mqo_batch* b, int32_t problem, int64_t* scores, int32_t* valid,
+                uint64_t* packed);
+
 #ifdef __cplusplus
 }
 #endif

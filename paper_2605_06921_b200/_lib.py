@@ -74,7 +74,19 @@ SIGNATURES: dict[str, tuple] = {
     "mqo_run_trajectories": (C.c_int, [_P, C.POINTER(Objective), C.POINTER(Optimizer),
                                        C.c_double, _I32, _I32]),
     "mqo_mis_fixed_point_check": (C.c_int, [_P, C.c_double, C.c_double, _I32]),
+    "mqo_batch_seed_streams": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
+    "mqo_batch_get_streams": (C.c_int, [_P, _P]),
+    "mqo_batch_set_streams": (C.c_int, [_P, _P]),
+    "mqo_init_states": (C.c_int, [_P, C.c_int32, C.c_double]),
+    "mqo_init_constant": (C.c_int, [_P, C.c_int32, C.c_double]),
+    "mqo_global_reset": (C.c_int, [_P, C.c_double]),
+    "mqo_set_pool": (C.c_int, [_P, C.c_int32, _U64]),
+    "mqo_reset_from_pool": (C.c_int, [_P, C.c_int32, C.c_double, _I32]),
+    "mqo_harvest": (C.c_int, [_P, C.c_int32, _I64, _I32, _U64]),
 }
+
+# mqo_rng_state as a numpy structured dtype (48 bytes)
+RNG_DTYPE = [("s", "<u8", (4,)), ("spare", "<f8"), ("has_spare", "<i4"), ("flags", "<i4")]
 
 
 def _load() -> C.CDLL:

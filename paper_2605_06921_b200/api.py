@@ -28,6 +28,7 @@ __all__ = [
     "Graph", "ErSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
+    "pack_bodies", "unpack_bodies",
     "InvalidArgument", "LogicError", "MqoError",
 ]
 
@@ -312,6 +313,67 @@ class ChainBatch:
         f = np.zeros(self.chains, np.int32)
         check(lib.mqo_mis_fixed_point_check(self._h, gamma, alpha, _ptr(f, _I32)))
         return f.astype(bool)
+
+    # -- streams, init, reset, harvest (solver.cpp) ------------------------
+    def seed_streams(self, master_seed: int, first_stream: int = 1) -> None:
+        """chain b <- Rng(derive_seed(master_seed, first_stream + b))."""
+        check(lib.mqo_batch_seed_streams(self._h, master_seed, first_stream))
+
+    def get_streams(self) -> np.ndarray:
+        out = np.zeros(self.chains, dtype=_lib.RNG_DTYPE)
+        check(lib.mqo_batch_get_streams(self._h, out.ctypes.data))
+        return out
+
+    def set_streams(self, states: np.ndarray) -> None:
+        st = np.ascontiguousarray(states, dtype=_lib.RNG_DTYPE)
+        check(lib.mqo_batch_set_streams(self._h, st.ctypes.data))
+
+    def init_states(self, problem: int, sigma: float) -> None:
+        check(lib.mqo_init_states(self._h, problem, sigma))
+
+    def init_constant(self, problem: int, c: float) -> None:
+        check(lib.mqo_init_constant(self._h, problem, c))
+
+    def global_reset(self, rho: float) -> None:
+        check(lib.mqo_global_reset(self._h, rho))
+
+    def set_pool(self, packed: np.ndarray) -> None:
+        p = np.ascontiguousarray(packed, dtype=np.uint64)
+        check(lib.mqo_set_pool(self._h, p.shape[0], _ptr(p, C.POINTER(C.c_uint64))))
+
+    def reset_from_pool(self, problem: int, rho: float) -> np.ndarray:
+        picks = np.zeros(self.chains, np.int32)
+        check(lib.mqo_reset_from_pool(self._h, problem, rho, _ptr(picks, _I32)))
+        return picks
+
+    def harvest(self, problem: int):
+        """-> scores int64[B], valid bool[B], packed bodies uint64[B][W]."""
+        W = (self.g.n() + 63) // 64
+        scores = np.zeros(self.chains, np.int64)
+        valid = np.zeros(self.chains, np.int32)
+        packed = np.zeros((self.chains, max(W, 1)), np.uint64)
+        check(lib.mqo_harvest(self._h, problem, _ptr(scores, _I64), _ptr(valid, _I32),
+                              _ptr(packed, C.POINTER(C.c_uint64))))
+        return scores, valid.astype(bool), packed[:, :W]
+
+
+def pack_bodies(bodies: np.ndarray) -> np.ndarray:
+    """uint8 [B][n] 0/1 -> packed uint64 [B][ceil(n/64)], vertex v at bit
+    63-(v%64) of word v//64 (word order = lexicographic body order)."""
+    b = np.atleast_2d(np.asarray(bodies, np.uint8))
+    B, n = b.shape
+    W = (n + 63) // 64
+    pad = np.zeros((B, W * 64), np.uint8)
+    pad[:, :n] = b
+    bits = np.packbits(pad.reshape(B, W, 64), axis=2, bitorder="big")  # [B][W][8] bytes
+    return bits.view(">u8").reshape(B, W).astype(np.uint64)
+
+
+def unpack_bodies(packed: np.ndarray, n: int) -> np.ndarray:
+    p = np.atleast_2d(np.asarray(packed, np.uint64))
+    B, W = p.shape
+    by = p.astype(">u8").view(np.uint8).reshape(B, W, 8)
+    return np.unpackbits(by, axis=2, bitorder="big").reshape(B, W * 64)[:, :n].copy()
 
 
 # ------------------------------------------- single-chain reference calls

@@ -88,6 +88,8 @@ void download_chain_major(mqo_batch* b, const double* src, double* host) {
   MQO_CUDA(cudaStreamSynchronize(b->stream));
 }
 
+void free_solver_buffers(mqo_batch* b);
+
 void launch_project(mqo_batch* b, double* x, int32_t problem) {
   const int64_t count = static_cast<int64_t>(b->g->n) * b->Bp;
   if (!count) return;
@@ -145,6 +147,7 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
     cudaFree(b->d_viol);
     cudaFree(b->d_chg);
     cudaFree(b->d_flag);
+    free_solver_buffers(b);
     if (b->h_flag) cudaFreeHost(b->h_flag);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;

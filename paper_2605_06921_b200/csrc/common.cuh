@@ -88,6 +88,19 @@ struct ChainCtl {
   int32_t final_buf;
 };
 
+// Per-chain random stream: the full state of an mqo::Rng (rng.hpp:64-69),
+// xoshiro words + the cached Box-Muller spare.  Layout == mqo_rng_state.
+struct ChainRng {
+  uint64_t s[4];
+  double spare;
+  int32_t has_spare;
+  int32_t flags;  // bit 0: a rejection happened in the last parallel replay
+};
+
+// Packed solution bodies: vertex v is bit 63-(v&63) of word v>>6, so that
+// comparing words as unsigned integers compares bodies lexicographically.
+inline int64_t body_words(int32_t n) { return (static_cast<int64_t>(n) + 63) / 64; }
+
 }  // namespace mqo_b200
 
 // ------------------------------------------------------------- handles
@@ -120,4 +133,16 @@ struct mqo_batch {
   int32_t* d_flag = nullptr;            // misc device flags [4]
   int32_t* h_flag = nullptr;            // pinned mirror [4]
   int coop_blocks = 0;                  // resident CTAs for the persistent kernel
+  // solver state (solver.cu)
+  mqo_b200::ChainRng* d_rng = nullptr;  // [Bp] per-chain streams
+  uint64_t* d_pool = nullptr;           // [pool_cap][W] packed pool bodies
+  int32_t pool_cap = 0, pool_size = 0;
+  uint64_t* d_bodies = nullptr;         // [Bp][W] packed harvested bodies
+  int64_t* d_scores = nullptr;          // [Bp]
+  int32_t* d_valid = nullptr;           // [Bp]
+  int32_t* d_pick = nullptr;            // [Bp] pool index drawn per chain
+  uint8_t* d_state8 = nullptr;          // [n][Bp] harvest / local-search states
+  int32_t* d_lastw = nullptr;           // [Bp][n] reset scratch
+  int32_t* d_jdraw = nullptr;           // [Bp][n] reset draws j_i
+  int32_t* d_counter = nullptr;         // [4] device counters
 };
