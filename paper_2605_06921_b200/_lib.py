@@ -83,7 +83,9 @@ SIGNATURES: dict[str, tuple] = {
     "mqo_set_pool": (C.c_int, [_P, C.c_int32, _U64]),
     "mqo_reset_from_pool": (C.c_int, [_P, C.c_int32, C.c_double, _I32]),
     "mqo_harvest": (C.c_int, [_P, C.c_int32, _I64, _I32, _U64]),
+    "mqo_local_search": (C.c_int, [_P, C.c_int32, C.c_int32, _U64, _I64]),
 }
+LS_ONE_FLIP, LS_TWO_FLIP, LS_ONE_TWO_FLIP, LS_ONE_TWO_SWAP = range(4)
 
 # mqo_rng_state as a numpy structured dtype (48 bytes)
 RNG_DTYPE = [("s", "<u8", (4,)), ("spare", "<f8"), ("has_spare", "<i4"), ("flags", "<i4")]

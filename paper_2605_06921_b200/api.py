@@ -28,7 +28,8 @@ __all__ = [
     "Graph", "ErSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
-    "pack_bodies", "unpack_bodies",
+    "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
+    "one_two_flip", "one_two_swap",
     "InvalidArgument", "LogicError", "MqoError",
 ]
 
@@ -420,3 +421,37 @@ def mis_fixed_point_check(g: Graph, x, gamma: float, alpha: float) -> bool:
     b = ChainBatch(g, 1)
     b.set_x(np.asarray(x, np.float64)[None, :])
     return bool(b.mis_fixed_point_check(gamma, alpha)[0])
+
+
+# ------------------------------------------------------------ local search
+def local_search(batch: ChainBatch, op: int, bodies: np.ndarray):
+    """Runs a local-search op (localsearch.hpp:28-48) on packed bodies
+    [count][W] on the batch's device.  Returns (packed bodies, out) where out
+    is the gain (flip ops) or the new set size (one_two_swap)."""
+    p = np.array(np.atleast_2d(bodies), dtype=np.uint64, order="C")
+    out = np.zeros(p.shape[0], np.int64)
+    check(lib.mqo_local_search(batch._h, op, p.shape[0], _ptr(p, C.POINTER(C.c_uint64)),
+                               _ptr(out, _I64)))
+    return p, out
+
+
+def _ls_single(g: Graph, op: int, body_u8) -> tuple:
+    b = ChainBatch(g, 1)
+    p, out = local_search(b, op, pack_bodies(np.asarray(body_u8, np.uint8)[None, :]))
+    return unpack_bodies(p, g.n())[0], int(out[0])
+
+
+def one_flip_pass(g: Graph, side):  # localsearch.hpp:39
+    return _ls_single(g, _lib.LS_ONE_FLIP, side)
+
+
+def two_flip_pass(g: Graph, side):  # localsearch.hpp:44
+    return _ls_single(g, _lib.LS_TWO_FLIP, side)
+
+
+def one_two_flip(g: Graph, side):  # localsearch.hpp:48
+    return _ls_single(g, _lib.LS_ONE_TWO_FLIP, side)
+
+
+def one_two_swap(g: Graph, indicator):  # localsearch.hpp:34
+    return _ls_single(g, _lib.LS_ONE_TWO_SWAP, indicator)

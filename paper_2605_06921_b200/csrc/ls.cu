@@ -1,0 +1,564 @@
+// ls.cu -- K7/K8 discrete local search with the reference's exact
+// sequential semantics (localsearch.cpp), one warp per solution.
+//
+//   MaxCut  build_gain_table / apply_flip / one_flip_pass / two_flip_pass /
+//           one_two_flip            localsearch.cpp:17-33, 139-190
+//   MIS     build_tightness / greedy_maximalize / swap_pair_for /
+//           one_two_swap            localsearch.cpp:9-15, 35-137
+//
+// The reference scans vertices in index order and commits every improving
+// move immediately, so a move's legality depends on every earlier commit.
+// Gains are built by a grid-parallel kernel; the commit loop then runs on
+// one warp per solution that scans 32 (x8 unrolled) vertices per step with
+// a ballot, jumps straight to the first improving lane and applies the
+// move's neighbourhood update across the lanes -- identical commits in
+// identical order, without touching non-improving vertices one by one.
+// (1,2)-swap restarts from vertex 0 after every swap (localsearch.cpp:167-
+// 199); the warp instead keeps the scanned prefix clean and re-examines
+// only the 2-hop neighbourhood a swap can change ("dirty" list), which
+// finds exactly the vertex the restarted scan would find.
+#include <algorithm>
+
+#include "common.cuh"
+
+using namespace mqo_b200;
+
+namespace {
+
+constexpr int kLsWarps = 4;  // solutions per CTA (one warp each)
+
+__device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 1; }
+
+// ---------------------------------------------------------------- MaxCut
+// build_gain_table (localsearch.cpp:17-26) for `count` solutions.
+__global__ void k_gain(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
+                       int32_t count, const uint8_t* __restrict__ side, int32_t* __restrict__ delta) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n, v = q % n;
+    const uint8_t* sd = side + s * n;
+    const uint8_t sv = sd[v];
+    int32_t same = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) same += sd[nbr[e]] == sv ? 1 : -1;
+    delta[q] = same;
+  }
+}
+
+// apply_flip (localsearch.cpp:28-33) by a whole warp.
+__device__ __forceinline__ void warp_flip(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                          uint8_t* side, int32_t* delta, int32_t v, int lane,
+                                          int32_t& dmax) {
+  int32_t local_max = INT_MIN;
+  if (lane == 0) {
+    side[v] ^= 1;
+    delta[v] = -delta[v];
+    local_max = delta[v];
+  }
+  __syncwarp();
+  const uint8_t sv = side[v];
+  for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+    const int32_t u = nbr[e];
+    const int32_t nd = delta[u] + (side[u] == sv ? 2 : -2);
+    delta[u] = nd;
+    local_max = max(local_max, nd);
+  }
+  for (int o = 16; o; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  dmax = max(dmax, local_max);
+  __syncwarp();
+}
+
+// one_flip_pass (localsearch.cpp:139-157) on a warp; returns the gain.
+__device__ int64_t warp_one_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
+                                      uint8_t* side, int32_t* delta, int lane, int32_t& dmax) {
+  int64_t total = 0;
+  bool improved = true;
+  while (improved) {
+    improved = false;
+    for (int32_t base = 0; base < n; base += 256) {
+      // 8 chunks of 32 in flight, then resolve them in order
+      int32_t d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int32_t v = base + k * 32 + lane;
+        d[k] = v < n ? *reinterpret_cast<volatile int32_t*>(delta + v) : 0;
+      }
+      unsigned any = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) any |= __ballot_sync(0xffffffffu, d[k] > 0);
+      if (!any) continue;
+      for (int k = 0; k < 8; ++k) {
+        const int32_t cb = base + k * 32;
+        int32_t dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : 0;
+        unsigned mask = __ballot_sync(0xffffffffu, dv > 0);
+        while (mask) {
+          const int i = warp_first(mask);
+          const int32_t v = cb + i;
+          const int32_t gain = __shfl_sync(0xffffffffu, dv, i);
+          total += gain;
+          warp_flip(off, nbr, side, delta, v, lane, dmax);
+          improved = true;
+          dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : 0;
+          mask = __ballot_sync(0xffffffffu, dv > 0) & (i == 31 ? 0u : (~0u << (i + 1)));
+        }
+      }
+    }
+  }
+  return total;
+}
+
+// two_flip_pass (localsearch.cpp:159-181) on a warp.  A vertex v can host a
+// joint move only if delta_v + max(delta) + 2 > 0; dmax is a running upper
+// bound of every delta, so the filter never skips a vertex the reference
+// would act on.  For a candidate v the warp evaluates 32 neighbours at a
+// time against the current state; after a joint flip it resumes right
+// after the flipped neighbour, exactly like the reference's inner loop.
+__device__ int64_t warp_two_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
+                                      uint8_t* side, int32_t* delta, int lane, int32_t& dmax) {
+  int64_t total = 0;
+  bool improved = true;
+  while (improved) {
+    improved = false;
+    for (int32_t cb = 0; cb < n; cb += 32) {
+      int32_t dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : INT_MIN / 2;
+      unsigned mask = __ballot_sync(0xffffffffu, dv + dmax + 2 > 0);
+      while (mask) {
+        const int i = warp_first(mask);
+        const int32_t v = cb + i;
+        const int64_t e1 = off[v + 1];
+        int64_t e = off[v];
+        while (e < e1) {
+          const int64_t my = e + lane;
+          bool ok = false;
+          int32_t u = 0, joint = 0;
+          if (my < e1) {
+            u = nbr[my];
+            const uint8_t sv = *reinterpret_cast<volatile uint8_t*>(side + v);
+            if (u > v && *reinterpret_cast<volatile uint8_t*>(side + u) != sv) {
+              joint = *reinterpret_cast<volatile int32_t*>(delta + v) +
+                      *reinterpret_cast<volatile int32_t*>(delta + u) + 2;
+              ok = joint > 0;
+            }
+          }
+          const unsigned hit = __ballot_sync(0xffffffffu, ok);
+          if (!hit) {
+            e += 32;
+            continue;
+          }
+          const int j = warp_first(hit);
+          const int32_t uu = __shfl_sync(0xffffffffu, u, j);
+          const int32_t jj = __shfl_sync(0xffffffffu, joint, j);
+          warp_flip(off, nbr, side, delta, v, lane, dmax);
+          warp_flip(off, nbr, side, delta, uu, lane, dmax);
+          total += jj;
+          improved = true;
+          e += j + 1;  // resume right after uu with the updated state
+        }
+        dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : INT_MIN / 2;
+        mask = __ballot_sync(0xffffffffu, dv + dmax + 2 > 0) & (i == 31 ? 0u : (~0u << (i + 1)));
+      }
+    }
+  }
+  return total;
+}
+
+__global__ void k_maxcut_ls(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
+                            int32_t count, uint8_t* side_all, int32_t* delta_all, int32_t op,
+                            int64_t* gains) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count) return;
+  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
+  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
+  int32_t dmax = INT_MIN;
+  for (int32_t v = lane; v < n; v += 32) dmax = max(dmax, delta[v]);
+  for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  int64_t total = 0;
+  if (op == 0) {
+    total = warp_one_flip_pass(off, nbr, n, side, delta, lane, dmax);
+  } else if (op == 1) {
+    total = warp_two_flip_pass(off, nbr, n, side, delta, lane, dmax);
+  } else {  // one_two_flip: alternate until a round gains nothing
+    for (;;) {
+      const int64_t round = warp_one_flip_pass(off, nbr, n, side, delta, lane, dmax) +
+                            warp_two_flip_pass(off, nbr, n, side, delta, lane, dmax);
+      total += round;
+      if (round == 0) break;
+    }
+  }
+  if (lane == 0) gains[s] = total;
+}
+
+}  // namespace
+
+namespace {
+
+// ------------------------------------------------------------------- MIS
+// build_tightness (localsearch.cpp:9-15) + the require_maximal_is checks
+// (76-84): flags[s] bit 0 = not independent, bit 1 = not maximal.
+__global__ void k_tight(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
+                        int32_t count, const uint8_t* __restrict__ sel, int32_t* __restrict__ tight,
+                        int32_t* __restrict__ flags) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n, v = q % n;
+    const uint8_t* sd = sel + s * n;
+    int32_t t = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) t += sd[nbr[e]];
+    tight[q] = t;
+    if (sd[v] && t) atomicOr(flags + s, 1);
+    if (!sd[v] && t == 0) atomicOr(flags + s, 2);
+  }
+}
+
+__device__ __forceinline__ bool has_edge(const int64_t* off, const int32_t* nbr, int32_t u, int32_t v) {
+  int64_t lo = off[u], hi = off[u + 1];  // graph.cpp:58-61 (binary search)
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (nbr[mid] < v)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < off[u + 1] && nbr[lo] == v;
+}
+
+// swap_pair_for (localsearch.cpp:60-74) evaluated by one lane: the first
+// pair (c_i, c_j), i < j, of unselected 1-tight neighbours of x in CSR
+// order that are non-adjacent.
+__device__ bool lane_swap_pair(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+                               const int32_t* tight, int32_t x, int32_t& pu, int32_t& pw) {
+  if (!*reinterpret_cast<const volatile uint8_t*>(sel + x)) return false;
+  const int64_t e0 = off[x], e1 = off[x + 1];
+  for (int64_t a = e0; a < e1; ++a) {
+    const int32_t ca = nbr[a];
+    if (*reinterpret_cast<const volatile uint8_t*>(sel + ca) ||
+        *reinterpret_cast<const volatile int32_t*>(tight + ca) != 1)
+      continue;
+    for (int64_t c = a + 1; c < e1; ++c) {
+      const int32_t cb = nbr[c];
+      if (*reinterpret_cast<const volatile uint8_t*>(sel + cb) ||
+          *reinterpret_cast<const volatile int32_t*>(tight + cb) != 1)
+        continue;
+      if (!has_edge(off, nbr, ca, cb)) {
+        pu = ca;
+        pw = cb;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+// Adds vertex z to the set: sel[z] = 1, tight[N(z)] += 1 (warp-parallel).
+__device__ __forceinline__ void warp_select(const int64_t* off, const int32_t* nbr, uint8_t* sel,
+                                            int32_t* tight, int32_t z, int delta, int lane) {
+  if (lane == 0) sel[z] = delta > 0 ? 1 : 0;
+  for (int64_t e = off[z] + lane; e < off[z + 1]; e += 32) tight[nbr[e]] += delta;
+  __syncwarp();
+}
+
+// Marks the selected vertices below the frontier whose swap_pair_for may
+// have changed: 2-hop neighbourhood of a changed vertex t.
+__device__ void warp_mark_dirty(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+                                uint8_t* dflag, int32_t* dlist, int32_t* dcount, int32_t t,
+                                int32_t frontier, int lane) {
+  // s ranges over {t} U N(t); y over {s} U N(s)
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+    const int32_t s = a < e0 ? t : nbr[a];
+    for (int64_t c = off[s] - 1; c < off[s + 1]; ++c) {
+      const int32_t y = c < off[s] ? s : nbr[c];
+      if (y >= frontier || !*reinterpret_cast<const volatile uint8_t*>(sel + y)) continue;
+      // byte flag claim via 32-bit CAS on the containing word
+      unsigned* word = reinterpret_cast<unsigned*>(reinterpret_cast<uintptr_t>(dflag + y) & ~uintptr_t(3));
+      const unsigned shift = (reinterpret_cast<uintptr_t>(dflag + y) & 3) * 8;
+      const unsigned old = atomicOr(word, 1u << shift);
+      if (!((old >> shift) & 0xFF)) dlist[atomicAdd(dcount, 1)] = y;
+    }
+  }
+  __syncwarp();
+}
+
+// Applies the (1,2)-swap at x (localsearch.cpp:174-196) and marks dirt.
+__device__ void warp_apply_swap(const int64_t* off, const int32_t* nbr, const int32_t* deg_unused,
+                                uint8_t* sel, int32_t* tight, uint8_t* dflag, int32_t* dlist,
+                                int32_t* dcount, int32_t* freed, int32_t x, int32_t u, int32_t w,
+                                int32_t frontier, int lane) {
+  (void)deg_unused;
+  warp_select(off, nbr, sel, tight, x, -1, lane);
+  warp_select(off, nbr, sel, tight, u, +1, lane);
+  warp_select(off, nbr, sel, tight, w, +1, lane);
+  // freed neighbours of x, greedily re-added in ascending (degree, id)
+  int32_t nf = 0;
+  if (lane == 0) {
+    for (int64_t e = off[x]; e < off[x + 1]; ++e) {
+      const int32_t z = nbr[e];
+      if (!sel[z] && tight[z] == 0) {
+        // insertion sort by (deg, id)
+        const int64_t dz = off[z + 1] - off[z];
+        int32_t k = nf++;
+        while (k > 0) {
+          const int32_t p = freed[k - 1];
+          const int64_t dp = off[p + 1] - off[p];
+          if (dp < dz || (dp == dz && p < z)) break;
+          freed[k] = p;
+          --k;
+        }
+        freed[k] = z;
+      }
+    }
+  }
+  nf = __shfl_sync(0xffffffffu, nf, 0);
+  __syncwarp();
+  for (int32_t i = 0; i < nf; ++i) {
+    const int32_t z = freed[i];
+    const bool add = !*reinterpret_cast<volatile uint8_t*>(sel + z) &&
+                     *reinterpret_cast<volatile int32_t*>(tight + z) == 0;
+    if (add) warp_select(off, nbr, sel, tight, z, +1, lane);
+    if (add) warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, z, frontier, lane);
+  }
+  warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, x, frontier, lane);
+  warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, u, frontier, lane);
+  warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, w, frontier, lane);
+}
+
+// one_two_swap (localsearch.cpp:88-137) on one warp per solution.
+__global__ void k_mis_swap(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
+                           int32_t count, uint8_t* sel_all, int32_t* tight_all, uint8_t* dflag_all,
+                           int32_t* dlist_all, int32_t* freed_all, int32_t* dcount_all,
+                           int32_t max_degree, int64_t* swaps_out) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count) return;
+  uint8_t* sel = sel_all + static_cast<int64_t>(s) * n;
+  int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
+  uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
+  int32_t* dlist = dlist_all + static_cast<int64_t>(s) * n;
+  int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
+  int32_t* dcount = dcount_all + s;
+  int32_t frontier = 0;
+  int64_t swaps = 0;
+  for (;;) {
+    // 1. lowest swappable vertex among the dirty ones below the frontier
+    __syncwarp();
+    const int32_t nd = *reinterpret_cast<volatile int32_t*>(dcount);
+    int32_t best = INT_MAX, bu = 0, bw = 0;
+    int32_t keep = 0;
+    for (int32_t k0 = 0; k0 < nd; k0 += 32) {
+      const int32_t k = k0 + lane;
+      int32_t x = -1, pu = 0, pw = 0;
+      bool ok = false;
+      if (k < nd) {
+        x = dlist[k];
+        ok = lane_swap_pair(off, nbr, sel, tight, x, pu, pw);
+      }
+      if (ok && x < best) {
+        best = x;
+        bu = pu;
+        bw = pw;
+      }
+      // compact: keep swappable ones (they must be re-checked after the
+      // next swap), drop the rest
+      const unsigned km = __ballot_sync(0xffffffffu, ok);
+      const int pos = __popc(km & ((1u << lane) - 1));
+      __syncwarp();
+      if (ok) dlist[keep + pos] = x;
+      if (!ok && k < nd) dflag[x] = 0;
+      keep += __popc(km);
+      __syncwarp();
+    }
+    if (lane == 0) *dcount = keep;
+    // warp min of best
+    for (int o = 16; o; o >>= 1) {
+      const int32_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int32_t ou = __shfl_xor_sync(0xffffffffu, bu, o);
+      const int32_t ow = __shfl_xor_sync(0xffffffffu, bw, o);
+      if (ob < best) {
+        best = ob;
+        bu = ou;
+        bw = ow;
+      }
+    }
+    __syncwarp();
+    if (best != INT_MAX) {
+      warp_apply_swap(off, nbr, nullptr, sel, tight, dflag, dlist, dcount, freed, best, bu, bw,
+                      frontier, lane);
+      ++swaps;
+      continue;
+    }
+    // 2. scan forward from the frontier
+    int32_t found = -1, fu = 0, fw = 0;
+    for (int32_t cb = frontier; cb < n; cb += 32) {
+      const int32_t x = cb + lane;
+      int32_t pu = 0, pw = 0;
+      const bool ok = x < n && lane_swap_pair(off, nbr, sel, tight, x, pu, pw);
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (m) {
+        const int i = warp_first(m);
+        found = cb + i;
+        fu = __shfl_sync(0xffffffffu, pu, i);
+        fw = __shfl_sync(0xffffffffu, pw, i);
+        break;
+      }
+    }
+    if (found < 0) break;
+    frontier = found + 1;
+    warp_apply_swap(off, nbr, nullptr, sel, tight, dflag, dlist, dcount, freed, found, fu, fw,
+                    frontier, lane);
+    ++swaps;
+  }
+  if (lane == 0) swaps_out[s] = swaps;
+}
+
+// packed [count][W] <-> bytes [count][n]
+__global__ void k_unpack(const uint64_t* __restrict__ packed, int64_t W, int32_t n, int32_t count,
+                         uint8_t* __restrict__ out) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n, v = q % n;
+    out[q] = (packed[s * W + (v >> 6)] >> (63 - (v & 63))) & 1;
+  }
+}
+
+__global__ void k_pack_bytes(const uint8_t* __restrict__ in, int64_t W, int32_t n, int32_t count,
+                             uint64_t* __restrict__ packed, int64_t* __restrict__ popc) {
+  const int64_t total = static_cast<int64_t>(count) * W;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / W, w = q % W;
+    uint64_t bits = 0;
+    for (int i = 0; i < 64; ++i) {
+      const int64_t v = w * 64 + i;
+      if (v < n && in[s * n + v]) bits |= 1ull << (63 - i);
+    }
+    packed[q] = bits;
+    if (popc && bits)
+      atomicAdd(reinterpret_cast<unsigned long long*>(popc + s),
+                static_cast<unsigned long long>(__popcll(bits)));
+  }
+}
+
+int ls_grid(int64_t work) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 32)));
+}
+
+}  // namespace
+
+// -------------------------------------------------------------- host side
+namespace mqo_b200 {
+
+struct LsWork {
+  uint8_t* bytes = nullptr;   // [count][n]
+  int32_t* ints = nullptr;    // [count][n] delta / tight
+  uint8_t* dflag = nullptr;   // [count][n+4]
+  int32_t* dlist = nullptr;   // [count][n]
+  int32_t* freed = nullptr;   // [count][max_degree+1]
+  int32_t* small = nullptr;   // [count] counters / flags
+  int64_t* out64 = nullptr;   // [count]
+  uint64_t* packed = nullptr; // [count][W]
+};
+
+// Runs local search op on `count` packed bodies already in device memory
+// (`d_packed`, [count][W]); results written back in place.
+//   op 0 one_flip_pass, 1 two_flip_pass, 2 one_two_flip (MaxCut: out64 =
+//   gain), 3 one_two_swap (MIS: out64 = new size).
+void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
+                         int64_t* d_out, cudaStream_t st) {
+  mqo_graph* g = b->g;
+  const int32_t n = g->n;
+  const int64_t W = body_words(n);
+  if (count <= 0) return;
+  LsWork w;
+  const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
+  MQO_CUDA(cudaMallocAsync(&w.bytes, cells, st));
+  MQO_CUDA(cudaMallocAsync(&w.ints, sizeof(int32_t) * cells, st));
+  MQO_CUDA(cudaMallocAsync(&w.small, sizeof(int32_t) * count, st));
+  MQO_CUDA(cudaMemsetAsync(w.small, 0, sizeof(int32_t) * count, st));
+  MQO_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t) * count, st));
+  k_unpack<<<ls_grid(cells), 256, 0, st>>>(d_packed, W, n, count, w.bytes);
+  MQO_CUDA(cudaGetLastError());
+  const int blocks = (count + kLsWarps - 1) / kLsWarps;
+  if (op <= 2) {
+    k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
+    MQO_CUDA(cudaGetLastError());
+    k_maxcut_ls<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
+                                                  op, d_out);
+    MQO_CUDA(cudaGetLastError());
+  } else {
+    k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.small);
+    MQO_CUDA(cudaGetLastError());
+    std::vector<int32_t> flags(count);
+    MQO_CUDA(cudaMemcpyAsync(flags.data(), w.small, sizeof(int32_t) * count,
+                             cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < count; ++i) {
+      if (flags[i] & 1) {
+        cudaFreeAsync(w.bytes, st);
+        cudaFreeAsync(w.ints, st);
+        cudaFreeAsync(w.small, st);
+        throw std::invalid_argument("one_two_swap: input not an independent set");
+      }
+      if (flags[i] & 2) {
+        cudaFreeAsync(w.bytes, st);
+        cudaFreeAsync(w.ints, st);
+        cudaFreeAsync(w.small, st);
+        throw std::invalid_argument("one_two_swap: input not maximal");
+      }
+    }
+    MQO_CUDA(cudaMemsetAsync(w.small, 0, sizeof(int32_t) * count, st));
+    MQO_CUDA(cudaMallocAsync(&w.dflag, int64_t(count) * (n + 4), st));
+    MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
+    MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
+    MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
+    k_mis_swap<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
+                                                 w.dflag, w.dlist, w.freed, w.small,
+                                                 g->max_degree, d_out);
+    MQO_CUDA(cudaGetLastError());
+    MQO_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t) * count, st));
+  }
+  k_pack_bytes<<<ls_grid(int64_t(count) * W), 256, 0, st>>>(w.bytes, W, n, count, d_packed,
+                                                            op == 3 ? d_out : nullptr);
+  MQO_CUDA(cudaGetLastError());
+  cudaFreeAsync(w.bytes, st);
+  cudaFreeAsync(w.ints, st);
+  cudaFreeAsync(w.small, st);
+  if (w.dflag) cudaFreeAsync(w.dflag, st);
+  if (w.dlist) cudaFreeAsync(w.dlist, st);
+  if (w.freed) cudaFreeAsync(w.freed, st);
+}
+
+}  // namespace mqo_b200
+
+extern "C" int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_t* packed,
+                                int64_t* out) {
+  return guard([&] {
+    if (!b || count < 0 || (count && (!packed || !out)))
+      throw std::invalid_argument("mqo_local_search: bad arguments");
+    if (op < 0 || op > 3) throw std::invalid_argument("mqo_local_search: unknown op");
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    if (count == 0) return;
+    const int64_t W = body_words(b->g->n);
+    uint64_t* d_packed = nullptr;
+    int64_t* d_out = nullptr;
+    cudaStream_t st = b->stream;
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * std::max<int64_t>(1, W * count), st));
+    MQO_CUDA(cudaMallocAsync(&d_out, sizeof(int64_t) * count, st));
+    MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * W * count, cudaMemcpyHostToDevice, st));
+    try {
+      local_search_device(b, op, count, d_packed, d_out, st);
+    } catch (...) {
+      cudaFreeAsync(d_packed, st);
+      cudaFreeAsync(d_out, st);
+      cudaStreamSynchronize(st);
+      throw;
+    }
+    MQO_CUDA(cudaMemcpyAsync(packed, d_packed, sizeof(uint64_t) * W * count, cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaMemcpyAsync(out, d_out, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(d_packed, st);
+    cudaFreeAsync(d_out, st);
+    MQO_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -1,0 +1,124 @@
+"""GPU parity of the local-search kernels (K7/K8) against the oracle:
+identical final bodies and gains / sizes (bit-exact integer paths).  KATs
+re-hosted from /root/reference/proj/tests/test_localsearch.cpp."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def P(cuda_ok):
+    import paper_2605_06921_b200 as P
+    return P
+
+
+def G(P, n, edges):
+    return P.Graph.from_edges(n, edges)
+
+
+def test_kats(P):  # test_localsearch.cpp:43-105, 138-160
+    c5 = G(P, 5, [(v, (v + 1) % 5) for v in range(5)])
+    assert P.one_two_swap(c5, [1, 0, 1, 0, 0])[0].tolist() == [1, 0, 1, 0, 0]
+    star = G(P, 5, [(0, v) for v in range(1, 5)])
+    body, size = P.one_two_swap(star, [1, 0, 0, 0, 0])
+    assert body.tolist() == [0, 1, 1, 1, 1] and size == 4
+    p5 = G(P, 5, [(v, v + 1) for v in range(4)])
+    assert P.one_two_swap(p5, [0, 1, 0, 1, 0])[0].tolist() == [0, 1, 0, 1, 0]
+    k3 = G(P, 3, [(0, 1), (1, 2), (0, 2)])
+    with pytest.raises(P.InvalidArgument, match="not an independent set"):
+        P.one_two_swap(k3, [1, 1, 0])
+    p3 = G(P, 3, [(0, 1), (1, 2)])
+    with pytest.raises(P.InvalidArgument, match="not maximal"):
+        P.one_two_swap(p3, [1, 0, 0])
+    side, gain = P.one_flip_pass(k3, [0, 0, 0])
+    assert gain == 2
+    c4 = G(P, 4, [(v, (v + 1) % 4) for v in range(4)])
+    side, gain = P.one_flip_pass(c4, [0, 1, 0, 1])
+    assert gain == 0 and side.tolist() == [0, 1, 0, 1]
+    side, gain = P.two_flip_pass(p3, [0, 1, 0])
+    assert gain == 0 and side.tolist() == [0, 1, 0]
+    c6 = G(P, 6, [(v, (v + 1) % 6) for v in range(6)])
+    assert P.two_flip_pass(c6, [0, 1, 0, 1, 0, 1])[1] == 0
+    assert P.one_two_flip(c6, [0, 1, 0, 1, 0, 1])[1] == 0
+    e4 = G(P, 4, [(0, 1)])
+    e4 = P.Graph.from_edges(4, [])
+    assert P.one_two_flip(e4, [0, 1, 0, 1])[1] == 0
+
+
+@pytest.mark.parametrize("op", ["one_flip_pass", "two_flip_pass", "one_two_flip"])
+def test_flips_random_vs_oracle(O, P, op):
+    rng = np.random.default_rng(107)
+    for trial in range(20):
+        n = int(rng.integers(6, 60))
+        seed = O.derive_seed(107, trial)
+        og = O.generate_er(n, 0.4 if n < 20 else 0.15, seed)
+        pg = P.generate(P.ErSpec(n, 0.4 if n < 20 else 0.15), seed)
+        # several random sides at once through one batched call
+        sides = rng.integers(0, 2, (7, n)).astype(np.uint8)
+        b = P.ChainBatch(pg, 1)
+        opcode = {"one_flip_pass": 0, "two_flip_pass": 1, "one_two_flip": 2}[op]
+        packed, gains = P.local_search(b, opcode, P.pack_bodies(sides))
+        got = P.unpack_bodies(packed, n)
+        for k in range(7):
+            ref_side, ref_gain = getattr(O, op)(og, sides[k])
+            assert gains[k] == ref_gain and (got[k] == ref_side).all(), (trial, k)
+
+
+def test_swap_random_vs_oracle(O, P):
+    rng = np.random.default_rng(103)
+    for trial in range(30):
+        n = 24 if trial < 20 else 200
+        p = float(rng.uniform(0.08, 0.35)) if n == 24 else 0.03
+        seed = O.derive_seed(103, trial)
+        og = O.generate_er(n, p, seed)
+        pg = P.generate(P.ErSpec(n, p), seed)
+        starts = []
+        for k in range(5):  # greedy completions of random independent seeds
+            ind = np.zeros(n, np.uint8)
+            for v in rng.permutation(n)[: n // 6]:
+                ind[v] = 1
+                if not O.is_independent(og, ind):
+                    ind[v] = 0
+            starts.append(O.greedy_maximalize(og, ind)[0])
+        starts = np.array(starts)
+        b = P.ChainBatch(pg, 1)
+        packed, sizes = P.local_search(b, 3, P.pack_bodies(starts))
+        got = P.unpack_bodies(packed, n)
+        for k in range(5):
+            ref, size = O.one_two_swap(og, starts[k])
+            assert sizes[k] == size and (got[k] == ref).all(), (trial, k)
+
+
+def test_goldens(P):
+    z = np.load(os.path.join(GOLD, "pieces.npz"))
+    g1 = P.generate(P.ErSpec(1000, 0.01), 1)
+    g2 = P.generate(P.ErSpec(2000, 6 / 2000), 1)
+    assert (P.one_two_swap(g1, z["c1_greedy"])[0] == z["c1_swap"]).all()
+    assert (P.one_two_swap(g1, z["c1_greedy_empty"])[0] == z["c1_swap_empty"]).all()
+    s1, a = P.one_flip_pass(g2, z["c2_harvest"])
+    s2, b = P.two_flip_pass(g2, z["c2_harvest"])
+    s3, c = P.one_two_flip(g2, z["c2_harvest"])
+    assert (s1 == z["c2_oneflip"]).all() and (s2 == z["c2_twoflip"]).all()
+    assert (s3 == z["c2_onetwo"]).all() and [a, b, c] == z["c2_gains"].tolist()
+
+
+def test_large_vs_oracle(O, P):
+    """BA(1e5,5) one_two_flip from random sides; ER(2e4, d=10) one_two_swap
+    from the greedy completion of the empty set."""
+    og = O.generate_ba(100000, 5, 2)
+    pg = P.generate(P.BaSpec(100000, 5), 2)
+    side = np.random.default_rng(1).integers(0, 2, 100000).astype(np.uint8)
+    got, gain = P.one_two_flip(pg, side)
+    ref, rgain = O.one_two_flip(og, side)
+    assert gain == rgain and (got == ref).all()
+    og = O.generate_er(20000, 10 / 20000, 3)
+    pg = P.generate(P.ErSpec(20000, 10 / 20000), 3)
+    start, _ = O.greedy_maximalize(og, np.zeros(20000, np.uint8))
+    got, size = P.one_two_swap(pg, start)
+    ref, rsize = O.one_two_swap(og, start)
+    assert size == rsize and (got == ref).all()
