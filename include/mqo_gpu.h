@@ -221,6 +221,74 @@ int mqo_harvest(mqo_batch* b, int32_t problem, int64_t* scores, int32_t* valid,
 enum { MQO_LS_ONE_FLIP = 0, MQO_LS_TWO_FLIP = 1, MQO_LS_ONE_TWO_FLIP = 2, MQO_LS_ONE_TWO_SWAP = 3 };
 int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_t* packed, int64_t* out);
 
+/* ---- the solver engine (solver.hpp:11-80, run_engine solver.cpp:192-372) -- */
+/* init_state noise source: EXACT replays Box-Muller on the host with the
+ * process's libm (bit-identical to the reference's glibc draws); DEVICE
+ * uses CUDA's log/sincos (within 1e-14 absolute, ~5% of values differ in
+ * the last bit).  Both consume the streams identically. */
+enum { MQO_INIT_EXACT = 0, MQO_INIT_DEVICE = 1 };
+/* RunReport::warnings (solver.cpp:222,230,362), as bits in emission order. */
+enum { MQO_WARN_EDGELESS = 1, MQO_WARN_RESET_NOOP = 2, MQO_WARN_NO_SOLUTION = 4 };
+
+/* SolverConfig (solver.hpp:17-36) + device placement. */
+typedef struct {
+  int32_t objective; /* MQO_MIS_QUBO ... MQO_PERTURBED_BIAS */
+  double param;      /* gamma / lambda */
+  double alpha, beta;
+  int32_t max_iters;
+  double conv_tol;
+  int32_t check_every;
+  double reset_fraction; /* rho */
+  int32_t reset_rounds;  /* T_gs */
+  double init_noise;     /* sigma */
+  double time_budget_secs;
+  uint64_t seed;
+  int32_t local_search;
+  int32_t pool_batch, pool_keep; /* B, K */
+  int32_t has_init_constant;
+  double init_constant;
+  int32_t has_stop_at_score;
+  int64_t stop_at_score;
+  int32_t has_max_outer_loops;
+  int32_t max_outer_loops;
+  int32_t init_mode; /* MQO_INIT_EXACT (default) | MQO_INIT_DEVICE */
+} mqo_solver_config;
+
+/* RunReport (solver.hpp:42-61); the best body goes to a separate buffer. */
+typedef struct {
+  int64_t score;
+  int32_t found_solution;
+  int64_t after_gradient, after_reset_loop, after_local_search;
+  int32_t outer_loops, trajectories;
+  int64_t resets_accepted, resets_rejected, total_iterations;
+  int32_t last_trajectory_stop;
+  double elapsed_secs;
+  int32_t n_warnings;
+  int32_t warnings; /* MQO_WARN_* bits */
+} mqo_run_report;
+
+/* Optional communicator for sharding the B chains over ranks (one process
+ * per GPU).  allgather: every rank contributes `bytes` from `send`; `recv`
+ * receives world * bytes in rank order.  Return 0 on success. */
+typedef struct {
+  void* ctx;
+  int32_t rank, world;
+  int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
+} mqo_comm;
+
+/* solve_pooled (solver.hpp:80): runs the engine on `g`'s device.
+ * best_body (may be NULL) receives the best solution as uint8[n]
+ * (MIS indicator / MaxCut side).  With comm != NULL rank r owns chains
+ * [r*ceil(B/world), ...) and every rank returns the identical report.
+ * solve_mis / solve_maxcut are solve_pooled with the reference's guards. */
+int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                     mqo_run_report* report, uint8_t* best_body);
+
+/* init_state on the host for one stream (the EXACT init path), usable on a
+ * host-only graph: x[n] out, *st advanced like Rng. */
+int mqo_init_state_host(const mqo_graph* g, int32_t problem, double sigma, mqo_rng_state* st,
+                        double* x);
+
 #ifdef __cplusplus
 }
 #endif

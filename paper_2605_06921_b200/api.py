@@ -29,7 +29,8 @@ __all__ = [
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
-    "one_two_flip", "one_two_swap",
+    "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
+    "solve_maxcut", "init_state_host", "INIT_EXACT", "INIT_DEVICE",
     "InvalidArgument", "LogicError", "MqoError",
 ]
 
@@ -455,3 +456,154 @@ def one_two_flip(g: Graph, side):  # localsearch.hpp:48
 
 def one_two_swap(g: Graph, indicator):  # localsearch.hpp:34
     return _ls_single(g, _lib.LS_ONE_TWO_SWAP, indicator)
+
+
+# ------------------------------------------------------------------ solver
+class _SolverCfg(C.Structure):
+    _fields_ = [
+        ("objective", C.c_int32), ("param", C.c_double), ("alpha", C.c_double),
+        ("beta", C.c_double), ("max_iters", C.c_int32), ("conv_tol", C.c_double),
+        ("check_every", C.c_int32), ("reset_fraction", C.c_double),
+        ("reset_rounds", C.c_int32), ("init_noise", C.c_double),
+        ("time_budget_secs", C.c_double), ("seed", C.c_uint64), ("local_search", C.c_int32),
+        ("pool_batch", C.c_int32), ("pool_keep", C.c_int32),
+        ("has_init_constant", C.c_int32), ("init_constant", C.c_double),
+        ("has_stop_at_score", C.c_int32), ("stop_at_score", C.c_int64),
+        ("has_max_outer_loops", C.c_int32), ("max_outer_loops", C.c_int32),
+        ("init_mode", C.c_int32)]
+
+
+class _RunReport(C.Structure):
+    _fields_ = [
+        ("score", C.c_int64), ("found_solution", C.c_int32), ("after_gradient", C.c_int64),
+        ("after_reset_loop", C.c_int64), ("after_local_search", C.c_int64),
+        ("outer_loops", C.c_int32), ("trajectories", C.c_int32),
+        ("resets_accepted", C.c_int64), ("resets_rejected", C.c_int64),
+        ("total_iterations", C.c_int64), ("last_trajectory_stop", C.c_int32),
+        ("elapsed_secs", C.c_double), ("n_warnings", C.c_int32), ("warnings", C.c_int32)]
+
+
+class _Comm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
+                ("allgather", C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_size_t))]
+
+
+lib.mqo_solve_pooled.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), C.POINTER(_Comm),
+                                 C.POINTER(_RunReport), _U8]
+lib.mqo_solve_pooled.restype = C.c_int
+lib.mqo_init_state_host.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, _D]
+lib.mqo_init_state_host.restype = C.c_int
+
+INIT_EXACT, INIT_DEVICE = 0, 1
+WARNINGS = {1: "graph has no edges; returning the trivial solution",
+            2: "floor(rho * n) = 0: global resets are no-ops",
+            4: "budget exhausted before the first trajectory finished"}
+
+
+@dataclass
+class SolverConfig:  # solver.hpp:17-36
+    objective: object = field(default_factory=MisQubo)
+    optimizer: OptimizerConfig = field(default_factory=OptimizerConfig)
+    reset_fraction: float = 0.5
+    reset_rounds: int = 60
+    init_noise: float = 0.15
+    time_budget_secs: float = 10.0
+    seed: int = 1
+    local_search: bool = True
+    pool_batch: int = 1
+    pool_keep: int = 1
+    init_constant: float | None = None
+    stop_at_score: int | None = None
+    max_outer_loops: int | None = None
+    init_mode: int = INIT_EXACT
+
+    def to_c(self) -> _SolverCfg:
+        c = _SolverCfg()
+        c.objective, c.param = self.objective.kind, float(self.objective.param)
+        o = self.optimizer
+        c.alpha, c.beta, c.max_iters = o.alpha, o.beta, o.max_iters
+        c.conv_tol, c.check_every = o.conv_tol, o.check_every
+        c.reset_fraction, c.reset_rounds = self.reset_fraction, self.reset_rounds
+        c.init_noise, c.time_budget_secs, c.seed = self.init_noise, self.time_budget_secs, self.seed
+        c.local_search = 1 if self.local_search else 0
+        c.pool_batch, c.pool_keep = self.pool_batch, self.pool_keep
+        c.has_init_constant = self.init_constant is not None
+        c.init_constant = self.init_constant or 0.0
+        c.has_stop_at_score = self.stop_at_score is not None
+        c.stop_at_score = self.stop_at_score or 0
+        c.has_max_outer_loops = self.max_outer_loops is not None
+        c.max_outer_loops = self.max_outer_loops or 0
+        c.init_mode = self.init_mode
+        return c
+
+
+@dataclass
+class RunReport:  # solver.hpp:48-61
+    best_score: int
+    best_body: np.ndarray
+    found_solution: bool
+    after_gradient: int
+    after_reset_loop: int
+    after_local_search: int
+    outer_loops: int
+    trajectories: int
+    resets_accepted: int
+    resets_rejected: int
+    total_iterations: int
+    last_trajectory_stop: int
+    elapsed_secs: float
+    warnings: list
+
+
+def solve_pooled(g: Graph, cfg: SolverConfig, comm=None) -> RunReport:
+    """solve_pooled (solver.hpp:80) on g's device.  `comm` (optional) is an
+    object with .rank, .world and .allgather(bytes) -> bytes (all ranks'
+    contributions concatenated in rank order), e.g. a torch.distributed
+    adapter; chains are then sharded over the ranks."""
+    rep = _RunReport()
+    body = np.zeros(max(g.n(), 1), np.uint8)
+    cptr = None
+    if comm is not None:
+        def _ag(ctx, send, recv, nbytes):
+            try:
+                data = C.string_at(send, nbytes)
+                out = comm.allgather(data)
+                C.memmove(recv, out, len(out))
+                return 0
+            except Exception:  # surfaced as an engine error
+                return 1
+        c = _Comm()
+        c.ctx, c.rank, c.world = None, comm.rank, comm.world
+        c.allgather = _Comm._fields_[3][1](_ag)  # kept alive by `c` for the call
+        cptr = C.byref(c)
+    check(lib.mqo_solve_pooled(g._h, C.byref(cfg.to_c()), cptr, C.byref(rep), _ptr(body, _U8)))
+    warns = [m for bit, m in WARNINGS.items() if rep.warnings & bit]
+    return RunReport(rep.score, body[: g.n()].copy(), bool(rep.found_solution), rep.after_gradient,
+                     rep.after_reset_loop, rep.after_local_search, rep.outer_loops,
+                     rep.trajectories, rep.resets_accepted, rep.resets_rejected,
+                     rep.total_iterations, rep.last_trajectory_stop, rep.elapsed_secs, warns)
+
+
+def solve_mis(g: Graph, cfg: SolverConfig) -> RunReport:  # solver.cpp:376-381
+    if problem_of(cfg.objective) != PROBLEM_MIS:
+        raise InvalidArgument(1, "solve_mis: objective must be the MIS QUBO")
+    if cfg.pool_batch != 1 or cfg.pool_keep != 1:
+        raise InvalidArgument(1, "solve_mis: sequential solver requires batch = keep = 1")
+    return solve_pooled(g, cfg)
+
+
+def solve_maxcut(g: Graph, cfg: SolverConfig) -> RunReport:  # solver.cpp:383-389
+    if problem_of(cfg.objective) != PROBLEM_MAXCUT:
+        raise InvalidArgument(1, "solve_maxcut: objective must be a MaxCut formulation")
+    if cfg.pool_batch != 1 or cfg.pool_keep != 1:
+        raise InvalidArgument(1, "solve_maxcut: sequential solver requires batch = keep = 1")
+    return solve_pooled(g, cfg)
+
+
+def init_state_host(g: Graph, problem: int, sigma: float, state: np.ndarray):
+    """init_state (solver.cpp:30-46) for one stream on the host (EXACT mode)."""
+    st = np.array(state, dtype=_lib.RNG_DTYPE).reshape(1)
+    x = np.empty(g.n(), np.float64)
+    check(lib.mqo_init_state_host(g._h, problem, sigma, st.ctypes.data, _ptr(x, _D)))
+    return x, st[0]

@@ -1,0 +1,496 @@
+// engine.cu -- the mQO solver engine (reference: run_engine,
+// solver.cpp:192-372; solve_pooled / solve_mis / solve_maxcut 376-392) as
+// native host orchestration of the device kernels:
+//
+//   Phase 1  fresh trajectories      init (K3) -> K1/K2 -> harvest (K5/K6)
+//   Phase 2  T_gs reset rounds        pick+encode+global_reset (K4) -> K1/K2 -> K5
+//   Phase 3  local search over pool   K7/K8
+//   final polish of the incumbent
+//
+// Merges run in global chain order on the host (TopKPool semantics of
+// solver.cpp:108-145, 252-275) over packed bodies; only candidates that can
+// enter the pool cross PCIe.  With a communicator the B chains are sharded
+// over ranks (chain b keeps stream derive_seed(seed, b+1)), every merge
+// all-gathers the per-chain records and the needed bodies, and every rank
+// replays the identical merge -- results do not depend on the rank count.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "common.cuh"
+#include "rng.cuh"
+
+using namespace mqo_b200;
+
+namespace mqo_b200 {
+void init_states_device(mqo_batch* b, int32_t problem, double sigma);
+void init_states_constant(mqo_batch* b, int32_t problem, double c);
+void reset_from_pool(mqo_batch* b, int32_t problem, double rho);
+void harvest_device(mqo_batch* b, int32_t problem);
+void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt,
+                      double deadline);
+void read_outcomes(mqo_batch* b, int32_t* iterations, int32_t* reasons);
+void launch_project(mqo_batch* b, double* x, int32_t problem);
+void upload_chain_major(mqo_batch* b, const double* host, double* dst);
+void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
+                         int64_t* d_out, cudaStream_t st);
+
+// init_state (solver.cpp:30-46) on the host with this process's libm, so the
+// Box-Muller draws are bit-identical to the reference's (glibc log/sin/cos
+// are not reproducible on the device).  Consumes `st` exactly like Rng.
+void host_init_state(const int64_t* off, int32_t n, int32_t dmax, int32_t problem, double sigma,
+                     mqo_rng_state& st, double* x) {
+  Xoshiro r{{st.s[0], st.s[1], st.s[2], st.s[3]}};
+  const double dm = static_cast<double>(dmax);
+  for (int32_t v = 0; v < n; ++v) {
+    const double ratio = 1.0 - static_cast<double>(off[v + 1] - off[v]) / dm;
+    double base = problem == MQO_PROBLEM_MIS ? ratio : 2.0 * ratio - 1.0;
+    if (sigma > 0.0) {  // Rng::normal(0, sigma), rng.hpp:49-62
+      double nv;
+      if (st.has_spare) {
+        st.has_spare = 0;
+        nv = 0.0 + sigma * st.spare;
+      } else {
+        double u1 = u01_of(xoshiro_next(r));
+        const double u2 = u01_of(xoshiro_next(r));
+        while (u1 <= 0.0) u1 = u01_of(xoshiro_next(r));
+        const double rad = std::sqrt(-2.0 * std::log(u1));
+        const double theta = 2.0 * 3.141592653589793 * u2;
+        st.spare = rad * std::sin(theta);
+        st.has_spare = 1;
+        nv = 0.0 + sigma * rad * std::cos(theta);
+      }
+      base += nv;
+    }
+    const double lo = problem == MQO_PROBLEM_MIS ? 0.0 : -1.0;
+    const double a = lo < base ? base : lo;
+    x[v] = a < 1.0 ? a : 1.0;
+  }
+  for (int w = 0; w < 4; ++w) st.s[w] = r.s[w];
+}
+
+}  // namespace mqo_b200
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double mono_now() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<double>(ts.tv_sec) + 1e-9 * static_cast<double>(ts.tv_nsec);
+}
+
+struct Entry {
+  int64_t score = 0;
+  std::vector<uint64_t> body;  // packed, W words
+};
+
+// body_less (solver.cpp:107-112) on packed bodies.  MaxCut: the side
+// vectors compare lexicographically == the packed words compare as
+// unsigned integers.  MIS: pool comparisons only ever involve equal scores
+// (= equal sizes); then the member list with the lower first differing
+// vertex is smaller, i.e. the larger packed word.
+bool body_less(int problem, const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+  for (size_t w = 0; w < a.size(); ++w)
+    if (a[w] != b[w]) return problem == MQO_PROBLEM_MAXCUT ? a[w] < b[w] : a[w] > b[w];
+  return false;
+}
+
+struct TopKPool {  // solver.cpp:121-145
+  int k;
+  int problem;
+  std::vector<Entry> e;
+  bool before(const Entry& a, const Entry& b) const {
+    if (a.score != b.score) return a.score > b.score;
+    return body_less(problem, a.body, b.body);
+  }
+  bool offer(const Entry& s) {  // returns true if the pool changed
+    auto pos = std::lower_bound(e.begin(), e.end(), s,
+                                [&](const Entry& x, const Entry& y) { return before(x, y); });
+    if (pos != e.end() && pos->score == s.score && pos->body == s.body) return false;
+    const size_t idx = static_cast<size_t>(pos - e.begin());
+    e.insert(pos, s);
+    if (static_cast<int>(e.size()) > k) e.resize(k);
+    return idx < e.size();
+  }
+};
+
+void validate(const mqo_solver_config& c) {  // solver.cpp:14-28
+  if (c.objective < 0 || c.objective > 4) throw std::invalid_argument("objective: unknown kind");
+  if (c.objective == MQO_MIS_QUBO && !(c.param > 1.0))
+    throw std::invalid_argument("mis-qubo: gamma must be > 1");
+  if (c.objective == MQO_PERTURBED_LAPLACIAN && !(c.param > 0.0))
+    throw std::invalid_argument("perturbed-laplacian: lambda must be > 0");
+  if (c.objective == MQO_PERTURBED_BIAS && !(c.param > 0.0 && c.param < 2.0))
+    throw std::invalid_argument("perturbed-bias: lambda must be in (0, 2)");
+  if (!(c.alpha > 0.0)) throw std::invalid_argument("optimizer: alpha must be > 0");
+  if (c.beta < 0.0 || c.beta >= 1.0) throw std::invalid_argument("optimizer: beta must be in [0, 1)");
+  if (c.max_iters < 1) throw std::invalid_argument("optimizer: max_iters must be >= 1");
+  if (c.conv_tol < 0.0) throw std::invalid_argument("optimizer: conv_tol must be >= 0");
+  if (c.check_every < 1) throw std::invalid_argument("optimizer: check_every must be >= 1");
+  if (c.reset_fraction < 0.0 || c.reset_fraction >= 1.0)
+    throw std::invalid_argument("solver: reset_fraction must be in [0, 1)");
+  if (c.reset_rounds < 0) throw std::invalid_argument("solver: reset_rounds must be >= 0");
+  if (c.init_noise < 0.0) throw std::invalid_argument("solver: init_noise must be >= 0");
+  if (!(c.time_budget_secs > 0.0)) throw std::invalid_argument("solver: time_budget_secs must be > 0");
+  if (c.pool_batch < 1 || c.pool_keep < 1)
+    throw std::invalid_argument("solver: pool batch and keep must be >= 1");
+  if (c.has_max_outer_loops && c.max_outer_loops < 1)
+    throw std::invalid_argument("solver: max_outer_loops must be >= 1");
+}
+
+// Communicator wrapper (single process when comm == nullptr).
+struct Comm {
+  const mqo_comm* c;
+  int rank() const { return c ? c->rank : 0; }
+  int world() const { return c ? c->world : 1; }
+  void allgather(const void* send, void* recv, size_t bytes) const {
+    if (!c) {
+      std::memcpy(recv, send, bytes);
+      return;
+    }
+    if (c->allgather(c->ctx, send, recv, bytes) != 0)
+      throw std::runtime_error("mqo_comm.allgather failed");
+  }
+};
+
+struct Engine {
+  mqo_graph* g;
+  mqo_solver_config cfg;
+  Comm comm;
+  int problem;
+  int32_t n;
+  int64_t W;
+  int B_global, B_local, first_chain;
+  mqo_batch* batch = nullptr;
+  TopKPool pool;
+  Entry best;
+  bool have_best = false;
+  bool pool_dirty = true;
+  mqo_run_report rep{};
+  int64_t best_of_gradient = 0, best_of_resets = 0, best_of_ls = 0;
+  double t0 = 0.0, deadline = 0.0;
+  // per-merge gathered records (global chain order)
+  std::vector<int64_t> g_scores;
+  std::vector<int32_t> g_valid, g_iters, g_stops;
+
+  bool past_deadline() const { return mono_now() >= deadline; }
+  bool target_hit() const {
+    return have_best && cfg.has_stop_at_score && best.score >= cfg.stop_at_score;
+  }
+
+  void init_phase() {
+    if (cfg.has_init_constant) {
+      init_states_constant(batch, problem, cfg.init_constant);
+      return;
+    }
+    if (cfg.init_mode == MQO_INIT_DEVICE || !(cfg.init_noise > 0.0)) {
+      init_states_device(batch, problem, cfg.init_noise);
+      return;
+    }
+    // exact replay: host Box-Muller with the reference's libm
+    std::vector<mqo_rng_state> st(B_local);
+    if (mqo_batch_get_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
+    std::vector<double> x(static_cast<size_t>(B_local) * n);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int threads = static_cast<int>(std::min<unsigned>(hw, static_cast<unsigned>(B_local)));
+    std::vector<std::thread> pool_t;
+    for (int t = 0; t < threads; ++t)
+      pool_t.emplace_back([&, t] {
+        for (int c = t; c < B_local; c += threads)
+          host_init_state(g->h_off.data(), n, g->max_degree, problem, cfg.init_noise, st[c],
+                          x.data() + static_cast<size_t>(c) * n);
+      });
+    for (auto& th : pool_t) th.join();
+    upload_chain_major(batch, x.data(), batch->d_x[batch->cur]);
+    if (mqo_batch_set_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
+  }
+
+  void trajectories() {
+    const mqo_objective obj{cfg.objective, cfg.param};
+    const mqo_optimizer opt{cfg.alpha, cfg.beta, cfg.max_iters, cfg.conv_tol, cfg.check_every};
+    launch_project(batch, batch->d_x[batch->cur], problem);
+    run_trajectories(batch, obj, opt, deadline);
+  }
+
+  // Gathers this phase's per-chain records in global chain order and the
+  // bodies of the candidates that can touch the pool, then merges
+  // (solver.cpp:252-275).
+  void harvest_and_merge(bool count_resets) {
+    harvest_device(batch, problem);
+    std::vector<int32_t> iters(B_local), stops(B_local), dep(B_local);
+    std::vector<int64_t> scores(B_local);
+    read_outcomes(batch, iters.data(), stops.data());
+    MQO_CUDA(cudaMemcpyAsync(scores.data(), batch->d_scores, sizeof(int64_t) * B_local,
+                             cudaMemcpyDeviceToHost, batch->stream));
+    MQO_CUDA(cudaMemcpyAsync(dep.data(), batch->d_valid, sizeof(int32_t) * B_local,
+                             cudaMemcpyDeviceToHost, batch->stream));
+    MQO_CUDA(cudaStreamSynchronize(batch->stream));
+    // record = {score, valid, iters, stop} for every local chain, padded
+    const int world = comm.world();
+    const int per = (B_global + world - 1) / world;
+    std::vector<int64_t> rec(static_cast<size_t>(per) * 4, 0), all(rec.size() * world);
+    for (int i = 0; i < B_local; ++i) {
+      rec[4 * i] = scores[i];
+      rec[4 * i + 1] = problem == MQO_PROBLEM_MIS ? (dep[i] ? 0 : 1) : 1;
+      rec[4 * i + 2] = iters[i];
+      rec[4 * i + 3] = stops[i];
+    }
+    comm.allgather(rec.data(), all.data(), rec.size() * sizeof(int64_t));
+    g_scores.assign(B_global, 0);
+    g_valid.assign(B_global, 0);
+    g_iters.assign(B_global, 0);
+    g_stops.assign(B_global, 0);
+    for (int r = 0; r < world; ++r)
+      for (int i = 0; i < per; ++i) {
+        const int b = r * per + i;
+        if (b >= B_global) break;
+        const int64_t* q = all.data() + (static_cast<size_t>(r) * per + i) * 4;
+        g_scores[b] = q[0];
+        g_valid[b] = static_cast<int32_t>(q[1]);
+        g_iters[b] = static_cast<int32_t>(q[2]);
+        g_stops[b] = static_cast<int32_t>(q[3]);
+      }
+    // candidates that can change the pool or the incumbent: score >= the
+    // pool's current worst when it is full (the worst only rises during a
+    // merge, so this start-of-merge threshold is conservative)
+    const bool full = static_cast<int>(pool.e.size()) >= pool.k;
+    const int64_t thr = full ? pool.e.back().score : INT64_MIN;
+    auto needed = [&](int b) { return g_valid[b] && (g_scores[b] >= thr || !have_best); };
+    std::vector<std::vector<uint64_t>> bodies(B_global);
+    // local bodies
+    std::vector<int> mine;
+    for (int i = 0; i < B_local; ++i)
+      if (needed(first_chain + i)) mine.push_back(i);
+    std::vector<uint64_t> local(static_cast<size_t>(mine.size()) * W);
+    for (size_t k = 0; k < mine.size(); ++k)
+      MQO_CUDA(cudaMemcpyAsync(local.data() + k * W, batch->d_bodies + static_cast<int64_t>(mine[k]) * W,
+                               sizeof(uint64_t) * W, cudaMemcpyDeviceToHost, batch->stream));
+    MQO_CUDA(cudaStreamSynchronize(batch->stream));
+    if (world == 1) {
+      for (size_t k = 0; k < mine.size(); ++k)
+        bodies[mine[k]].assign(local.begin() + k * W, local.begin() + (k + 1) * W);
+    } else {
+      // every rank knows every rank's needed set from the gathered records
+      std::vector<int> cnt(world, 0);
+      int maxc = 0;
+      for (int b = 0; b < B_global; ++b)
+        if (needed(b)) maxc = std::max(maxc, ++cnt[b / per]);
+      std::vector<uint64_t> send(static_cast<size_t>(std::max(maxc, 1)) * W, 0),
+          recv(send.size() * world);
+      std::copy(local.begin(), local.end(), send.begin());
+      comm.allgather(send.data(), recv.data(), send.size() * sizeof(uint64_t));
+      for (int r = 0; r < world; ++r) {
+        int k = 0;
+        for (int i = 0; i < per; ++i) {
+          const int b = r * per + i;
+          if (b >= B_global || !needed(b)) continue;
+          const uint64_t* src = recv.data() + (static_cast<size_t>(r) * send.size()) + k * W;
+          bodies[b].assign(src, src + W);
+          ++k;
+        }
+      }
+    }
+    for (int b = 0; b < B_global; ++b) {
+      rep.total_iterations += g_iters[b];
+      rep.last_trajectory_stop = g_stops[b];
+      ++rep.trajectories;
+      if (!g_valid[b]) continue;
+      const int64_t sc = g_scores[b];
+      if (count_resets)
+        best_of_resets = std::max(best_of_resets, sc);
+      else
+        best_of_gradient = std::max(best_of_gradient, sc);
+      const bool better = !have_best || sc > best.score;
+      if (!needed(b)) {  // cannot enter a full pool: offer is a no-op
+        if (count_resets) ++rep.resets_rejected;
+        continue;
+      }
+      Entry e{sc, std::move(bodies[b])};
+      if (pool.offer(e)) pool_dirty = true;
+      if (better) {
+        best = std::move(e);
+        have_best = true;
+        if (count_resets) ++rep.resets_accepted;
+      } else if (count_resets) {
+        ++rep.resets_rejected;
+      }
+    }
+  }
+
+  void upload_pool() {
+    if (!pool_dirty) return;
+    std::vector<uint64_t> packed(pool.e.size() * W);
+    for (size_t i = 0; i < pool.e.size(); ++i)
+      std::copy(pool.e[i].body.begin(), pool.e[i].body.end(), packed.begin() + i * W);
+    if (mqo_set_pool(batch, static_cast<int32_t>(pool.e.size()), packed.data()) != MQO_OK)
+      throw CudaError(mqo_last_error());
+    pool_dirty = false;
+  }
+
+  // Polishes `members` bodies with one_two_swap / one_two_flip on the
+  // device (solver.cpp:318-327); scores updated like the reference.
+  void polish(std::vector<Entry>& members) {
+    if (members.empty()) return;
+    const int count = static_cast<int>(members.size());
+    uint64_t* d_packed = nullptr;
+    int64_t* d_out = nullptr;
+    cudaStream_t st = batch->stream;
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * W * count, st));
+    MQO_CUDA(cudaMallocAsync(&d_out, sizeof(int64_t) * count, st));
+    for (int i = 0; i < count; ++i)
+      MQO_CUDA(cudaMemcpyAsync(d_packed + static_cast<int64_t>(i) * W, members[i].body.data(),
+                               sizeof(uint64_t) * W, cudaMemcpyHostToDevice, st));
+    const int op = problem == MQO_PROBLEM_MIS ? MQO_LS_ONE_TWO_SWAP : MQO_LS_ONE_TWO_FLIP;
+    local_search_device(batch, op, count, d_packed, d_out, st);
+    std::vector<int64_t> out(count);
+    for (int i = 0; i < count; ++i)
+      MQO_CUDA(cudaMemcpyAsync(members[i].body.data(), d_packed + static_cast<int64_t>(i) * W,
+                               sizeof(uint64_t) * W, cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaMemcpyAsync(out.data(), d_out, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(d_packed, st);
+    cudaFreeAsync(d_out, st);
+    MQO_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < count; ++i)
+      members[i].score = problem == MQO_PROBLEM_MIS ? out[i] : members[i].score + out[i];
+  }
+
+  void run() {
+    validate(cfg);
+    problem = cfg.objective == MQO_MIS_QUBO ? MQO_PROBLEM_MIS : MQO_PROBLEM_MAXCUT;
+    t0 = mono_now();
+    deadline = t0 + cfg.time_budget_secs;
+    rep = mqo_run_report{};
+    rep.last_trajectory_stop = MQO_ITER_CAP;
+    n = g->n;
+    if (n == 0) throw std::invalid_argument("solver: empty graph");
+    W = body_words(n);
+    pool.k = cfg.pool_keep;
+    pool.problem = problem;
+    if (g->m == 0) {  // solver.cpp:221-226, trivial_solution 176-189
+      rep.warnings |= MQO_WARN_EDGELESS;
+      best.body.assign(W, 0);
+      if (problem == MQO_PROBLEM_MIS) {
+        for (int32_t v = 0; v < n; ++v) best.body[v >> 6] |= 1ull << (63 - (v & 63));
+        best.score = n;
+      }
+      best_of_gradient = best.score;
+      have_best = true;
+      return finish();
+    }
+    if (cfg.reset_rounds > 0 && static_cast<int32_t>(std::floor(cfg.reset_fraction * n)) == 0)
+      rep.warnings |= MQO_WARN_RESET_NOOP;
+
+    B_global = cfg.pool_batch;
+    const int world = comm.world(), rank = comm.rank();
+    const int per = (B_global + world - 1) / world;
+    first_chain = std::min(B_global, rank * per);
+    B_local = std::max(0, std::min(B_global, first_chain + per) - first_chain);
+    if (B_local < 1) throw std::invalid_argument("solver: more ranks than chains");
+    if (mqo_batch_create(g, B_local, &batch) != MQO_OK) throw CudaError(mqo_last_error());
+    try {
+      if (mqo_batch_seed_streams(batch, cfg.seed, 1 + static_cast<uint64_t>(first_chain)) != MQO_OK)
+        throw CudaError(mqo_last_error());
+      loop();
+    } catch (...) {
+      mqo_batch_free(batch);
+      batch = nullptr;
+      throw;
+    }
+    mqo_batch_free(batch);
+    batch = nullptr;
+    finish();
+  }
+
+  void loop() {
+    const mqo_objective obj{cfg.objective, cfg.param};
+    (void)obj;
+    while (!past_deadline() && !target_hit()) {
+      if (cfg.has_max_outer_loops && rep.outer_loops >= cfg.max_outer_loops) break;
+      // Phase 1 (solver.cpp:280-296)
+      init_phase();
+      trajectories();
+      harvest_and_merge(false);
+      // Phase 2 (298-312)
+      for (int round = 0; round < cfg.reset_rounds; ++round) {
+        if (past_deadline() || target_hit() || pool.e.empty()) break;
+        upload_pool();
+        reset_from_pool(batch, problem, cfg.reset_fraction);
+        trajectories();
+        harvest_and_merge(true);
+      }
+      // Phase 3 (314-339)
+      if (cfg.local_search && !pool.e.empty() && !past_deadline() && !target_hit()) {
+        std::vector<Entry> polished = pool.e;
+        polish(polished);
+        for (auto& s : polished) {
+          best_of_ls = std::max(best_of_ls, s.score);
+          const bool better = !have_best || s.score > best.score;
+          if (pool.offer(s)) pool_dirty = true;
+          if (better) {
+            best = s;
+            have_best = true;
+          }
+        }
+      }
+      ++rep.outer_loops;
+    }
+    // final polish (344-359)
+    if (cfg.local_search && have_best) {
+      std::vector<Entry> p{best};
+      polish(p);
+      best_of_ls = std::max(best_of_ls, p[0].score);
+      if (pool.offer(p[0])) pool_dirty = true;
+      if (p[0].score > best.score) best = p[0];
+    }
+    if (!have_best) {  // 361-370
+      rep.warnings |= MQO_WARN_NO_SOLUTION;
+      best.body.assign(W, 0);
+      best.score = 0;
+    }
+  }
+
+  void finish() {  // 209-219
+    rep.found_solution = have_best ? 1 : 0;
+    rep.score = best.score;
+    rep.after_gradient = best_of_gradient;
+    rep.after_reset_loop = std::max(best_of_gradient, best_of_resets);
+    rep.after_local_search = std::max(rep.after_reset_loop, best_of_ls);
+    rep.elapsed_secs = mono_now() - t0;
+    rep.n_warnings = __builtin_popcount(static_cast<unsigned>(rep.warnings));
+  }
+};
+
+}  // namespace
+
+extern "C" int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                                mqo_run_report* report, uint8_t* best_body) {
+  return guard([&] {
+    if (!g || !cfg || !report) throw std::invalid_argument("mqo_solve_pooled: null argument");
+    if (g->device >= 0) MQO_CUDA(cudaSetDevice(g->device));
+    Engine e;
+    e.g = g;
+    e.cfg = *cfg;
+    e.comm = Comm{comm};
+    e.run();
+    *report = e.rep;
+    if (best_body) {
+      for (int32_t v = 0; v < g->n; ++v)
+        best_body[v] = e.best.body.empty() ? 0 : (e.best.body[v >> 6] >> (63 - (v & 63))) & 1;
+    }
+  });
+}
+
+extern "C" int mqo_init_state_host(const mqo_graph* g, int32_t problem, double sigma,
+                                   mqo_rng_state* st, double* x) {
+  return guard([&] {
+    if (!g || !st || !x) throw std::invalid_argument("mqo_init_state_host: null argument");
+    if (g->n == 0) throw std::invalid_argument("init_state: empty graph");
+    if (g->max_degree < 1)
+      throw std::invalid_argument("init_state: edgeless graph (strip isolated vertices upstream)");
+    host_init_state(g->h_off.data(), g->n, g->max_degree, problem, sigma, *st, x);
+  });
+}

@@ -1,0 +1,50 @@
+"""Multi-GPU plumbing for the solver engine: a torch.distributed adapter for
+the engine's communicator (include/mqo_gpu.h `mqo_comm`).
+
+One process per GPU; the engine shards the B chains over the ranks and, at
+every merge, all-gathers the per-chain records and the candidate bodies
+("Mode P").  The payloads are tiny (B x 32 bytes of
+records plus at most a few packed bodies), so a plain all-gather is used:
+NCCL over NVLink on GPUs, gloo on CPU (tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class TorchComm:
+    """Adapter: allgather(bytes) -> bytes of all ranks in rank order."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.torch = torch
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        if device is None:
+            device = (torch.device("cuda", torch.cuda.current_device())
+                      if backend == "nccl" else torch.device("cpu"))
+        self.device = device
+
+    def allgather(self, data: bytes) -> bytes:
+        torch = self.torch
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(self.device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return b"".join(o.cpu().numpy().tobytes() for o in out)
+
+
+def shard(b_global: int, world: int, rank: int) -> range:
+    """Chains owned by `rank` (contiguous blocks of ceil(B/world)), the same
+    split the engine uses."""
+    per = (b_global + world - 1) // world
+    lo = min(b_global, rank * per)
+    return range(lo, min(b_global, lo + per))
+
+
+def argmax_best(scores: np.ndarray) -> int:
+    """Global best over ranks: highest score, ties to the lowest rank."""
+    return int(np.argmax(scores))
