@@ -208,6 +208,17 @@ int mqo_reset_from_pool(mqo_batch* b, int32_t problem, double rho, int32_t* pick
 int mqo_harvest(mqo_batch* b, int32_t problem, int64_t* scores, int32_t* valid,
                 uint64_t* packed);
 
+/* extract_solution (objectives.cpp:143-161) without repair: MIS members are
+ * x > 0.5 (score |I|; independent[b] = is_independent, 173-180), MaxCut
+ * sides x > 0 (score cut_value, 163-171).  Any output may be NULL. */
+int mqo_extract(mqo_batch* b, int32_t problem, int64_t* scores, int32_t* independent,
+                uint64_t* packed);
+
+/* build_gain_table (kind 0, localsearch.cpp:17-26) or build_tightness
+ * (kind 1, 9-15) for `count` packed bodies; out = int32 [count][n]. */
+int mqo_build_tables(mqo_batch* b, int32_t kind, int32_t count, const uint64_t* packed,
+                     int32_t* out);
+
 /* ---- K7/K8 local search (localsearch.hpp:28-48) ---------------------------
  * Runs `op` on `count` packed bodies (host, [count][ceil(n/64)], updated in
  * place) on the batch's device, one warp per body, with the reference's

@@ -562,3 +562,40 @@ extern "C" int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_
     MQO_CUDA(cudaStreamSynchronize(st));
   });
 }
+
+// build_gain_table (kind 0) / build_tightness (kind 1) for `count` packed
+// bodies: out [count][n] int32 (localsearch.cpp:9-26).
+extern "C" int mqo_build_tables(mqo_batch* b, int32_t kind, int32_t count, const uint64_t* packed,
+                                int32_t* out) {
+  return guard([&] {
+    if (!b || count < 0 || (count && (!packed || !out)))
+      throw std::invalid_argument("mqo_build_tables: bad arguments");
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    if (count == 0 || b->g->n == 0) return;
+    mqo_graph* g = b->g;
+    const int32_t n = g->n;
+    const int64_t W = body_words(n), cells = int64_t(count) * n;
+    cudaStream_t st = b->stream;
+    uint64_t* d_packed = nullptr;
+    uint8_t* d_bytes = nullptr;
+    int32_t *d_out = nullptr, *d_flags = nullptr;
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * W * count, st));
+    MQO_CUDA(cudaMallocAsync(&d_bytes, cells, st));
+    MQO_CUDA(cudaMallocAsync(&d_out, sizeof(int32_t) * cells, st));
+    MQO_CUDA(cudaMallocAsync(&d_flags, sizeof(int32_t) * count, st));
+    MQO_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(int32_t) * count, st));
+    MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * W * count, cudaMemcpyHostToDevice, st));
+    k_unpack<<<ls_grid(cells), 256, 0, st>>>(d_packed, W, n, count, d_bytes);
+    if (kind == 0)
+      k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, d_bytes, d_out);
+    else
+      k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, d_bytes, d_out, d_flags);
+    MQO_CUDA(cudaGetLastError());
+    MQO_CUDA(cudaMemcpyAsync(out, d_out, sizeof(int32_t) * cells, cudaMemcpyDeviceToHost, st));
+    cudaFreeAsync(d_packed, st);
+    cudaFreeAsync(d_bytes, st);
+    cudaFreeAsync(d_out, st);
+    cudaFreeAsync(d_flags, st);
+    MQO_CUDA(cudaStreamSynchronize(st));
+  });
+}

@@ -780,3 +780,56 @@ extern "C" int mqo_harvest(mqo_batch* b, int32_t problem, int64_t* scores, int32
       for (int i = 0; i < b->B; ++i) valid[i] = problem == MQO_PROBLEM_MIS ? (dep[i] ? 0 : 1) : 1;
   });
 }
+
+namespace {
+__global__ void k_threshold_mis(const double* __restrict__ X, int64_t total, int32_t B, int32_t Bp,
+                                uint8_t* __restrict__ st) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    st[i] = (static_cast<int>(i % Bp) < B && X[i] > 0.5) ? 1 : 0;  // objectives.cpp:150
+}
+}  // namespace
+
+// extract_solution (objectives.cpp:143-161) without repair: MIS members
+// x > 0.5 (score = |I|, independent[b] = is_independent), MaxCut sides
+// x > 0 (score = cut_value).
+extern "C" int mqo_extract(mqo_batch* b, int32_t problem, int64_t* scores, int32_t* independent,
+                           uint64_t* packed) {
+  return guard([&] {
+    if (!b) throw std::invalid_argument("mqo_extract: null batch");
+    MQO_CUDA(cudaSetDevice(b->g->device));
+    ensure_solver_buffers(b);
+    mqo_graph* g = b->g;
+    const int32_t n = g->n;
+    const int64_t W = body_words(n), cells = int64_t(n) * b->Bp;
+    double* X = b->d_x[b->cur];
+    MQO_CUDA(cudaMemsetAsync(b->d_scores, 0, sizeof(int64_t) * b->Bp, b->stream));
+    MQO_CUDA(cudaMemsetAsync(b->d_valid, 0, sizeof(int32_t) * b->Bp, b->stream));
+    if (n) {
+      if (problem == MQO_PROBLEM_MIS) {
+        k_mis_prepare<<<grid_for(cells), 256, 0, b->stream>>>(g->d_off, g->d_nbr, n, b->B, b->Bp,
+                                                              X, b->d_state8, b->d_valid);
+        k_threshold_mis<<<grid_for(cells), 256, 0, b->stream>>>(X, cells, b->B, b->Bp, b->d_state8);
+      }
+      const int64_t warps = W * b->B;
+      k_pack<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, b->stream>>>(
+          b->d_state8, X, problem == MQO_PROBLEM_MIS, n, b->B, b->Bp, b->d_bodies, W, b->d_scores);
+      if (problem == MQO_PROBLEM_MAXCUT)
+        k_cut<<<grid_for(int64_t(n) * b->B), 256, 0, b->stream>>>(g->d_off, g->d_nbr, n, b->B,
+                                                                  b->d_bodies, W, b->d_scores);
+      MQO_CUDA(cudaGetLastError());
+    }
+    std::vector<int32_t> dep(b->B);
+    MQO_CUDA(cudaMemcpyAsync(dep.data(), b->d_valid, sizeof(int32_t) * b->B, cudaMemcpyDeviceToHost,
+                             b->stream));
+    if (scores)
+      MQO_CUDA(cudaMemcpyAsync(scores, b->d_scores, sizeof(int64_t) * b->B, cudaMemcpyDeviceToHost,
+                               b->stream));
+    if (packed)
+      MQO_CUDA(cudaMemcpyAsync(packed, b->d_bodies, sizeof(uint64_t) * W * b->B,
+                               cudaMemcpyDeviceToHost, b->stream));
+    MQO_CUDA(cudaStreamSynchronize(b->stream));
+    if (independent)
+      for (int i = 0; i < b->B; ++i) independent[i] = dep[i] ? 0 : 1;
+  });
+}

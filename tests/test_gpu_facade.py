@@ -1,0 +1,24 @@
+"""The drop-in C++ API: the reference's unit-test cases compiled against
+paper_2605_06921_b200/cpp/include/mqo/*.hpp and run on the B200
+(cpp/tests/facade_tests.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_facade_cpp_suite(cuda_ok):
+    pkg = os.path.join(ROOT, "paper_2605_06921_b200")
+    exe = os.path.join(pkg, "cpp", "tests", "facade_tests.bin")
+    if not os.path.exists(exe):  # compile against the shipped .so files
+        subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(pkg, "cpp", "include"),
+                        "-I", os.path.join(ROOT, "include"), "-o", exe,
+                        os.path.join(pkg, "cpp", "tests", "facade_tests.cpp"), f"-L{pkg}",
+                        "-lmqo_core_b200", "-lmqo_b200", f"-Wl,-rpath,{pkg}"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
