@@ -161,6 +161,11 @@ int mqo_run_trajectories(mqo_batch* b, const mqo_objective* obj, const mqo_optim
  * range. */
 int mqo_mis_fixed_point_check(mqo_batch* b, double gamma, double alpha, int32_t* fixed);
 
+/* Tuning knobs of the fused kernels, for measurement scripts:
+ * "k1_variant" (K1 instantiation, 0 = default) and "hot_frac" (fraction of
+ * L2 kept for gathers of hot rows).  Not needed for normal use. */
+int mqo_tune(const char* key, double value);
+
 /* ---- per-chain random streams (rng.hpp:13-86) ---------------------------
  * The complete state of an mqo::Rng: xoshiro256** words plus the cached
  * Box-Muller spare.  Chain b of a batch owns one stream. */

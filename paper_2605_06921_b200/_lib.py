@@ -84,6 +84,7 @@ SIGNATURES: dict[str, tuple] = {
     "mqo_reset_from_pool": (C.c_int, [_P, C.c_int32, C.c_double, _I32]),
     "mqo_harvest": (C.c_int, [_P, C.c_int32, _I64, _I32, _U64]),
     "mqo_local_search": (C.c_int, [_P, C.c_int32, C.c_int32, _U64, _I64]),
+    "mqo_tune": (C.c_int, [C.c_char_p, C.c_double]),
 }
 LS_ONE_FLIP, LS_TWO_FLIP, LS_ONE_TWO_FLIP, LS_ONE_TWO_SWAP = range(4)
 

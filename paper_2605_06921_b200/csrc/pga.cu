@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <ctime>
 
 #include "common.cuh"
@@ -66,7 +67,51 @@ struct PassArgs {
   int32_t check_every;
   double conv_tol;
   int32_t is_mis;
+  int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
 };
+
+// Compile-time tuning of the fused kernels: neighbours in flight per lane,
+// minimum resident CTAs per SM (register cap), cache-policy hints.
+// MEM: 0 = two 128-bit ld.cg per lane, 1 = one 256-bit load with L2
+// eviction-priority policies, 2 = one 256-bit load without policies.
+template <int U_, int MINB_, int MEM_>
+struct Tune {
+  static constexpr int U = U_;
+  static constexpr int MINB = MINB_;
+  static constexpr int MEM = MEM_;
+  static constexpr bool HINT = MEM_ != 0;  // 256-bit path
+  static constexpr bool POLICY = MEM_ == 1;
+};
+using TuneDefault = Tune<6, 3, 1>;
+
+// Cache policies: gathers of hot rows are marked L2::evict_last, every
+// streamed access (own row, velocity, stores) L2::evict_first, and nothing
+// allocates in L1 (random gathers have no L1 reuse).  One 256-bit access
+// per lane covers its 4 chains (one 32-byte sector).
+enum Pol : int { kPolNormal = 0, kPolLast = 1, kPolFirst = 2 };
+
+template <int POL>
+__device__ __forceinline__ void ld4(const double* p, double (&o)[4]) {
+  if constexpr (POL == kPolLast)
+    asm volatile("ld.global.L1::no_allocate.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+  else if constexpr (POL == kPolFirst)
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+}
+
+template <bool POLICY>
+__device__ __forceinline__ void st4(double* p, const double (&o)[4]) {
+  if constexpr (POLICY)
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(o[0]), "d"(o[1]), "d"(o[2]), "d"(o[3]) : "memory");
+  else
+    asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "d"(o[0]), "d"(o[1]), "d"(o[2]), "d"(o[3]) : "memory");
+}
 
 template <int CPL>
 __device__ __forceinline__ void ldx(const double* p, double (&o)[CPL]) {
@@ -122,15 +167,20 @@ struct Acc {
 };
 
 // One (row, quad) work unit.
-template <int KIND, int CPL, int MODE, bool CHECK>
+template <int KIND, int CPL, int MODE, bool CHECK, class TU>
 __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __restrict__ X,
                                          double* __restrict__ Xo, int32_t v, int32_t col,
                                          unsigned amask, bool write, Acc<CPL>& acc) {
-  constexpr int U = CPL == 4 ? 8 : 16;
+  constexpr int U = CPL == 4 ? TU::U : 16;
+  constexpr bool HINT = CPL == 4 && TU::HINT;
+  constexpr int kFirst = TU::POLICY ? kPolFirst : kPolNormal;
   const int64_t e0 = __ldg(a.off + v), e1 = __ldg(a.off + v + 1);
   const int64_t rowbase = static_cast<int64_t>(v) * a.Bp + col;
   double xv[CPL];
-  ldx<CPL>(X + rowbase, xv);
+  if constexpr (HINT)
+    ld4<kFirst>(X + rowbase, xv);
+  else
+    ldx<CPL>(X + rowbase, xv);
   double s[CPL];
   int cnt[CPL];
 #pragma unroll
@@ -145,7 +195,17 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
     double val[U][CPL];
 #pragma unroll
     for (int j = 0; j < U; ++j)
-      if (us[j] >= 0) ldx<CPL>(X + static_cast<int64_t>(us[j]) * a.Bp + col, val[j]);
+      if (us[j] >= 0) {
+        const double* src = X + static_cast<int64_t>(us[j]) * a.Bp + col;
+        if constexpr (HINT) {
+          if (TU::POLICY && us[j] < a.hot_rows)
+            ld4<kPolLast>(src, val[j]);
+          else
+            ld4<kPolNormal>(src, val[j]);
+        } else {
+          ldx<CPL>(src, val[j]);
+        }
+      }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (us[j] < 0) break;
@@ -182,7 +242,10 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
   }
   if (!write) return;
   double vv[CPL], xn[CPL];
-  ldx<CPL>(a.v + rowbase, vv);
+  if constexpr (HINT)
+    ld4<kFirst>(a.v + rowbase, vv);
+  else
+    ldx<CPL>(a.v + rowbase, vv);
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     // pga.cpp:82-85: v = beta v + g ; next = clamp(x + alpha v)
@@ -191,13 +254,20 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
     const double d = fabs(ex_sub(xn[c], xv[c]));
     acc.chg[c] = acc.chg[c] < d ? d : acc.chg[c];  // std::max(max_change, d)
   }
+  if constexpr (HINT) {
+    if (amask == 0xF) {
+      st4<TU::POLICY>(a.v + rowbase, vv);
+      st4<TU::POLICY>(Xo + rowbase, xn);
+      return;
+    }
+  }
   stx<CPL>(a.v + rowbase, vv, amask);
   stx<CPL>(Xo + rowbase, xn, amask);
 }
 
 // Walks this thread's (row, quad) units for one pass.  Thread -> quad is
 // fixed for the whole launch so per-chain accumulators live in registers.
-template <int KIND, int CPL, int MODE, bool CHECK>
+template <int KIND, int CPL, int MODE, bool CHECK, class TU>
 __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, double* Xo,
                                           const uint8_t* qmask, bool write, Acc<CPL>& acc,
                                           int32_t& my_q) {
@@ -227,7 +297,7 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
   }
   if (!amask) return;
   for (int32_t r = r0; r < a.n; r += rstep)
-    row_unit<KIND, CPL, MODE, CHECK>(a, X, Xo, __ldg(a.order + r), col, amask, write, acc);
+    row_unit<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, __ldg(a.order + r), col, amask, write, acc);
 }
 
 // Folds thread accumulators into shared per-chain slots.
@@ -243,8 +313,8 @@ __device__ __forceinline__ void fold_to_smem(const Acc<CPL>& acc, int32_t q, uin
 }
 
 // Single-pass kernels: step / gradient / fixed-point check.
-template <int KIND, int CPL, int MODE>
-__global__ void __launch_bounds__(kThreads) k_pass(PassArgs a) {
+template <int KIND, int CPL, int MODE, class TU>
+__global__ void __launch_bounds__(kThreads, TU::MINB) k_pass(PassArgs a) {
   constexpr bool CHECK = MODE == kCheck;
   Acc<CPL> acc;
   int32_t q = 0;
@@ -254,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) k_pass(PassArgs a) {
   // kStep must not read rows another unit already updated, so it writes the
   // other buffer; the host flips `cur` afterwards.
   if constexpr (MODE == kStep) Xo = a.x[a.base ^ 1];
-  pass_rows<KIND, CPL, MODE, CHECK>(a, X, Xo, nullptr, true, acc, q);
+  pass_rows<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, nullptr, true, acc, q);
   if constexpr (CHECK) {
     if (acc.viol) {
 #pragma unroll
@@ -266,8 +336,8 @@ __global__ void __launch_bounds__(kThreads) k_pass(PassArgs a) {
 }
 
 // Cooperative persistent trajectory kernel (K1 + K2).
-template <int KIND, int CPL>
-__global__ void __launch_bounds__(kThreads) k_traj(PassArgs a) {
+template <int KIND, int CPL, class TU>
+__global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned long long smem_u64[];
@@ -304,7 +374,7 @@ __global__ void __launch_bounds__(kThreads) k_traj(PassArgs a) {
     const bool write = !MIS || p <= a.T;  // pass T+1 is check-only (MIS)
     Acc<CPL> acc;
     int32_t q = 0;
-    pass_rows<KIND, CPL, kTraj, MIS>(a, X, Xo, s_qmask, write, acc, q);
+    pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
     fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
     __syncthreads();
     for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
@@ -364,6 +434,95 @@ __global__ void __launch_bounds__(kThreads) k_traj(PassArgs a) {
   }
 }
 
+// One trajectory pass as a plain launch, for large graphs where a pass is
+// long enough that launch latency is irrelevant and the hardware block
+// scheduler balances rows better than a static persistent split.  The stop
+// decisions of pass p run in k_traj_ctl right after it (same stream).
+template <int KIND, int CPL, class TU>
+__global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
+  constexpr bool MIS = KIND == MQO_MIS_QUBO;
+  if (*reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;  // every chain stopped
+  extern __shared__ unsigned long long smem_u64[];
+  unsigned long long* s_chg = smem_u64;
+  uint32_t* s_viol = reinterpret_cast<uint32_t*>(s_chg + a.Bp);
+  uint8_t* s_qmask = reinterpret_cast<uint8_t*>(s_viol + a.Bp);
+  const int32_t p = a.p_begin;
+  const int slot = p % 3;
+  for (int q = threadIdx.x; q < a.Q; q += blockDim.x) {
+    unsigned m = 0;
+    for (int c = 0; c < CPL; ++c) {
+      const int b = q * CPL + c;
+      m |= (b < a.B && a.ctl[b].active) ? (1u << c) : 0u;
+    }
+    s_qmask[q] = static_cast<uint8_t>(m);
+  }
+  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+    s_viol[b] = 0u;
+    s_chg[b] = 0ull;
+  }
+  __syncthreads();
+  const double* X = a.x[(a.base + p - 1) & 1];
+  double* Xo = a.x[(a.base + p) & 1];
+  const bool write = !MIS || p <= a.T;
+  Acc<CPL> acc;
+  int32_t q = 0;
+  pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
+  fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+    if (MIS) {
+      if (s_viol[b]) {
+        uint32_t* gv = a.viol + slot * a.Bp + b;
+        if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
+      }
+    } else if (s_chg[b]) {
+      unsigned long long* gc = a.chg + slot * a.Bp + b;
+      if (*reinterpret_cast<volatile unsigned long long*>(gc) < s_chg[b]) atomicMax(gc, s_chg[b]);
+    }
+  }
+}
+
+// K2 for the per-launch path: one CTA takes pass p's stop decisions
+// (pga.cpp:89-102), clears the next accumulator slot, publishes the count.
+__global__ void k_traj_ctl(PassArgs a) {
+  __shared__ int s_count;
+  if (*reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;
+  const int32_t p = a.p_begin;
+  const int slot = p % 3, next = (p + 1) % 3;
+  if (threadIdx.x == 0) s_count = 0;
+  __syncthreads();
+  int local = 0;
+  for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
+    ChainCtl c = a.ctl[b];
+    if (!c.active) continue;
+    bool stop = false;
+    if (a.is_mis) {
+      const int32_t t = p - 1;
+      if (t >= 1 && t % a.check_every == 0 && a.viol[slot * a.Bp + b] == 0u) {
+        stop = true;
+        c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
+      }
+    } else {
+      const double ch = __longlong_as_double(static_cast<long long>(a.chg[slot * a.Bp + b]));
+      if (ch <= a.conv_tol) {
+        stop = true;
+        c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
+      }
+    }
+    if (stop)
+      a.ctl[b] = c;
+    else
+      ++local;
+  }
+  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
+    a.viol[next * a.Bp + b] = 0u;
+    a.chg[next * a.Bp + b] = 0ull;
+  }
+  if (local) atomicAdd(&s_count, local);
+  __syncthreads();
+  if (threadIdx.x == 0) a.flag[0] = s_count;
+}
+
 // Chains still running at the end: IterCap at iterate T (pga.cpp:109-110).
 __global__ void k_finalize(ChainCtl* ctl, int32_t B, int32_t T, int32_t base) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -392,11 +551,56 @@ __global__ void k_gather_final(double* __restrict__ dst, const double* __restric
 
 using PassFn = void (*)(PassArgs);
 
+// K1 tuning variants (MQO_K1_VARIANT, default 0) -- kept selectable so the
+// choice can be re-measured on new parts; 0 is the measured best.
+int g_k1_variant = [] {
+  const char* e = std::getenv("MQO_K1_VARIANT");
+  return e ? std::atoi(e) : 0;
+}();
+double g_hot_frac = [] {
+  const char* e = std::getenv("MQO_HOT_FRAC");
+  return e ? std::atof(e) : 0.5;
+}();
+int k1_variant() { return g_k1_variant; }
+
+template <int MODE, class TU>
+PassFn pass_fn_tu(int kind, int cpl) {
+#define MQO_K(K)                                                        \
+  case K:                                                               \
+    return cpl == 4 ? k_pass<K, 4, MODE, TU> : k_pass<K, 1, MODE, TU>;
+  switch (kind) {
+    MQO_K(MQO_MIS_QUBO)
+    MQO_K(MQO_LAPLACIAN)
+    MQO_K(MQO_PERTURBED_LAPLACIAN)
+    MQO_K(MQO_ADJACENCY)
+    MQO_K(MQO_PERTURBED_BIAS)
+  }
+#undef MQO_K
+  throw std::invalid_argument("objective: unknown kind");
+}
+
 template <int MODE>
 PassFn pass_fn(int kind, int cpl) {
-#define MQO_K(K)                                              \
-  case K:                                                     \
-    return cpl == 4 ? k_pass<K, 4, MODE> : k_pass<K, 1, MODE>;
+  if constexpr (MODE == kStep) {
+    switch (k1_variant()) {
+      case 1: return pass_fn_tu<MODE, Tune<8, 2, 0>>(kind, cpl);  // round-1 kernel
+      case 2: return pass_fn_tu<MODE, Tune<6, 3, 2>>(kind, cpl);
+      case 3: return pass_fn_tu<MODE, Tune<4, 4, 1>>(kind, cpl);
+      case 4: return pass_fn_tu<MODE, Tune<4, 4, 2>>(kind, cpl);
+      case 5: return pass_fn_tu<MODE, Tune<5, 3, 1>>(kind, cpl);
+      case 6: return pass_fn_tu<MODE, Tune<4, 3, 1>>(kind, cpl);
+      case 7: return pass_fn_tu<MODE, Tune<7, 3, 1>>(kind, cpl);
+      case 8: return pass_fn_tu<MODE, Tune<3, 4, 1>>(kind, cpl);
+      default: break;
+    }
+  }
+  return pass_fn_tu<MODE, TuneDefault>(kind, cpl);
+}
+
+PassFn traj_pass_fn(int kind, int cpl) {
+#define MQO_K(K) \
+  case K:        \
+    return cpl == 4 ? k_traj_pass<K, 4, TuneDefault> : k_traj_pass<K, 1, TuneDefault>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
     MQO_K(MQO_LAPLACIAN)
@@ -411,7 +615,7 @@ PassFn pass_fn(int kind, int cpl) {
 PassFn traj_fn(int kind, int cpl) {
 #define MQO_K(K) \
   case K:        \
-    return cpl == 4 ? k_traj<K, 4> : k_traj<K, 1>;
+    return cpl == 4 ? k_traj<K, 4, TuneDefault> : k_traj<K, 1, TuneDefault>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
     MQO_K(MQO_LAPLACIAN)
@@ -474,6 +678,18 @@ void validate_optimizer(const mqo_optimizer& c) {  // pga.cpp:9-18
   if (c.check_every < 1) throw std::invalid_argument("optimizer: check_every must be >= 1");
 }
 
+// Rows whose gathers are marked L2::evict_last: a prefix of the vertex
+// order (hubs come first in preferential-attachment labelings) sized to
+// MQO_HOT_FRAC (default 0.3) of the L2.
+int32_t hot_rows(const mqo_batch* b) {
+  const double frac = g_hot_frac;
+  static int l2[64] = {0};
+  const int dev = b->g->device;
+  if (!l2[dev]) MQO_CUDA(cudaDeviceGetAttribute(&l2[dev], cudaDevAttrL2CacheSize, dev));
+  const double rows = frac * l2[dev] / (8.0 * b->Bp);
+  return static_cast<int32_t>(std::min<double>(b->g->n, std::max(0.0, rows)));
+}
+
 PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   PassArgs a{};
   const mqo_graph* g = b->g;
@@ -495,7 +711,17 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   a.flag = b->d_flag;
   a.base = b->cur;
   a.is_mis = obj.kind == MQO_MIS_QUBO;
+  a.hot_rows = hot_rows(b);
   return a;
+}
+
+// Problems up to this many (vertex, chain) cells run the persistent kernel.
+int64_t persistent_cells() {
+  static const int64_t c = [] {
+    const char* e = std::getenv("MQO_PERSISTENT_CELLS");
+    return e ? std::atoll(e) : int64_t(1) << 22;
+  }();
+  return c;
 }
 
 double now_monotonic() {
@@ -541,15 +767,25 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
   a.conv_tol = opt.conv_tol;
   a.T = T;
 
-  PassFn fn = traj_fn(obj.kind, b->cpl);
+  // Small problems: one cooperative persistent kernel per 256-pass chunk
+  // (passes separated by grid.sync, launch-free).  Large problems: one
+  // launch per pass + a one-CTA control kernel.
+  const bool persistent = int64_t(g->n) * b->Bp <= persistent_cells();
+  PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl);
   const size_t smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
-  int per_sm = 0;
-  MQO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn),
-                                                         kThreads, smem));
-  if (per_sm < 1) throw std::logic_error("trajectory kernel cannot be resident");
-  const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
-  const int blocks = align_blocks(
-      b, std::max<int64_t>(1, std::min<int64_t>(need, int64_t(per_sm) * sm_count(g->device))));
+  int blocks = pass_blocks(b);
+  if (persistent) {
+    int per_sm = 0;
+    MQO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(fn), kThreads, smem));
+    if (per_sm < 1) throw std::logic_error("trajectory kernel cannot be resident");
+    const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
+    blocks = align_blocks(
+        b, std::max<int64_t>(1, std::min<int64_t>(need, int64_t(per_sm) * sm_count(g->device))));
+  }
+  b->h_flag[0] = b->B;
+  MQO_CUDA(cudaMemcpyAsync(b->d_flag, b->h_flag, sizeof(int32_t), cudaMemcpyHostToDevice,
+                           b->stream));
 
   int32_t last = mis ? T + 1 : T;  // MIS needs one check-only pass for x_T
   int32_t p = 1;
@@ -557,21 +793,34 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
     // Chunks end on multiples of 256 so the deadline is polled where the
     // reference polls it ((iter & 255) == 0, pga.cpp:104-107).
     const int32_t chunk_end = std::min<int32_t>(last + 1, (p / 256 + 1) * 256 + 1);
-    MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * 3 * b->Bp, b->stream));
-    MQO_CUDA(cudaMemsetAsync(b->d_chg, 0, sizeof(unsigned long long) * 3 * b->Bp, b->stream));
-    a.p_begin = p;
-    a.p_end = chunk_end;
     a.T = T;
-    void* args[] = {&a};
-    MQO_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), blocks, kThreads,
-                                         args, smem, b->stream));
+    if (persistent) {
+      MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * 3 * b->Bp, b->stream));
+      MQO_CUDA(cudaMemsetAsync(b->d_chg, 0, sizeof(unsigned long long) * 3 * b->Bp, b->stream));
+      a.p_begin = p;
+      a.p_end = chunk_end;
+      void* args[] = {&a};
+      MQO_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), blocks, kThreads,
+                                           args, smem, b->stream));
+    } else {
+      if (p == 1) {
+        MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * 3 * b->Bp, b->stream));
+        MQO_CUDA(cudaMemsetAsync(b->d_chg, 0, sizeof(unsigned long long) * 3 * b->Bp, b->stream));
+      }
+      for (int32_t q = p; q < chunk_end; ++q) {
+        a.p_begin = q;
+        a.p_end = q + 1;
+        fn<<<blocks, kThreads, smem, b->stream>>>(a);
+        k_traj_ctl<<<1, 256, 0, b->stream>>>(a);
+      }
+      MQO_CUDA(cudaGetLastError());
+    }
     MQO_CUDA(cudaMemcpyAsync(b->h_flag, b->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
                              b->stream));
     MQO_CUDA(cudaStreamSynchronize(b->stream));
     if (b->h_flag[0] == 0) break;
     const int32_t done = chunk_end - 1;  // passes completed
-    if (deadline >= 0.0 && done <= T && (done & 255) == 0 && done < T &&
-        now_monotonic() >= deadline) {
+    if (deadline >= 0.0 && (done & 255) == 0 && done < T && now_monotonic() >= deadline) {
       T = done;  // IterCap at this iterate after (MIS) checking it
       last = mis ? T + 1 : T;
     }
@@ -600,6 +849,21 @@ void read_outcomes(mqo_batch* b, int32_t* iterations, int32_t* reasons) {
 }
 
 }  // namespace mqo_b200
+
+// Tuning knobs of the fused kernels (measurement scripts only):
+//   "k1_variant"  K1 Tune<> instantiation (0 = default), "hot_frac"
+//   fraction of L2 reserved (evict_last) for hot-row gathers.
+extern "C" int mqo_tune(const char* key, double value) {
+  return guard([&] {
+    const std::string k = key ? key : "";
+    if (k == "k1_variant")
+      g_k1_variant = static_cast<int>(value);
+    else if (k == "hot_frac")
+      g_hot_frac = value;
+    else
+      throw std::invalid_argument("mqo_tune: unknown key");
+  });
+}
 
 extern "C" int mqo_step(mqo_batch* b, const mqo_objective* obj, const mqo_optimizer* opt) {
   return guard([&] {

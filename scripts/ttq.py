@@ -1,0 +1,84 @@
+"""Time-to-quality: best MIS size / cut at a fixed wall-clock budget, GPU
+engine vs the reference's CPU solve_pooled on the same graph, seed and
+config (BASELINE.json's second metric).
+
+python scripts/ttq.py --budget 20 [--configs c1,c2,c3] [--out profiles/ttq.json]
+
+The reference runs through oracle/_ref (the compiled reference core) with
+MQO_THREADS = all host cores; the GPU runs the engine through the C ABI.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (generator, problem cfg, B, K)
+    "c1": (("er", 1000, 0.01), dict(objective=0, param=2.0, alpha=0.8, beta=0.3,
+                                    reset_fraction=0.7, reset_rounds=60), 1, 1),
+    "c1_b256": (("er", 1000, 0.01), dict(objective=0, param=2.0, alpha=0.8, beta=0.3,
+                                         reset_fraction=0.7, reset_rounds=60), 256, 8),
+    "c2": (("er", 2000, 6 / 2000), dict(objective=4, param=0.001, alpha=0.0025, beta=0.8,
+                                        reset_fraction=0.8, reset_rounds=90), 1, 1),
+    "c2_b256": (("er", 2000, 6 / 2000), dict(objective=4, param=0.001, alpha=0.0025, beta=0.8,
+                                             reset_fraction=0.8, reset_rounds=90), 256, 8),
+    "c3": (("er", 100000, 1e-4), dict(objective=0, param=2.0, alpha=0.8, beta=0.3,
+                                      reset_fraction=0.6, reset_rounds=60), 256, 8),
+}
+
+
+def run(name, budget, seed, which):
+    import oracle
+    gen, pc, B, K = CONFIGS[name]
+    if which == "gpu":
+        import paper_2605_06921_b200 as P
+        g = P.generate(P.ErSpec(gen[1], gen[2]), seed)
+        spec = P.MisQubo(pc["param"]) if pc["objective"] == 0 else P.PerturbedBias(pc["param"])
+        cfg = P.SolverConfig(objective=spec, optimizer=P.OptimizerConfig(pc["alpha"], pc["beta"]),
+                             reset_fraction=pc["reset_fraction"], reset_rounds=pc["reset_rounds"],
+                             time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K)
+        t0 = time.time()
+        r = P.solve_pooled(g, cfg)
+        return dict(score=r.best_score, outer_loops=r.outer_loops, trajectories=r.trajectories,
+                    iterations=r.total_iterations, wall=time.time() - t0,
+                    edge_chain_per_s=r.total_iterations * 2 * g.m() / max(r.elapsed_secs, 1e-9))
+    L = oracle.load("ref" if oracle.have_ref() else "oracle")
+    os.environ["MQO_THREADS"] = str(os.cpu_count() or 1)
+    g = L.generate_er(gen[1], gen[2], seed)
+    c = oracle.Cfg(time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K, **pc)
+    t0 = time.time()
+    rep, _ = L.solve_pooled(g, c.to_c())
+    return dict(score=rep["score"], outer_loops=rep["outer_loops"],
+                trajectories=rep["trajectories"], iterations=rep["total_iterations"],
+                wall=time.time() - t0,
+                edge_chain_per_s=rep["total_iterations"] * 2 * g.m / max(rep["elapsed_secs"], 1e-9),
+                impl=L.name, threads=os.cpu_count())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--budget", type=float, default=20.0)
+    ap.add_argument("--configs", default="c1,c1_b256,c2,c2_b256")
+    ap.add_argument("--seeds", default="1")
+    ap.add_argument("--which", default="gpu,ref")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    rows = []
+    for name in args.configs.split(","):
+        for seed in [int(s) for s in args.seeds.split(",")]:
+            for which in args.which.split(","):
+                res = run(name, args.budget, seed, which)
+                row = dict(config=name, seed=seed, impl=which, budget_secs=args.budget, **res)
+                print(json.dumps(row), flush=True)
+                rows.append(row)
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(rows, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -162,7 +162,8 @@ sys.path.insert(0, {ROOT!r})
 import torch.distributed as dist
 import paper_2605_06921_b200 as P
 from paper_2605_06921_b200.dist import TorchComm
-dist.init_process_group("gloo")
+import datetime
+dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=120))
 g = P.generate(P.ErSpec(400, 0.03), 7)
 cfg = P.SolverConfig(objective=P.MisQubo(2.0), optimizer=P.OptimizerConfig(0.8, 0.3),
                      reset_fraction=0.6, reset_rounds=6, seed=7, time_budget_secs=600,
@@ -173,10 +174,20 @@ out = dict(score=r.best_score, it=r.total_iterations, acc=r.resets_accepted,
 open(os.environ["OUT"] + str(dist.get_rank()), "w").write(json.dumps(out))
 dist.destroy_process_group()
 """)
-    env = dict(os.environ, OUT=str(tmp_path / "r"))
-    subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                    "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29631",
-                    str(script)], check=True, env=env, timeout=600)
+    # two ranks share this one GPU here: keep to the per-pass kernels (no
+    # cooperative grid barriers competing for one device across processes)
+    env = dict(os.environ, OUT=str(tmp_path / "r"), MQO_PERSISTENT_CELLS="0")
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    proc = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           "--nproc-per-node=2", "--master-addr=127.0.0.1",
+                           f"--master-port={port}", str(script)], env=env, timeout=400,
+                          capture_output=True, text=True)
+    print(proc.stdout[-3000:], proc.stderr[-3000:])
+    assert proc.returncode == 0
     import json
     r0 = json.loads((tmp_path / "r0").read_text())
     r1 = json.loads((tmp_path / "r1").read_text())
