@@ -318,7 +318,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                          "algorithmic_bytes_per_launch": alg,
-                         "kernel": "k_pass<PerturbedBias,4,kStep>"},
+                         "kernel": "k_pass<PerturbedBias,4,kStep,Tune<4,3,1>>"},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(hx.numel() * 8),
                     "d2h_bytes_per_step": int(hout.numel() * 8 + 2 * 4 * B)},

@@ -96,7 +96,11 @@ int mqo_graph_from_edges(int32_t n, int64_t num_edges, const int32_t* eu, const 
 
 /* GraphGenSpec (graph.hpp:67-91) and generate() (graph.cpp:169-178):
  * bit-identical graphs to the reference for the same (spec, seed). */
-enum { MQO_GEN_ER = 0, MQO_GEN_BA = 1, MQO_GEN_SBM = 2 };
+/* MQO_GEN_ER_FAST: O(m) G(n,p) by geometric skipping -- a different draw
+ * sequence from the reference's O(n^2) ER (graph.cpp:107-116, infeasible at
+ * n = 1e7); used for the large configs, with the edge list then fed to both
+ * sides. */
+enum { MQO_GEN_ER = 0, MQO_GEN_BA = 1, MQO_GEN_SBM = 2, MQO_GEN_ER_FAST = 3 };
 typedef struct {
   int32_t kind;
   int32_t n;

@@ -25,7 +25,7 @@ from ._lib import (ADJACENCY, CHECKER_ACCEPTED, CONVERGED, ITER_CAP, LAPLACIAN, 
                    InvalidArgument, LogicError, MqoError, Objective, Optimizer, check, lib)
 
 __all__ = [
-    "Graph", "ErSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
+    "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
@@ -116,6 +116,13 @@ class OptimizerConfig:  # pga.hpp:13-19
 # ------------------------------------------------------------------ graph
 @dataclass(frozen=True)
 class ErSpec:  # graph.hpp:67-70
+    n: int
+    p: float
+
+
+@dataclass(frozen=True)
+class ErFastSpec:
+    """O(m) G(n, p) (geometric skipping); not the reference's draw sequence."""
     n: int
     p: float
 
@@ -222,6 +229,8 @@ def generate(spec, seed: int, device: int = 0) -> Graph:
     s.seed = seed
     if isinstance(spec, ErSpec):
         s.kind, s.n, s.p = 0, spec.n, spec.p
+    elif isinstance(spec, ErFastSpec):
+        s.kind, s.n, s.p = 3, spec.n, spec.p
     elif isinstance(spec, BaSpec):
         s.kind, s.n, s.m_attach = 1, spec.n, spec.m_attach
     elif isinstance(spec, SbmSpec):

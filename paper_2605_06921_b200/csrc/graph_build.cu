@@ -4,6 +4,7 @@
 // reference, so a (spec, seed) pair yields the identical CSR; the result is
 // uploaded to HBM by mqo_graph_upload.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "common.cuh"
@@ -72,6 +73,45 @@ void generate_er(int32_t n, double p, uint64_t seed, std::vector<int64_t>& off,
   for (int32_t u = 0; u < n; ++u)
     for (int32_t v = u + 1; v < n; ++v)
       if (u01_of(xoshiro_next(r)) < p) keys.push_back(key_of(u, v));
+  csr_from_keys(n, keys, off, nbr);
+}
+
+// O(m) Erdos-Renyi G(n, p) by geometric skipping over the canonical
+// (u < v) pair order (Batagelj & Brandes 2005).  NOT the reference's draw
+// sequence (which needs n(n-1)/2 draws: ~49 h at n = 1e7, SURVEY.md section
+// 6); a distinct generator for the large configs whose edge list is fed to
+// both sides.  Stream: Rng(derive_seed(seed, 0xE5F)).
+void generate_er_fast(int32_t n, double p, uint64_t seed, std::vector<int64_t>& off,
+                      std::vector<int32_t>& nbr) {
+  if (n < 0) throw std::invalid_argument("er: negative n");
+  if (p < 0.0 || p > 1.0) throw std::invalid_argument("er: p outside [0,1]");
+  std::vector<uint64_t> keys;
+  if (p > 0.0 && n > 1) {
+    Xoshiro r = xoshiro_seed(derive_seed(seed, 0xE5FULL));
+    const double expect = 0.5 * static_cast<double>(n) * (n - 1.0) * p;
+    keys.reserve(static_cast<size_t>(expect * 1.01 + 1024));
+    const double lq = std::log1p(-p);
+    int64_t u = 0, v = 0;  // current pair (u, v) with v > u; start before (0, 1)
+    for (;;) {
+      double skip;
+      if (p >= 1.0) {
+        skip = 0.0;
+      } else {
+        double x = u01_of(xoshiro_next(r));
+        skip = std::floor(std::log1p(-x) / lq);
+      }
+      // advance (u, v) by skip + 1 pairs in row-major (u < v) order
+      int64_t adv = static_cast<int64_t>(skip) + 1;
+      while (u < n && v + adv >= n) {
+        adv -= (n - 1 - v);
+        ++u;
+        v = u;
+      }
+      if (u >= n - 1) break;
+      v += adv;
+      keys.push_back(key_of(static_cast<int32_t>(u), static_cast<int32_t>(v)));
+    }
+  }
   csr_from_keys(n, keys, off, nbr);
 }
 
@@ -148,6 +188,7 @@ extern "C" int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph*
     switch (spec->kind) {
       case MQO_GEN_ER: generate_er(spec->n, spec->p, spec->seed, off, nbr); break;
       case MQO_GEN_BA: generate_ba(spec->n, spec->m_attach, spec->seed, off, nbr); break;
+      case MQO_GEN_ER_FAST: generate_er_fast(spec->n, spec->p, spec->seed, off, nbr); break;
       case MQO_GEN_SBM:
         generate_sbm(spec->n, spec->k, spec->p_in, spec->p_out, spec->seed, off, nbr);
         break;

@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdlib>
 #include <ctime>
@@ -82,7 +83,13 @@ struct Tune {
   static constexpr bool HINT = MEM_ != 0;  // 256-bit path
   static constexpr bool POLICY = MEM_ == 1;
 };
-using TuneDefault = Tune<6, 3, 1>;
+// Measured on B200 (scripts/tune_k1.py, profiles/r01_tune_k1.txt): 4
+// neighbours in flight x 3 CTAs/SM for the MaxCut objectives, 3 x 4 CTAs/SM
+// for MIS (its checker counters add registers).
+using TuneDefault = Tune<4, 3, 1>;
+using TuneMis = Tune<3, 4, 1>;
+template <int KIND>
+using TuneFor = std::conditional_t<KIND == MQO_MIS_QUBO, TuneMis, TuneDefault>;
 
 // Cache policies: gathers of hot rows are marked L2::evict_last, every
 // streamed access (own row, velocity, stores) L2::evict_first, and nothing
@@ -594,13 +601,14 @@ PassFn pass_fn(int kind, int cpl) {
       default: break;
     }
   }
+  if (kind == MQO_MIS_QUBO) return pass_fn_tu<MODE, TuneMis>(kind, cpl);
   return pass_fn_tu<MODE, TuneDefault>(kind, cpl);
 }
 
 PassFn traj_pass_fn(int kind, int cpl) {
 #define MQO_K(K) \
   case K:        \
-    return cpl == 4 ? k_traj_pass<K, 4, TuneDefault> : k_traj_pass<K, 1, TuneDefault>;
+    return cpl == 4 ? k_traj_pass<K, 4, TuneFor<K>> : k_traj_pass<K, 1, TuneFor<K>>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
     MQO_K(MQO_LAPLACIAN)
@@ -615,7 +623,7 @@ PassFn traj_pass_fn(int kind, int cpl) {
 PassFn traj_fn(int kind, int cpl) {
 #define MQO_K(K) \
   case K:        \
-    return cpl == 4 ? k_traj<K, 4, TuneDefault> : k_traj<K, 1, TuneDefault>;
+    return cpl == 4 ? k_traj<K, 4, TuneFor<K>> : k_traj<K, 1, TuneFor<K>>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
     MQO_K(MQO_LAPLACIAN)
