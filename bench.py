@@ -247,7 +247,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if dist:
         tdist.barrier()
     ms = start.elapsed_time(end)
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{device}")
+    red_dev = f"cuda:{device}" if (not dist or tdist.get_backend() == "nccl") else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if dist:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -284,7 +285,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for _ in range(e2e_steps):
         it_total += e2e_once()
     e2e_dt = time.perf_counter() - t0
-    te = torch.tensor([e2e_dt, float(it_total)], dtype=torch.float64, device=f"cuda:{device}")
+    te = torch.tensor([e2e_dt, float(it_total)], dtype=torch.float64, device=red_dev)
     if dist:
         tmax = te[:1].clone()
         tsum = te[1:].clone()
@@ -342,6 +343,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: several ranks sharing fewer GPUs (gloo for the timing
+    # reductions); production runs one rank per GPU over NCCL
+    backend = os.environ.get("MQO_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        import torch
+        local_rank %= max(1, torch.cuda.device_count())
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -349,7 +356,10 @@ def main():
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        else:
+            tdist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -177,7 +177,18 @@ struct Engine {
   std::vector<int64_t> g_scores;
   std::vector<int32_t> g_valid, g_iters, g_stops;
 
-  bool past_deadline() const { return mono_now() >= deadline; }
+  // Deadline decisions are collective: any rank past the deadline stops
+  // every rank at the same point, so the ranks' merge sequences never
+  // diverge (each decision is one tiny all-gather).
+  bool past_deadline() const {
+    const uint8_t mine = mono_now() >= deadline ? 1 : 0;
+    if (comm.world() == 1) return mine != 0;
+    std::vector<uint8_t> all(comm.world());
+    comm.allgather(&mine, all.data(), 1);
+    for (uint8_t a : all)
+      if (a) return true;
+    return false;
+  }
   bool target_hit() const {
     return have_best && cfg.has_stop_at_score && best.score >= cfg.stop_at_score;
   }
@@ -358,6 +369,31 @@ struct Engine {
       members[i].score = problem == MQO_PROBLEM_MIS ? out[i] : members[i].score + out[i];
   }
 
+  // Phase-3 polish with the pool members dealt round-robin over the ranks,
+  // results all-gathered back (identical on every rank).
+  void polish_sharded(std::vector<Entry>& members) {
+    const int world = comm.world(), rank = comm.rank();
+    if (world == 1) return polish(members);
+    const int count = static_cast<int>(members.size());
+    std::vector<Entry> mine;
+    for (int i = rank; i < count; i += world) mine.push_back(members[i]);
+    polish(mine);
+    const int per = (count + world - 1) / world;
+    const size_t rec = 1 + static_cast<size_t>(W);  // score + body words
+    std::vector<uint64_t> send(per * rec, 0), recv(send.size() * world);
+    for (size_t k = 0; k < mine.size(); ++k) {
+      send[k * rec] = static_cast<uint64_t>(mine[k].score);
+      std::copy(mine[k].body.begin(), mine[k].body.end(), send.begin() + k * rec + 1);
+    }
+    comm.allgather(send.data(), recv.data(), send.size() * sizeof(uint64_t));
+    for (int i = 0; i < count; ++i) {
+      const int r = i % world, k = i / world;
+      const uint64_t* src = recv.data() + (static_cast<size_t>(r) * per + k) * rec;
+      members[i].score = static_cast<int64_t>(src[0]);
+      members[i].body.assign(src + 1, src + rec);
+    }
+  }
+
   void run() {
     validate(cfg);
     problem = cfg.objective == MQO_MIS_QUBO ? MQO_PROBLEM_MIS : MQO_PROBLEM_MAXCUT;
@@ -425,7 +461,7 @@ struct Engine {
       // Phase 3 (314-339)
       if (cfg.local_search && !pool.e.empty() && !past_deadline() && !target_hit()) {
         std::vector<Entry> polished = pool.e;
-        polish(polished);
+        polish_sharded(polished);
         for (auto& s : polished) {
           best_of_ls = std::max(best_of_ls, s.score);
           const bool better = !have_best || s.score > best.score;

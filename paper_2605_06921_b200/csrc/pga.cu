@@ -568,6 +568,10 @@ double g_hot_frac = [] {
   const char* e = std::getenv("MQO_HOT_FRAC");
   return e ? std::atof(e) : 0.5;
 }();
+int g_grid_per_sm = [] {
+  const char* e = std::getenv("MQO_GRID_PER_SM");
+  return e ? std::atoi(e) : 8;
+}();
 int k1_variant() { return g_k1_variant; }
 
 template <int MODE, class TU>
@@ -660,11 +664,11 @@ int align_blocks(const mqo_batch* b, int64_t blocks) {
   return static_cast<int>(blocks);
 }
 
+// Grid of the per-pass kernels: g_grid_per_sm CTAs per SM (grid-stride
+// over rows), never more than the work needs.
 int pass_blocks(const mqo_batch* b) {
   const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
-  // ~8 resident CTAs of 256 threads per SM is the register-limited ceiling;
-  // keep the grid a multiple of the SM count worth of waves.
-  const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * 8;
+  const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * g_grid_per_sm;
   return align_blocks(b, std::max<int64_t>(1, std::min(need, cap)));
 }
 
@@ -868,6 +872,8 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_k1_variant = static_cast<int>(value);
     else if (k == "hot_frac")
       g_hot_frac = value;
+    else if (k == "grid_per_sm")
+      g_grid_per_sm = std::max(1, static_cast<int>(value));
     else
       throw std::invalid_argument("mqo_tune: unknown key");
   });

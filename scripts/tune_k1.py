@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--variants", default="0,1,2,3,4")
     ap.add_argument("--fracs", default="0,0.3,0.5,0.7")
+    ap.add_argument("--grids", default="8")
+    ap.add_argument("--traj", action="store_true", help="also time 20-pass trajectories")
     args = ap.parse_args()
     import torch
     import paper_2605_06921_b200 as P
@@ -40,10 +42,13 @@ def main():
         batch = P.ChainBatch(g, B)
         stream = torch.cuda.ExternalStream(batch.stream)
         ref = None
-        for var in [int(v) for v in args.variants.split(",")]:
-            for frac in [float(f) for f in args.fracs.split(",")]:
+        combos = [(int(v), float(f), int(gr)) for v in args.variants.split(",")
+                  for f in args.fracs.split(",") for gr in args.grids.split(",")]
+        for var, frac, grid in combos:
+            if True:
                 _lib.check(_lib.lib.mqo_tune(b"k1_variant", var))
                 _lib.check(_lib.lib.mqo_tune(b"hot_frac", frac))
+                _lib.check(_lib.lib.mqo_tune(b"grid_per_sm", grid))
                 batch.set_x(X)
                 batch.zero_v()
                 for _ in range(3):
@@ -62,7 +67,15 @@ def main():
                 e.record(stream)
                 e.synchronize()
                 ms = s.elapsed_time(e) / args.steps
-                print(json.dumps({"case": name, "variant": var, "hot_frac": frac,
+                traj_ms = None
+                if args.traj:
+                    tcfg = P.OptimizerConfig(alpha=cfg.alpha, beta=cfg.beta, max_iters=20)
+                    batch.set_x(X)
+                    t0 = time.time()
+                    batch.run_trajectories(spec, tcfg)
+                    traj_ms = round((time.time() - t0) * 1e3 / 20, 4)
+                print(json.dumps({"case": name, "variant": var, "hot_frac": frac, "grid": grid,
+                                  "traj_ms_per_pass_wall": traj_ms,
                                   "ms_per_step": round(ms, 4),
                                   "edge_chain_per_s": nnz * B / ms * 1e3,
                                   "alg_GBps": round(alg / ms / 1e6, 1),
