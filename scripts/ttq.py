@@ -56,7 +56,7 @@ def run(name, budget, seed, which):
                 trajectories=rep["trajectories"], iterations=rep["total_iterations"],
                 wall=time.time() - t0,
                 edge_chain_per_s=rep["total_iterations"] * 2 * g.m / max(rep["elapsed_secs"], 1e-9),
-                impl=L.name, threads=os.cpu_count())
+                ref_impl=L.name, threads=os.cpu_count())
 
 
 def main():
