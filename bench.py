@@ -13,7 +13,7 @@ of every chain.  Metric: edge-chain updates / s = nnz * B / step time.
 * e2e          the same metric through the C-ABI call a user makes
                (mqo_run_trajectories) with pinned host buffers: every step
                copies the B initial states in, runs a bounded trajectory
-               (max_iters = 100) and copies the final states out.
+               (max_iters = 1000) and copies the final states out.
 * roofline     achieved algorithmic GB/s of the fused kernel vs the
                measured HBM copy peak (MEASURED_PEAKS.json).
 * cpu_baseline the reference's own CPU step (oracle/_ref, else the oracle
@@ -43,7 +43,7 @@ M_ATTACH = 5
 GRAPH_SEED = 1
 CHAINS_PER_GPU = 128
 ALPHA, BETA, LAMBDA = 0.0025, 0.8, 0.001
-E2E_ITERS = 100
+E2E_ITERS = 1000
 METRIC = "edge-chain updates/sec of mQO gradient step"
 UNIT = "edge-chain updates/s"
 

@@ -124,7 +124,8 @@ extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
       MQO_CUDA(cudaMalloc(&b->d_viol, sizeof(uint32_t) * 3 * b->Bp));
       MQO_CUDA(cudaMalloc(&b->d_chg, sizeof(unsigned long long) * 3 * b->Bp));
       MQO_CUDA(cudaMalloc(&b->d_flag, sizeof(int32_t) * 4));
-      MQO_CUDA(cudaHostAlloc(&b->h_flag, sizeof(int32_t) * 4, cudaHostAllocDefault));
+      MQO_CUDA(cudaHostAlloc(&b->h_flag, sizeof(int32_t) * 4, cudaHostAllocMapped));
+      b->h_flag[2] = 0;
       MQO_CUDA(cudaStreamSynchronize(b->stream));
     } catch (...) {
       mqo_batch_free(b);

@@ -36,6 +36,10 @@ namespace cg = cooperative_groups;
 using namespace mqo_b200;
 
 namespace mqo_b200 {
+extern bool g_cta_disabled;
+int cta_group(const mqo_batch* b);
+void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt,
+                          double deadline, int G, double (*now)());
 double* aux_buffer(mqo_batch* b);
 void upload_chain_major(mqo_batch* b, const double* host, double* dst);
 void download_chain_major(mqo_batch* b, const double* src, double* host);
@@ -69,6 +73,7 @@ struct PassArgs {
   double conv_tol;
   int32_t is_mis;
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
+  int32_t dbg;               // measurement-only switches (mqo_tune "traj_dbg")
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -448,7 +453,8 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
 template <int KIND, int CPL, class TU>
 __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
-  if (*reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;  // every chain stopped
+  const int dbg = a.dbg;
+  if (!(dbg & 1) && *reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;  // all stopped
   extern __shared__ unsigned long long smem_u64[];
   unsigned long long* s_chg = smem_u64;
   uint32_t* s_viol = reinterpret_cast<uint32_t*>(s_chg + a.Bp);
@@ -459,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
     unsigned m = 0;
     for (int c = 0; c < CPL; ++c) {
       const int b = q * CPL + c;
-      m |= (b < a.B && a.ctl[b].active) ? (1u << c) : 0u;
+      m |= (b < a.B && ((dbg & 1) || a.ctl[b].active)) ? (1u << c) : 0u;
     }
     s_qmask[q] = static_cast<uint8_t>(m);
   }
@@ -474,6 +480,7 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   Acc<CPL> acc;
   int32_t q = 0;
   pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
+  if (dbg & 2) return;
   fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
   __syncthreads();
   for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
@@ -573,6 +580,7 @@ int g_grid_per_sm = [] {
   return e ? std::atoi(e) : 8;
 }();
 int k1_variant() { return g_k1_variant; }
+int g_traj_dbg = 0;
 
 template <int MODE, class TU>
 PassFn pass_fn_tu(int kind, int cpl) {
@@ -724,17 +732,16 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   a.base = b->cur;
   a.is_mis = obj.kind == MQO_MIS_QUBO;
   a.hot_rows = hot_rows(b);
+  a.dbg = g_traj_dbg;
   return a;
 }
 
 // Problems up to this many (vertex, chain) cells run the persistent kernel.
-int64_t persistent_cells() {
-  static const int64_t c = [] {
-    const char* e = std::getenv("MQO_PERSISTENT_CELLS");
-    return e ? std::atoll(e) : int64_t(1) << 22;
-  }();
-  return c;
-}
+int64_t g_persistent_cells = [] {
+  const char* e = std::getenv("MQO_PERSISTENT_CELLS");
+  return e ? std::atoll(e) : int64_t(1) << 22;
+}();
+int64_t persistent_cells() { return g_persistent_cells; }
 
 double now_monotonic() {
   timespec ts;
@@ -770,6 +777,12 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
   int32_t T = opt.max_iters;
   if (g->n == 0) {
     k_finalize<<<(b->B + 255) / 256, 256, 0, b->stream>>>(b->d_ctl, b->B, T, b->cur);
+    return;
+  }
+  // Graphs whose per-chain state fits in SMEM: one CTA per chain, whole
+  // trajectories without grid barriers (traj_cta.cu).
+  if (const int G = cta_group(b)) {
+    run_trajectories_cta(b, obj, opt, deadline, G, now_monotonic);
     return;
   }
   PassArgs a = make_args(b, obj);
@@ -872,6 +885,12 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_k1_variant = static_cast<int>(value);
     else if (k == "hot_frac")
       g_hot_frac = value;
+    else if (k == "traj_dbg")
+      g_traj_dbg = static_cast<int>(value);
+    else if (k == "persistent_cells")
+      g_persistent_cells = static_cast<int64_t>(value);
+    else if (k == "cta_traj")
+      g_cta_disabled = value == 0.0;
     else if (k == "grid_per_sm")
       g_grid_per_sm = std::max(1, static_cast<int>(value));
     else

@@ -28,6 +28,8 @@ CONFIGS = {
                                              reset_fraction=0.8, reset_rounds=90), 256, 8),
     "c3": (("er", 100000, 1e-4), dict(objective=0, param=2.0, alpha=0.8, beta=0.3,
                                       reset_fraction=0.6, reset_rounds=60), 256, 8),
+    "c4": (("ba", 1000000, 5), dict(objective=4, param=0.001, alpha=0.0025, beta=0.8,
+                                    reset_fraction=0.8, reset_rounds=90), 128, 8),
 }
 
 
@@ -36,7 +38,8 @@ def run(name, budget, seed, which):
     gen, pc, B, K = CONFIGS[name]
     if which == "gpu":
         import paper_2605_06921_b200 as P
-        g = P.generate(P.ErSpec(gen[1], gen[2]), seed)
+        g = (P.generate(P.ErSpec(gen[1], gen[2]), seed) if gen[0] == "er"
+             else P.generate(P.BaSpec(gen[1], gen[2]), seed))
         spec = P.MisQubo(pc["param"]) if pc["objective"] == 0 else P.PerturbedBias(pc["param"])
         cfg = P.SolverConfig(objective=spec, optimizer=P.OptimizerConfig(pc["alpha"], pc["beta"]),
                              reset_fraction=pc["reset_fraction"], reset_rounds=pc["reset_rounds"],
@@ -48,7 +51,7 @@ def run(name, budget, seed, which):
                     edge_chain_per_s=r.total_iterations * 2 * g.m() / max(r.elapsed_secs, 1e-9))
     L = oracle.load("ref" if oracle.have_ref() else "oracle")
     os.environ["MQO_THREADS"] = str(os.cpu_count() or 1)
-    g = L.generate_er(gen[1], gen[2], seed)
+    g = L.generate_er(gen[1], gen[2], seed) if gen[0] == "er" else L.generate_ba(gen[1], gen[2], seed)
     c = oracle.Cfg(time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K, **pc)
     t0 = time.time()
     rep, _ = L.solve_pooled(g, c.to_c())

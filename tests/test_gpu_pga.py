@@ -150,13 +150,29 @@ def test_trajectory_kats(P):  # test_pga.cpp:77-119
         P.run_trajectory(P.MisQubo(2.0), k3, [0.4, 0.4, 0.4], P.OptimizerConfig(alpha=0.0))
 
 
+PATHS = {"cta": (1, 1 << 22), "persistent": (0, 1 << 22), "perpass": (0, 0)}
+
+
+@pytest.fixture(params=list(PATHS))
+def traj_path(request, P):
+    """Run the trajectory parity tests through each device path: SMEM
+    one-CTA-per-chain, cooperative persistent, launch-per-pass."""
+    from paper_2605_06921_b200 import _lib
+    cta, cells = PATHS[request.param]
+    _lib.check(_lib.lib.mqo_tune(b"cta_traj", cta))
+    _lib.check(_lib.lib.mqo_tune(b"persistent_cells", cells))
+    yield request.param
+    _lib.check(_lib.lib.mqo_tune(b"cta_traj", 1))
+    _lib.check(_lib.lib.mqo_tune(b"persistent_cells", 1 << 22))
+
+
 @pytest.mark.parametrize("kind,param,alpha,beta,ce", [
     (MIS_QUBO, 2.0, 0.8, 0.3, 1), (MIS_QUBO, 2.0, 0.8, 0.3, 3), (MIS_QUBO, 2.0, 0.3, 0.0, 1),
     (PERTURBED_BIAS, 0.001, 0.0025, 0.8, 1), (PERTURBED_BIAS, 0.001, 0.1, 0.0, 1),
     (PERTURBED_BIAS, 0.001, 0.02, 0.5, 1),
     (LAPLACIAN, 0.0, 0.1, 0.0, 1), (PERTURBED_LAPLACIAN, 0.001, 0.1, 0.0, 1),
     (ADJACENCY, 0.0, 0.05, 0.5, 1)])
-def test_batched_trajectories_vs_oracle(O, P, kind, param, alpha, beta, ce):
+def test_batched_trajectories_vs_oracle(O, P, traj_path, kind, param, alpha, beta, ce):
     """Per-chain TrajectoryOutcome (state bits, iterations, reason) equal
     run_trajectory's for chains that stop at different iterations."""
     og = O.generate_er(400, 0.02, 11)
@@ -178,7 +194,7 @@ def test_batched_trajectories_vs_oracle(O, P, kind, param, alpha, beta, ce):
         assert same(gx[c], x), c
 
 
-def test_trajectory_golden(O, P):
+def test_trajectory_golden(O, P, traj_path):
     z = np.load(os.path.join(GOLD, "steps.npz"))
     g = graphs(O, P)
     for gname, kind in (("c1", MIS_QUBO), ("c2", PERTURBED_BIAS), ("c2", LAPLACIAN),
