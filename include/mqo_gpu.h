@@ -112,6 +112,13 @@ typedef struct {
 } mqo_gen_spec;
 int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph** out);
 
+/* Graph files (graph_io.cpp:74-106): format 0 = binary CSR cache
+ * ("MQOCSR01" n m offsets neighbours), 1 = the reference's canonical text
+ * ("n m" + one "u v" line per edge, u < v).  mqo_graph_load sniffs the
+ * format and uploads to `device` (< 0: host-only). */
+int mqo_graph_save(const mqo_graph* g, const char* path, int32_t format);
+int mqo_graph_load(const char* path, int32_t device, mqo_graph** out);
+
 /* ---- chain batch -------------------------------------------------------
  * A batch of `chains` relaxed states (RelaxedState, objectives.hpp:45-48)
  * plus velocities, the per-chain xoshiro streams and control words, on the

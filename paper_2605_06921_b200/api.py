@@ -154,6 +154,10 @@ lib.mqo_graph_from_edges.argtypes = [C.c_int32, C.c_int64, _I32, _I32, C.c_int32
 lib.mqo_graph_from_edges.restype = C.c_int
 lib.mqo_graph_csr.argtypes = [C.c_void_p, _I64, _I32]
 lib.mqo_graph_csr.restype = C.c_int
+lib.mqo_graph_save.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
+lib.mqo_graph_save.restype = C.c_int
+lib.mqo_graph_load.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]
+lib.mqo_graph_load.restype = C.c_int
 
 
 class Graph:
@@ -195,6 +199,16 @@ class Graph:
         check(lib.mqo_graph_upload(len(off) - 1, _ptr(off, _I64), _ptr(nbr, _I32), device,
                                    C.byref(h)))
         return Graph(h, device)
+
+    @staticmethod
+    def load(path: str, device: int = 0) -> "Graph":
+        """Binary CSR cache or the reference's canonical text (graph_io.cpp:74-106)."""
+        h = C.c_void_p()
+        check(lib.mqo_graph_load(path.encode(), device, C.byref(h)))
+        return Graph(h, device)
+
+    def save(self, path: str, text: bool = False) -> None:
+        check(lib.mqo_graph_save(self._h, path.encode(), 1 if text else 0))
 
     # accessors ------------------------------------------------------------
     def n(self) -> int:

@@ -6,7 +6,10 @@
 
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -17,6 +20,18 @@ namespace mqo_b200 {
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
+
+// MQO_TRACE=1: one stderr line per engine / trajectory stage (debugging).
+bool trace_on();
+#define MQO_TRACE(...)                                   \
+  do {                                                  \
+    if (::mqo_b200::trace_on()) {                       \
+      std::fprintf(stderr, "[mqo %d] ", (int)getpid()); \
+      std::fprintf(stderr, __VA_ARGS__);                \
+      std::fprintf(stderr, "\n");                       \
+      std::fflush(stderr);                              \
+    }                                                   \
+  } while (0)
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;

@@ -205,6 +205,7 @@ struct Engine {
     // exact replay: host Box-Muller with the reference's libm
     std::vector<mqo_rng_state> st(B_local);
     if (mqo_batch_get_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
+    MQO_TRACE("init: streams read");
     std::vector<double> x(static_cast<size_t>(B_local) * n);
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const int threads = static_cast<int>(std::min<unsigned>(hw, static_cast<unsigned>(B_local)));
@@ -216,8 +217,11 @@ struct Engine {
                           x.data() + static_cast<size_t>(c) * n);
       });
     for (auto& th : pool_t) th.join();
+    MQO_TRACE("init: host normals done (%d threads)", threads);
     upload_chain_major(batch, x.data(), batch->d_x[batch->cur]);
+    MQO_TRACE("init: uploaded");
     if (mqo_batch_set_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
+    MQO_TRACE("init: streams written");
   }
 
   void trajectories() {
@@ -447,20 +451,27 @@ struct Engine {
     while (!past_deadline() && !target_hit()) {
       if (cfg.has_max_outer_loops && rep.outer_loops >= cfg.max_outer_loops) break;
       // Phase 1 (solver.cpp:280-296)
+      MQO_TRACE("outer %d: init", rep.outer_loops);
       init_phase();
+      MQO_TRACE("outer %d: trajectories", rep.outer_loops);
       trajectories();
+      MQO_TRACE("outer %d: harvest", rep.outer_loops);
       harvest_and_merge(false);
       // Phase 2 (298-312)
       for (int round = 0; round < cfg.reset_rounds; ++round) {
         if (past_deadline() || target_hit() || pool.e.empty()) break;
+        MQO_TRACE("round %d: reset", round);
         upload_pool();
         reset_from_pool(batch, problem, cfg.reset_fraction);
+        MQO_TRACE("round %d: trajectories", round);
         trajectories();
+        MQO_TRACE("round %d: harvest", round);
         harvest_and_merge(true);
       }
       // Phase 3 (314-339)
       if (cfg.local_search && !pool.e.empty() && !past_deadline() && !target_hit()) {
         std::vector<Entry> polished = pool.e;
+        MQO_TRACE("outer %d: local search", rep.outer_loops);
         polish_sharded(polished);
         for (auto& s : polished) {
           best_of_ls = std::max(best_of_ls, s.score);
@@ -475,6 +486,7 @@ struct Engine {
       ++rep.outer_loops;
     }
     // final polish (344-359)
+    MQO_TRACE("final polish");
     if (cfg.local_search && have_best) {
       std::vector<Entry> p{best};
       polish(p);

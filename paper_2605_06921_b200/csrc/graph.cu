@@ -7,6 +7,7 @@
 // row order sorted by degree descending (stable by id) that the kernels
 // walk so hub rows start first and rows of similar degree share a warp.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -15,6 +16,13 @@ namespace mqo_b200 {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("MQO_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
 
 }  // namespace mqo_b200
 

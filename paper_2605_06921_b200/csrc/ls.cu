@@ -471,6 +471,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   const int32_t n = g->n;
   const int64_t W = body_words(n);
   if (count <= 0) return;
+  MQO_TRACE("local search op %d on %d bodies", op, count);
   LsWork w;
   const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
   MQO_CUDA(cudaMallocAsync(&w.bytes, cells, st));

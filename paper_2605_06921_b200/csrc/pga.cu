@@ -518,7 +518,7 @@ __global__ void k_traj_ctl(PassArgs a) {
       }
     } else {
       const double ch = __longlong_as_double(static_cast<long long>(a.chg[slot * a.Bp + b]));
-      if (ch <= a.conv_tol) {
+      if (ch <= a.conv_tol && !(a.dbg & 4)) {
         stop = true;
         c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
       }

@@ -485,7 +485,9 @@ void ensure_solver_buffers(mqo_batch* b) {
   const int64_t W = body_words(g->n);
   if (!b->d_rng) {
     MQO_CUDA(cudaMalloc(&b->d_rng, sizeof(ChainRng) * b->Bp * 2));  // [0]: live, [Bp]: saved
-    MQO_CUDA(cudaMemset(b->d_rng, 0, sizeof(ChainRng) * b->Bp * 2));
+    // on the batch stream: a legacy-stream memset is not ordered with the
+    // (non-blocking) batch stream and could land after the seeding copy
+    MQO_CUDA(cudaMemsetAsync(b->d_rng, 0, sizeof(ChainRng) * b->Bp * 2, b->stream));
   }
   if (!b->d_bodies) {
     MQO_CUDA(cudaMalloc(&b->d_bodies, sizeof(uint64_t) * std::max<int64_t>(1, W * b->Bp)));
@@ -640,6 +642,7 @@ void harvest_device(mqo_batch* b, int32_t problem) {
       MQO_CUDA(cudaMemcpyAsync(b->h_flag, b->d_counter, sizeof(int32_t) * 2,
                                cudaMemcpyDeviceToHost, b->stream));
       MQO_CUDA(cudaStreamSynchronize(b->stream));
+      MQO_TRACE("greedy round %d: changed %d undecided %d", round, b->h_flag[0], b->h_flag[1]);
       if (b->h_flag[1] == 0) break;
       if (b->h_flag[0] == 0) throw std::logic_error("greedy_maximalize: no progress");
     }

@@ -221,6 +221,7 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   const int threads = std::max(G * 32, std::min(512, ((a.n * G + 31) / 32) * 32));
   fn<<<blocks, threads - threads % G, smem, b->stream>>>(a);
   MQO_CUDA(cudaGetLastError());
+  MQO_TRACE("cta trajectories launched: %d CTAs x %d threads, smem %zu", blocks, threads, smem);
   // wait, raising the stop flag once the deadline has passed
   for (;;) {
     const cudaError_t q = cudaStreamQuery(b->stream);
@@ -229,6 +230,7 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
     if (deadline >= 0.0 && now() >= deadline) *reinterpret_cast<volatile int32_t*>(h_stop) = 1;
     std::this_thread::sleep_for(std::chrono::microseconds(50));
   }
+  MQO_TRACE("cta trajectories done");
 }
 
 }  // namespace mqo_b200

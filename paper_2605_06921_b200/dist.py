@@ -28,9 +28,18 @@ class TorchComm:
             device = (torch.device("cuda", torch.cuda.current_device())
                       if backend == "nccl" else torch.device("cpu"))
         self.device = device
+        import os
+        self.trace = bool(os.environ.get("MQO_COMM_TRACE"))
+        self.calls = 0
 
     def allgather(self, data: bytes) -> bytes:
         torch = self.torch
+        if self.trace:
+            import sys
+            import time
+            self.calls += 1
+            print(f"[comm rank{self.rank}] #{self.calls} {len(data)} B t={time.time():.3f}",
+                  file=sys.stderr, flush=True)
         t = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(self.device)
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)

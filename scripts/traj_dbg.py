@@ -6,7 +6,7 @@ g = P.generate(P.BaSpec(1_000_000, 5), 1)
 b = P.ChainBatch(g, 128)
 X = np.random.default_rng(0).uniform(-1, 1, (128, g.n()))
 spec, cfg = P.PerturbedBias(0.001), P.OptimizerConfig(alpha=0.0025, beta=0.8, max_iters=40)
-for dbg in [0, 1, 2, 3, 0]:
+for dbg in [0, 4, 5, 6, 7, 4]:
     _lib.check(_lib.lib.mqo_tune(b"traj_dbg", dbg))
     b.set_x(X); b.sync()
     t0 = time.time(); b.run_trajectories(spec, cfg); dt = time.time() - t0

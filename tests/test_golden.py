@@ -198,3 +198,20 @@ def test_engine_reports(O, name):
     keys = [str(k) for k in z["report_keys"]]
     assert [rep[k] for k in keys] == z[name + "_report"].tolist()
     assert (body == z[name + "_body"]).all()
+
+
+def test_graph_files_roundtrip(tmp_path):
+    """Binary CSR cache and the reference's canonical text format."""
+    from paper_2605_06921_b200 import Graph, InvalidArgument
+    z = load("graphs")
+    g = Graph.from_csr(z["er2000_off"], z["er2000_nbr"], device=-1)
+    for text in (False, True):
+        p = str(tmp_path / ("g.txt" if text else "g.csr"))
+        g.save(p, text=text)
+        h = Graph.load(p, device=-1)
+        assert (h.csr()[0] == z["er2000_off"]).all() and (h.csr()[1] == z["er2000_nbr"]).all()
+    lines = open(str(tmp_path / "g.txt")).read().split("\n")
+    assert lines[0] == f"{g.n()} {g.m()}"
+    (tmp_path / "bad.txt").write_text("5 2\n0 1\n")
+    with pytest.raises(InvalidArgument, match="truncated"):
+        Graph.load(str(tmp_path / "bad.txt"), device=-1)

@@ -176,7 +176,8 @@ dist.destroy_process_group()
 """)
     # two ranks share this one GPU here: keep to the per-pass kernels (no
     # cooperative grid barriers competing for one device across processes)
-    env = dict(os.environ, OUT=str(tmp_path / "r"), MQO_PERSISTENT_CELLS="0")
+    env = dict(os.environ, OUT=str(tmp_path / "r"), MQO_PERSISTENT_CELLS="0",
+               MQO_COMM_TRACE="1")
     import socket
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
@@ -186,8 +187,12 @@ dist.destroy_process_group()
                            "--nproc-per-node=2", "--master-addr=127.0.0.1",
                            f"--master-port={port}", str(script)], env=env, timeout=400,
                           capture_output=True, text=True)
-    print(proc.stdout[-3000:], proc.stderr[-3000:])
-    assert proc.returncode == 0
+    if proc.returncode != 0:
+        log = os.path.join(ROOT, "gpurun_out", "two_ranks_failure.log")
+        os.makedirs(os.path.dirname(log), exist_ok=True)
+        with open(log, "a") as f:
+            f.write(proc.stdout + "\n----\n" + proc.stderr + "\n====\n")
+    assert proc.returncode == 0, proc.stderr[-4000:]
     import json
     r0 = json.loads((tmp_path / "r0").read_text())
     r1 = json.loads((tmp_path / "r1").read_text())
