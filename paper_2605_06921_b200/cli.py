@@ -1,0 +1,257 @@
+"""`mqo solve` / `mqo gen` on the B200 backend.
+
+    python -m paper_2605_06921_b200.cli solve --problem mis --gen er:1000:10 --seed 1
+    python -m paper_2605_06921_b200.cli gen --gen ba:1000000:5 --seed 1 --out ba.csr
+
+Flags, defaults and the flow follow the reference CLI
+(tools/src/main.cpp:11-46, cli_common.cpp:44-203): generator spec strings,
+preset `auto` (nearest Appendix-G row, explicit flags win), isolated vertices
+stripped before solving and re-embedded after, a RunRecord JSON (report_json
+.cpp:108-137: same fields, bitmaps run-length encoded above 512 vertices)
+and exit codes 0 / 2.  Graph files: the reference's canonical text format or
+this backend's binary CSR cache (`gen --out x.csr`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+import time
+
+import numpy as np
+
+from . import api as P
+
+SCHEMA_VERSION = 1
+EXIT_OK, EXIT_USAGE = 0, 2
+
+MIS_ROWS = [(1000, 100, (0.80, 0.30, 0.70, 60)), (1000, 300, (0.80, 0.45, 0.70, 60)),
+            (1000, 500, (0.80, 0.45, 0.60, 60)), (3000, 100, (0.80, 0.30, 0.60, 60)),
+            (3000, 300, (0.80, 0.45, 0.60, 60)), (3000, 1000, (0.80, 0.45, 0.50, 60)),
+            (10000, 5000, (0.80, 0.75, 0.50, 60)), (20000, 10000, (0.80, 0.75, 0.50, 60)),
+            (30000, 15000, (0.80, 0.75, 0.50, 60))]
+CUT_ROWS = [(100, 50, (0.0025, 0.90, 0.80, 90)), (1000, 100, (0.0025, 0.80, 0.80, 90)),
+            (1000, 500, (0.0025, 0.80, 0.80, 90)), (1000, 800, (0.0025, 0.80, 0.80, 90)),
+            (30000, 15000, (5e-5, 0.80, 0.80, 90)), (30000, 24000, (5e-5, 0.80, 0.80, 90)),
+            (40000, 20000, (5e-5, 0.80, 0.80, 90)), (40000, 32000, (5e-5, 0.80, 0.80, 90))]
+
+
+class UsageError(Exception):
+    pass
+
+
+def preset_for(problem: str, n: int, mean_degree: float):
+    """presets.cpp:43-60: nearest row in (log n, log d) space."""
+    rows = MIS_ROWS if problem == "mis" else CUT_ROWS
+    ln, ld = math.log(max(1.0, n)), math.log(max(1.0, mean_degree))
+    best, out = math.inf, rows[0][2]
+    for rn, rd, p in rows:
+        dist = (ln - math.log(rn)) ** 2 + (ld - math.log(rd)) ** 2
+        if dist < best:
+            best, out = dist, p
+    return out
+
+
+def parse_gen_spec(text: str):
+    """cli_common.cpp:44-75 (+ er-fast:<n>:<d>, the O(m) generator)."""
+    parts = text.split(":")
+    try:
+        if parts[0] in ("er", "er-fast") and len(parts) == 3:
+            n = int(parts[1])
+            p = float(parts[2][1:]) if parts[2].startswith("p") else float(parts[2]) / n
+            return (P.ErSpec if parts[0] == "er" else P.ErFastSpec)(n, p)
+        if parts[0] == "ba" and len(parts) == 3:
+            return P.BaSpec(int(parts[1]), int(parts[2]))
+        if parts[0] == "sbm" and len(parts) == 5:
+            return P.SbmSpec(int(parts[1]), int(parts[2]), float(parts[3]), float(parts[4]))
+    except ValueError as e:
+        raise UsageError(f"cannot parse generator spec '{text}': {e}")
+    raise UsageError(f"unknown generator spec '{text}' (er, er-fast, ba, sbm)")
+
+
+def encode_bits(bits: np.ndarray) -> dict:
+    """report_json.cpp:15-32."""
+    bits = np.asarray(bits, np.uint8)
+    if len(bits) <= 512:
+        return {"encoding": "plain", "bits": [int(b) for b in bits]}
+    change = np.flatnonzero(np.diff(bits)) + 1
+    edges = np.concatenate([[0], change, [len(bits)]])
+    return {"encoding": "rle", "first": int(bits[0]), "runs": np.diff(edges).tolist()}
+
+
+def decode_bits(j: dict, n: int) -> np.ndarray:
+    if j["encoding"] == "plain":
+        out = np.array(j["bits"], np.uint8)
+    else:
+        vals, v = [], j["first"]
+        for r in j["runs"]:
+            vals.append(np.full(r, v, np.uint8))
+            v ^= 1
+        out = np.concatenate(vals) if vals else np.zeros(0, np.uint8)
+    if len(out) != n:
+        raise ValueError("solution bitmap length does not match n")
+    return out
+
+
+OBJECTIVES = {"mis-qubo": lambda a: P.MisQubo(a.gamma if a.gamma is not None else 2.0),
+              "laplacian": lambda a: P.Laplacian(),
+              "perturbed-laplacian": lambda a: P.PerturbedLaplacian(
+                  a.lam if a.lam is not None else 0.001),
+              "adjacency": lambda a: P.Adjacency(),
+              "perturbed-bias": lambda a: P.PerturbedBias(a.lam if a.lam is not None else 0.001)}
+
+
+def build_config(a, g) -> P.SolverConfig:
+    """cli_common.cpp:100-152."""
+    obj_name = a.objective or ("mis-qubo" if a.problem == "mis" else "perturbed-bias")
+    spec = OBJECTIVES[obj_name](a)
+    if (P.problem_of(spec) == P.PROBLEM_MIS) != (a.problem == "mis"):
+        raise UsageError(f"objective '{obj_name}' does not fit problem '{a.problem}'")
+    cfg = P.SolverConfig(objective=spec)
+    if a.preset == "auto":
+        md = 2.0 * g.m() / g.n() if g.n() > 0 else 0.0
+        alpha, mom, rho, tgs = preset_for(a.problem, g.n(), md)
+        cfg.optimizer.alpha, cfg.optimizer.beta = alpha, mom
+        cfg.reset_fraction, cfg.reset_rounds = rho, tgs
+    for flag, setter in (("alpha", lambda v: setattr(cfg.optimizer, "alpha", v)),
+                         ("momentum", lambda v: setattr(cfg.optimizer, "beta", v)),
+                         ("max_iters", lambda v: setattr(cfg.optimizer, "max_iters", v)),
+                         ("conv_tol", lambda v: setattr(cfg.optimizer, "conv_tol", v)),
+                         ("check_every", lambda v: setattr(cfg.optimizer, "check_every", v)),
+                         ("rho", lambda v: setattr(cfg, "reset_fraction", v)),
+                         ("tgs", lambda v: setattr(cfg, "reset_rounds", v)),
+                         ("sigma", lambda v: setattr(cfg, "init_noise", v)),
+                         ("pool_b", lambda v: setattr(cfg, "pool_batch", v)),
+                         ("pool_k", lambda v: setattr(cfg, "pool_keep", v))):
+        if getattr(a, flag) is not None:
+            setter(getattr(a, flag))
+    cfg.time_budget_secs, cfg.seed = a.budget_secs, a.seed
+    cfg.local_search = not a.no_local_search
+    cfg.init_constant, cfg.stop_at_score, cfg.max_outer_loops = (
+        a.init_constant, a.stop_at_score, a.max_outer)
+    return cfg
+
+
+def run_solve(a) -> dict:
+    """cli_common.cpp:154-203 + report_json.cpp:108-137."""
+    if bool(a.graph) == bool(a.gen):
+        raise UsageError("exactly one of --graph and --gen is required")
+    t0 = time.time()
+    if a.graph:
+        g = P.Graph.load(a.graph, device=a.device)
+        desc = {"source": "file", "n": g.n(), "m": g.m(), "path": a.graph}
+    else:
+        g = P.generate(parse_gen_spec(a.gen), a.seed, device=a.device)
+        desc = {"source": "generator", "n": g.n(), "m": g.m(), "spec": a.gen, "seed": a.seed}
+    load_secs = time.time() - t0
+    cfg = build_config(a, g)
+    off, nbr = g.csr()
+    deg = np.diff(off)
+    warnings = []
+    if g.m() > 0 and (deg == 0).any():  # strip isolated vertices, solve, re-embed
+        keep = np.flatnonzero(deg > 0)
+        remap = np.full(g.n(), -1, np.int64)
+        remap[keep] = np.arange(len(keep))
+        src = np.repeat(np.arange(g.n()), deg)
+        mask = src < nbr
+        core = P.Graph.from_edges(len(keep), np.stack([remap[src[mask]], remap[nbr[mask]]], 1),
+                                  device=a.device)
+        rep = P.solve_pooled(core, cfg)
+        body = np.zeros(g.n(), np.uint8)
+        body[keep] = rep.best_body
+        removed = g.n() - len(keep)
+        if a.problem == "mis":
+            body[deg == 0] = 1
+            rep.best_score += removed
+            rep.after_gradient += removed
+            rep.after_reset_loop += removed
+            rep.after_local_search += removed
+        rep.best_body = body
+        rep.warnings.append(f"stripped {removed} isolated vertices before solving")
+    else:
+        rep = P.solve_pooled(g, cfg)
+    warnings = rep.warnings
+    o = cfg.objective
+    obj = {"name": [k for k, f in OBJECTIVES.items() if type(f(a)) is type(o)][0]}
+    if isinstance(o, P.MisQubo):
+        obj["gamma"] = o.gamma
+    elif isinstance(o, (P.PerturbedLaplacian, P.PerturbedBias)):
+        obj["lambda"] = o.lam
+    config = {"objective": obj, "alpha": cfg.optimizer.alpha, "momentum": cfg.optimizer.beta,
+              "max_iters": cfg.optimizer.max_iters, "conv_tol": cfg.optimizer.conv_tol,
+              "check_every": cfg.optimizer.check_every, "rho": cfg.reset_fraction,
+              "tgs": cfg.reset_rounds, "sigma": cfg.init_noise, "budget_secs": cfg.time_budget_secs,
+              "seed": cfg.seed, "local_search": cfg.local_search, "pool_b": cfg.pool_batch,
+              "pool_k": cfg.pool_keep}
+    for k, v in (("init_constant", cfg.init_constant), ("stop_at_score", cfg.stop_at_score),
+                 ("max_outer_loops", cfg.max_outer_loops)):
+        if v is not None:
+            config[k] = v
+    sol = ({"kind": "independent_set", "members": encode_bits(rep.best_body)} if a.problem == "mis"
+           else {"kind": "cut_partition", "side": encode_bits(rep.best_body)})
+    sol["score"] = rep.best_score
+    return {"schema_version": SCHEMA_VERSION, "problem": a.problem, "graph": desc,
+            "config": config, "best_score": rep.best_score,
+            "found_solution": rep.found_solution, "solution": sol,
+            "phases": {"after_gradient": rep.after_gradient,
+                       "after_reset_loop": rep.after_reset_loop,
+                       "after_local_search": rep.after_local_search},
+            "counters": {"outer_loops": rep.outer_loops, "trajectories": rep.trajectories,
+                         "resets_accepted": rep.resets_accepted,
+                         "resets_rejected": rep.resets_rejected,
+                         "iterations": rep.total_iterations},
+            "stop": P.StopReason.names[rep.last_trajectory_stop],
+            "timing": {"solve_secs": rep.elapsed_secs, "graph_load_secs": load_secs},
+            "warnings": warnings, "backend": "b200"}
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="mqo", description="mQO on the B200 backend")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    s = sub.add_parser("solve")
+    s.add_argument("--problem", choices=["mis", "maxcut"], default="mis")
+    s.add_argument("--graph", default="")
+    s.add_argument("--gen", default="")
+    s.add_argument("--budget-secs", type=float, default=10.0)
+    s.add_argument("--seed", type=int, default=1)
+    for f, t in (("alpha", float), ("momentum", float), ("rho", float), ("lambda", float),
+                 ("gamma", float), ("sigma", float), ("conv-tol", float), ("tgs", int),
+                 ("max-iters", int), ("check-every", int), ("pool-b", int), ("pool-k", int),
+                 ("init-constant", float), ("stop-at-score", int), ("max-outer", int)):
+        s.add_argument(f"--{f}", type=t, default=None, dest=f.replace("-", "_").replace(
+            "lambda", "lam"))
+    s.add_argument("--no-local-search", action="store_true")
+    s.add_argument("--objective", choices=list(OBJECTIVES), default="")
+    s.add_argument("--preset", choices=["auto", "none"], default="auto")
+    s.add_argument("--out", default="")
+    s.add_argument("--device", type=int, default=0)
+    gsub = sub.add_parser("gen")
+    gsub.add_argument("--gen", required=True)
+    gsub.add_argument("--seed", type=int, default=1)
+    gsub.add_argument("--out", required=True)
+    gsub.add_argument("--text", action="store_true", help="canonical text instead of binary CSR")
+    a = ap.parse_args(argv)
+    try:
+        if a.cmd == "gen":
+            g = P.generate(parse_gen_spec(a.gen), a.seed, device=-1)
+            g.save(a.out, text=a.text)
+            print(json.dumps({"n": g.n(), "m": g.m(), "out": a.out}))
+            return EXIT_OK
+        rec = run_solve(a)
+        text = json.dumps(rec, sort_keys=True, separators=(",", ":"))
+        if a.out:
+            with open(a.out, "w") as f:
+                f.write(text + "\n")
+        else:
+            print(text)
+        for w in rec["warnings"]:
+            print(f"warning: {w}", file=sys.stderr)
+        return EXIT_OK
+    except (UsageError, P.InvalidArgument, P.LogicError, P.MqoError, OSError, ValueError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_USAGE
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -169,13 +169,11 @@ __device__ __forceinline__ double grad_epi(double acc, double x, double deg, dou
 // Per-thread accumulators of one pass (this thread's fixed quad).
 template <int CPL>
 struct Acc {
-  unsigned viol = 0;     // bit c: chain c of the quad violates the MIS check
-  double chg[CPL];       // max |x_new - x_old|
+  // bit c: chain c of the quad violates the MIS fixed-point check (MIS), or
+  // moved by more than conv_tol this pass (MaxCut: max|dx| <= conv_tol
+  // <=> no element exceeds it, NaN ignored exactly like std::max does)
+  unsigned viol = 0;
   unsigned nonbin = 0;   // kCheck: a state not in {0,1}
-  __device__ Acc() {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) chg[c] = 0.0;
-  }
 };
 
 // One (row, quad) work unit.
@@ -263,8 +261,10 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
     // pga.cpp:82-85: v = beta v + g ; next = clamp(x + alpha v)
     vv[c] = ex_add(ex_mul(a.beta, vv[c]), g[c]);
     xn[c] = clamp_box(ex_add(xv[c], ex_mul(a.alpha, vv[c])), a.lo);
-    const double d = fabs(ex_sub(xn[c], xv[c]));
-    acc.chg[c] = acc.chg[c] < d ? d : acc.chg[c];  // std::max(max_change, d)
+    if constexpr (MODE == kTraj && !CHECK) {  // pga.cpp:86, 99-102
+      const double d = fabs(ex_sub(xn[c], xv[c]));
+      if (d > a.conv_tol && (amask & (1u << c))) acc.viol |= 1u << c;
+    }
   }
   if constexpr (HINT) {
     if (amask == 0xF) {
@@ -314,14 +314,11 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
 
 // Folds thread accumulators into shared per-chain slots.
 template <int CPL>
-__device__ __forceinline__ void fold_to_smem(const Acc<CPL>& acc, int32_t q, uint32_t* s_viol,
-                                             unsigned long long* s_chg, bool chg) {
+__device__ __forceinline__ void fold_to_smem(const Acc<CPL>& acc, int32_t q, uint32_t* s_viol) {
+  if (!acc.viol) return;
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
+  for (int c = 0; c < CPL; ++c)
     if (acc.viol & (1u << c)) atomicOr(s_viol + q * CPL + c, 1u);
-    if (chg && acc.chg[c] > 0.0)
-      atomicMax(s_chg + q * CPL + c, static_cast<unsigned long long>(__double_as_longlong(acc.chg[c])));
-  }
 }
 
 // Single-pass kernels: step / gradient / fixed-point check.
@@ -387,19 +384,12 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
     Acc<CPL> acc;
     int32_t q = 0;
     pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
-    fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
+    fold_to_smem<CPL>(acc, q, s_viol);
     __syncthreads();
     for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
-      if (!s_active[b]) continue;
-      if (MIS) {
-        if (s_viol[b]) {
-          uint32_t* gv = a.viol + slot * a.Bp + b;
-          if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
-        }
-      } else if (s_chg[b]) {
-        unsigned long long* gc = a.chg + slot * a.Bp + b;
-        if (*reinterpret_cast<volatile unsigned long long*>(gc) < s_chg[b]) atomicMax(gc, s_chg[b]);
-      }
+      if (!s_active[b] || !s_viol[b]) continue;
+      uint32_t* gv = a.viol + slot * a.Bp + b;
+      if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
     }
     grid.sync();
 
@@ -417,13 +407,9 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
           stop = true;
           c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
         }
-      } else {
-        const double ch = __longlong_as_double(
-            static_cast<long long>(__ldcg(a.chg + slot * a.Bp + b)));
-        if (ch <= a.conv_tol) {
-          stop = true;
-          c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
-        }
+      } else if (__ldcg(a.viol + slot * a.Bp + b) == 0u) {  // max|dx| <= conv_tol
+        stop = true;
+        c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
       }
       if (stop) {
         s_active[b] = 0;
@@ -481,18 +467,12 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   int32_t q = 0;
   pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
   if (dbg & 2) return;
-  fold_to_smem<CPL>(acc, q, s_viol, s_chg, !MIS);
+  fold_to_smem<CPL>(acc, q, s_viol);
   __syncthreads();
   for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
-    if (MIS) {
-      if (s_viol[b]) {
-        uint32_t* gv = a.viol + slot * a.Bp + b;
-        if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
-      }
-    } else if (s_chg[b]) {
-      unsigned long long* gc = a.chg + slot * a.Bp + b;
-      if (*reinterpret_cast<volatile unsigned long long*>(gc) < s_chg[b]) atomicMax(gc, s_chg[b]);
-    }
+    if (!s_viol[b]) continue;
+    uint32_t* gv = a.viol + slot * a.Bp + b;
+    if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
   }
 }
 
@@ -516,12 +496,9 @@ __global__ void k_traj_ctl(PassArgs a) {
         stop = true;
         c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
       }
-    } else {
-      const double ch = __longlong_as_double(static_cast<long long>(a.chg[slot * a.Bp + b]));
-      if (ch <= a.conv_tol && !(a.dbg & 4)) {
-        stop = true;
-        c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
-      }
+    } else if (a.viol[slot * a.Bp + b] == 0u && !(a.dbg & 4)) {  // max|dx| <= conv_tol
+      stop = true;
+      c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
     }
     if (stop)
       a.ctl[b] = c;
