@@ -192,11 +192,10 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
   else
     ldx<CPL>(X + rowbase, xv);
   double s[CPL];
-  int cnt[CPL];
+  unsigned nbsel = 0;  // bit c: some neighbour of v is selected (x_u > 0.5) in chain c
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     s[c] = 0.0;
-    cnt[c] = 0;
   }
   for (int64_t e = e0; e < e1; e += U) {
     int32_t us[U];
@@ -225,7 +224,7 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
           s[c] = ex_add(s[c], ex_sub(xv[c], val[j][c]));  // graph.cpp:85
         else
           s[c] = ex_add(s[c], val[j][c]);               // graph.cpp:68
-        if constexpr (CHECK) cnt[c] += val[j][c] > 0.5 ? 1 : 0;
+        if constexpr (CHECK) nbsel |= (val[j][c] > 0.5 ? 1u : 0u) << c;
       }
     }
   }
@@ -235,7 +234,8 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       const bool sel = xv[c] > 0.5;
-      const bool bad = sel ? (cnt[c] > 0) : (cnt[c] < 1);
+      const bool any = (nbsel >> c) & 1u;  // count > 0 (pga.cpp:127-133)
+      const bool bad = sel ? any : !any;
       if (bad && (amask & (1u << c))) acc.viol |= 1u << c;
       if constexpr (MODE == kCheck)
         if (xv[c] != 0.0 && xv[c] != 1.0 && (amask & (1u << c))) acc.nonbin = 1;
