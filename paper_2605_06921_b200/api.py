@@ -30,7 +30,7 @@ __all__ = [
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
     "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
-    "solve_maxcut", "init_state_host", "INIT_EXACT", "INIT_DEVICE",
+    "solve_maxcut", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
     "InvalidArgument", "LogicError", "MqoError",
 ]
 

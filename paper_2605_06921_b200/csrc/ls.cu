@@ -119,6 +119,11 @@ __device__ int64_t warp_two_flip_pass(const int64_t* off, const int32_t* nbr, in
   bool improved = true;
   while (improved) {
     improved = false;
+    // exact max(delta) at the start of every scan: the running bound only
+    // grows, and a stale large value would disable the filter
+    dmax = INT_MIN;
+    for (int32_t v = lane; v < n; v += 32) dmax = max(dmax, *reinterpret_cast<volatile int32_t*>(delta + v));
+    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     for (int32_t cb = 0; cb < n; cb += 32) {
       int32_t dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : INT_MIN / 2;
       unsigned mask = __ballot_sync(0xffffffffu, dv + dmax + 2 > 0);
