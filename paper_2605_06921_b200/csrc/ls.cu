@@ -167,6 +167,126 @@ __device__ int64_t warp_two_flip_pass(const int64_t* off, const int32_t* nbr, in
   return total;
 }
 
+// ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
+// cand(v) = exists u in N(v), u > v, opposite side, delta_v + delta_u + 2 > 0:
+// the exact "v acts in this sweep if nothing before it changes" test,
+// computed for every vertex of every body in one grid pass.  The warp then
+// visits candidates only; a joint flip of (v, u) can make a later vertex w a
+// candidate only if delta or side changed at some y in Z = {v,u} U N(v) U
+// N(u) with y = w or y in N(w), y > w -- those w > v are re-marked (cand = 1,
+// a superset: the exact evaluation rejects false positives).
+__global__ void k_two_cand(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                           const int32_t* __restrict__ delta_all, const int32_t* __restrict__ live,
+                           uint8_t* __restrict__ cand_all) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n, v = q % n;
+    if (!live[s]) continue;
+    const uint8_t* side = side_all + s * n;
+    const int32_t* delta = delta_all + s * n;
+    const uint8_t sv = side[v];
+    const int32_t dv = delta[v];
+    uint8_t c = 0;
+    for (int64_t e = off[v + 1] - 1; e >= off[v]; --e) {  // u > v lie at the row's end
+      const int32_t u = nbr[e];
+      if (u <= v) break;
+      if (side[u] != sv && dv + delta[u] + 2 > 0) {
+        c = 1;
+        break;
+      }
+    }
+    cand_all[q] = c;
+  }
+}
+
+__device__ void warp_mark_after_flip(const int64_t* off, const int32_t* nbr, uint8_t* cand,
+                                     int32_t t, int32_t v, int lane) {
+  // y over {t} U N(t); mark y and its smaller neighbours w (w > v only)
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+    const int32_t y = a < e0 ? t : nbr[a];
+    if (y > v) cand[y] = 1;
+    for (int64_t c = off[y]; c < off[y + 1]; ++c) {
+      const int32_t w = nbr[c];
+      if (w >= y) break;  // rows ascending: only w < y
+      if (w > v) cand[w] = 1;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void k_two_scan(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           int32_t n, int32_t count, uint8_t* side_all, int32_t* delta_all,
+                           uint8_t* cand_all, int32_t* live, int64_t* gains) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count || !live[s]) return;
+  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
+  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
+  uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
+  int64_t total = 0;
+  int32_t dmax = INT_MIN;  // unused bound for warp_flip
+  for (int32_t cb = 0; cb < n; cb += 32) {
+    bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+    unsigned mask = __ballot_sync(0xffffffffu, f);
+    while (mask) {
+      const int i = warp_first(mask);
+      const int32_t v = cb + i;
+      const int64_t e1 = off[v + 1];
+      int64_t e = off[v];
+      while (e < e1) {
+        const int64_t my = e + lane;
+        bool ok = false;
+        int32_t u = 0, joint = 0;
+        if (my < e1) {
+          u = nbr[my];
+          const uint8_t sv = *reinterpret_cast<volatile uint8_t*>(side + v);
+          if (u > v && *reinterpret_cast<volatile uint8_t*>(side + u) != sv) {
+            joint = *reinterpret_cast<volatile int32_t*>(delta + v) +
+                    *reinterpret_cast<volatile int32_t*>(delta + u) + 2;
+            ok = joint > 0;
+          }
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, ok);
+        if (!hit) {
+          e += 32;
+          continue;
+        }
+        const int j = warp_first(hit);
+        const int32_t uu = __shfl_sync(0xffffffffu, u, j);
+        const int32_t jj = __shfl_sync(0xffffffffu, joint, j);
+        warp_flip(off, nbr, side, delta, v, lane, dmax);
+        warp_flip(off, nbr, side, delta, uu, lane, dmax);
+        total += jj;
+        warp_mark_after_flip(off, nbr, cand, v, v, lane);
+        warp_mark_after_flip(off, nbr, cand, uu, v, lane);
+        e += j + 1;
+      }
+      f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+      mask = __ballot_sync(0xffffffffu, f) & (i == 31 ? 0u : (~0u << (i + 1)));
+    }
+  }
+  if (lane == 0) {
+    gains[s] += total;
+    live[s] = total > 0 ? 1 : 0;  // improved: sweep again
+  }
+}
+
+// one_flip_pass on the live bodies; gains[s] receives its gain.
+__global__ void k_one_flip(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           int32_t n, int32_t count, uint8_t* side_all, int32_t* delta_all,
+                           const int32_t* live, int64_t* gains) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count || !live[s]) return;
+  int32_t dmax = INT_MIN;
+  const int64_t g = warp_one_flip_pass(off, nbr, n, side_all + static_cast<int64_t>(s) * n,
+                                       delta_all + static_cast<int64_t>(s) * n, lane, dmax);
+  if (lane == 0) gains[s] = g;
+}
+
 __global__ void k_maxcut_ls(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
                             int32_t count, uint8_t* side_all, int32_t* delta_all, int32_t op,
                             int64_t* gains) {
@@ -470,6 +590,84 @@ struct LsWork {
 // (`d_packed`, [count][W]); results written back in place.
 //   op 0 one_flip_pass, 1 two_flip_pass, 2 one_two_flip (MaxCut: out64 =
 //   gain), 3 one_two_swap (MIS: out64 = new size).
+// one_flip_pass / two_flip_pass / one_two_flip (localsearch.cpp:139-190)
+// for `count` bodies: 1-flip passes on one warp per body; 2-flip passes as
+// host-driven sweeps of (grid candidate test, warp candidate scan) until a
+// sweep flips nothing; one_two_flip alternates per body until a round gains
+// nothing.  gains[s] = total gain.
+void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* side, int32_t* delta,
+                           int64_t* d_out, cudaStream_t st) {
+  const int32_t n = g->n;
+  const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
+  const int blocks = (count + kLsWarps - 1) / kLsWarps;
+  int32_t *d_live = nullptr, *d_live2 = nullptr;
+  int64_t *d_g1 = nullptr, *d_g2 = nullptr;
+  uint8_t* d_cand = nullptr;
+  MQO_CUDA(cudaMallocAsync(&d_live, sizeof(int32_t) * count, st));
+  MQO_CUDA(cudaMallocAsync(&d_live2, sizeof(int32_t) * count, st));
+  MQO_CUDA(cudaMallocAsync(&d_g1, sizeof(int64_t) * count, st));
+  MQO_CUDA(cudaMallocAsync(&d_g2, sizeof(int64_t) * count, st));
+  MQO_CUDA(cudaMallocAsync(&d_cand, cells, st));
+  std::vector<int32_t> live(count, 1), live2(count);
+  std::vector<int64_t> total(count, 0), g1(count, 0), g2(count, 0);
+  auto two_flip = [&](const std::vector<int32_t>& who) {
+    MQO_CUDA(cudaMemcpyAsync(d_live2, who.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
+    MQO_CUDA(cudaMemsetAsync(d_g2, 0, sizeof(int64_t) * count, st));
+    for (int sweep = 0;; ++sweep) {
+      k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_live2,
+                                                 d_cand);
+      k_two_scan<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_cand,
+                                                   d_live2, d_g2);
+      MQO_CUDA(cudaGetLastError());
+      MQO_CUDA(cudaMemcpyAsync(live2.data(), d_live2, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
+      MQO_CUDA(cudaStreamSynchronize(st));
+      bool any = false;
+      for (int i = 0; i < count; ++i) any |= live2[i] != 0;
+      MQO_TRACE("two_flip sweep %d", sweep);
+      if (!any) break;
+    }
+    MQO_CUDA(cudaMemcpyAsync(g2.data(), d_g2, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaStreamSynchronize(st));
+  };
+  auto one_flip = [&](const std::vector<int32_t>& who) {
+    MQO_CUDA(cudaMemcpyAsync(d_live, who.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
+    MQO_CUDA(cudaMemsetAsync(d_g1, 0, sizeof(int64_t) * count, st));
+    k_one_flip<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_live, d_g1);
+    MQO_CUDA(cudaGetLastError());
+    MQO_CUDA(cudaMemcpyAsync(g1.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaStreamSynchronize(st));
+  };
+  if (op == 0) {
+    one_flip(live);
+    total = g1;
+  } else if (op == 1) {
+    two_flip(live);
+    total = g2;
+  } else {
+    for (int round = 0;; ++round) {
+      bool any = false;
+      for (int i = 0; i < count; ++i) any |= live[i] != 0;
+      if (!any) break;
+      one_flip(live);
+      two_flip(live);
+      for (int i = 0; i < count; ++i) {
+        if (!live[i]) continue;
+        const int64_t r = g1[i] + g2[i];
+        total[i] += r;
+        if (r == 0) live[i] = 0;  // localsearch.cpp:187-188
+      }
+      MQO_TRACE("one_two_flip round %d", round);
+    }
+  }
+  MQO_CUDA(cudaMemcpyAsync(d_out, total.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st));
+  MQO_CUDA(cudaStreamSynchronize(st));
+  cudaFreeAsync(d_live, st);
+  cudaFreeAsync(d_live2, st);
+  cudaFreeAsync(d_g1, st);
+  cudaFreeAsync(d_g2, st);
+  cudaFreeAsync(d_cand, st);
+}
+
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
                          int64_t* d_out, cudaStream_t st) {
   mqo_graph* g = b->g;
@@ -490,9 +688,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (op <= 2) {
     k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
     MQO_CUDA(cudaGetLastError());
-    k_maxcut_ls<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
-                                                  op, d_out);
-    MQO_CUDA(cudaGetLastError());
+    maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
   } else {
     k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.small);
     MQO_CUDA(cudaGetLastError());
