@@ -23,14 +23,15 @@ void set_error(const std::string& msg);
 
 // MQO_TRACE=1: one stderr line per engine / trajectory stage (debugging).
 bool trace_on();
-#define MQO_TRACE(...)                                   \
-  do {                                                  \
-    if (::mqo_b200::trace_on()) {                       \
-      std::fprintf(stderr, "[mqo %d] ", (int)getpid()); \
-      std::fprintf(stderr, __VA_ARGS__);                \
-      std::fprintf(stderr, "\n");                       \
-      std::fflush(stderr);                              \
-    }                                                   \
+double trace_clock();
+#define MQO_TRACE(...)                                                          \
+  do {                                                                         \
+    if (::mqo_b200::trace_on()) {                                              \
+      std::fprintf(stderr, "[mqo %d %.6f] ", (int)getpid(), ::mqo_b200::trace_clock()); \
+      std::fprintf(stderr, __VA_ARGS__);                                       \
+      std::fprintf(stderr, "\n");                                              \
+      std::fflush(stderr);                                                     \
+    }                                                                          \
   } while (0)
 
 struct CudaError : std::runtime_error {

@@ -73,7 +73,6 @@ struct PassArgs {
   double conv_tol;
   int32_t is_mis;
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
-  int32_t dbg;               // measurement-only switches (mqo_tune "traj_dbg")
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -439,8 +438,7 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
 template <int KIND, int CPL, class TU>
 __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
-  const int dbg = a.dbg;
-  if (!(dbg & 1) && *reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;  // all stopped
+  if (*reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;  // every chain stopped
   extern __shared__ unsigned long long smem_u64[];
   unsigned long long* s_chg = smem_u64;
   uint32_t* s_viol = reinterpret_cast<uint32_t*>(s_chg + a.Bp);
@@ -451,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
     unsigned m = 0;
     for (int c = 0; c < CPL; ++c) {
       const int b = q * CPL + c;
-      m |= (b < a.B && ((dbg & 1) || a.ctl[b].active)) ? (1u << c) : 0u;
+      m |= (b < a.B && a.ctl[b].active) ? (1u << c) : 0u;
     }
     s_qmask[q] = static_cast<uint8_t>(m);
   }
@@ -466,7 +464,6 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   Acc<CPL> acc;
   int32_t q = 0;
   pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
-  if (dbg & 2) return;
   fold_to_smem<CPL>(acc, q, s_viol);
   __syncthreads();
   for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
@@ -496,7 +493,7 @@ __global__ void k_traj_ctl(PassArgs a) {
         stop = true;
         c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
       }
-    } else if (a.viol[slot * a.Bp + b] == 0u && !(a.dbg & 4)) {  // max|dx| <= conv_tol
+    } else if (a.viol[slot * a.Bp + b] == 0u) {  // max|dx| <= conv_tol
       stop = true;
       c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
     }
@@ -557,7 +554,6 @@ int g_grid_per_sm = [] {
   return e ? std::atoi(e) : 8;
 }();
 int k1_variant() { return g_k1_variant; }
-int g_traj_dbg = 0;
 
 template <int MODE, class TU>
 PassFn pass_fn_tu(int kind, int cpl) {
@@ -709,7 +705,6 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   a.base = b->cur;
   a.is_mis = obj.kind == MQO_MIS_QUBO;
   a.hot_rows = hot_rows(b);
-  a.dbg = g_traj_dbg;
   return a;
 }
 
@@ -862,8 +857,6 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_k1_variant = static_cast<int>(value);
     else if (k == "hot_frac")
       g_hot_frac = value;
-    else if (k == "traj_dbg")
-      g_traj_dbg = static_cast<int>(value);
     else if (k == "persistent_cells")
       g_persistent_cells = static_cast<int64_t>(value);
     else if (k == "cta_traj")
