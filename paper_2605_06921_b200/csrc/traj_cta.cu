@@ -1,14 +1,16 @@
-// traj_cta.cu -- trajectories of small graphs, one CTA per chain group.
+// traj_cta.cu -- trajectories of small graphs, one CTA per chain.
 //
 // Same reference path as pga.cu (run_trajectory, pga.cpp:63-111: fused
 // gradient + momentum + clip, MIS fixed-point check, MaxCut ||dx||_inf stop,
-// 256-iteration deadline poll) for graphs whose state fits in shared memory
-// (C1/C2-sized: n x G x 24 B <= ~200 KB).  Chains are independent, so each
-// CTA runs its G chains' whole trajectories with __syncthreads only -- no
-// grid barrier, no per-iteration launch -- and x, v live in SMEM (the CSR
-// is read through L1).  The MIS check of x_t is a second sweep over SMEM
-// right after x_t is formed, in the reference's order.  Arithmetic and
-// summation order are those of the fused kernel (bit-identical).
+// 256-iteration deadline poll) for graphs whose chain state -- and, when it
+// fits, the CSR itself -- fits in shared memory (C1/C2-sized).  Chains are
+// independent, so each CTA runs one chain's whole trajectory with no grid
+// barrier and no per-iteration launch: x (double-buffered) and v live in
+// SMEM, the stop flags are block-wide __syncthreads_or reductions, and every
+// thread takes the (identical) stop decision itself.  The MIS check of x_t is
+// a second SMEM sweep right after x_t is formed, in the reference's order.
+// Arithmetic and summation order are those of the fused kernel
+// (bit-identical).
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
@@ -23,7 +25,8 @@ namespace {
 struct CtaArgs {
   const int64_t* __restrict__ off;
   const int32_t* __restrict__ nbr;
-  int32_t n, B, Bp, G;
+  int32_t n, B, Bp;
+  int64_t nnz;
   double* X;  // [n][Bp] in/out (current buffer)
   ChainCtl* ctl;
   double param, alpha, beta, lo, conv_tol;
@@ -41,129 +44,118 @@ __device__ __forceinline__ double grad_cta(double acc, double x, double deg, dou
   return ex_sub(ex_mul(-2.0, acc), param);
 }
 
-template <int KIND>
+// SMEM_CSR: offsets/neighbours copied to shared memory (int32) when they fit.
+template <int KIND, bool SMEM_CSR>
 __global__ void __launch_bounds__(512) k_traj_cta(CtaArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
   extern __shared__ double sm[];
-  const int G = a.G, cells = a.n * G;
+  const int n = a.n;
   double* xs0 = sm;
-  double* xs1 = sm + cells;
-  double* vs = sm + 2 * cells;
-  __shared__ unsigned long long s_chg[8];
-  __shared__ int s_viol[8], s_active[8], s_final[8], s_iters[8], s_reason[8], s_any;
-  const int b0 = blockIdx.x * G;
+  double* xs1 = sm + n;
+  double* vs = sm + 2 * n;
+  int32_t* s_off = reinterpret_cast<int32_t*>(sm + 3 * n);  // [n+1]   (SMEM_CSR)
+  int32_t* s_nbr = s_off + n + 1;                            // [nnz]   (SMEM_CSR)
+  const int b = blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int my_c = tid % G;  // nt is a multiple of G: a thread keeps one chain
 
-  for (int i = tid; i < cells; i += nt) {
-    const int v = i / G, c = i % G;
-    xs0[i] = a.X[static_cast<int64_t>(v) * a.Bp + b0 + c];
-    vs[i] = 0.0;  // fresh velocity (pga.cpp:75)
+  for (int v = tid; v < n; v += nt) {
+    xs0[v] = a.X[static_cast<int64_t>(v) * a.Bp + b];
+    vs[v] = 0.0;  // fresh velocity (pga.cpp:75)
   }
-  if (tid < G) {
-    s_active[tid] = (b0 + tid < a.B) ? 1 : 0;
-    s_final[tid] = 0;
-    s_iters[tid] = 0;
-    s_reason[tid] = MQO_ITER_CAP;
+  if constexpr (SMEM_CSR) {
+    for (int v = tid; v <= n; v += nt) s_off[v] = static_cast<int32_t>(a.off[v]);
+    for (int64_t e = tid; e < a.nnz; e += nt) s_nbr[e] = a.nbr[e];
   }
   __syncthreads();
+  auto row_begin = [&](int v) -> int32_t {
+    if constexpr (SMEM_CSR) return s_off[v]; else return static_cast<int32_t>(__ldg(a.off + v));
+  };
+  auto nb = [&](int32_t e) -> int32_t {
+    if constexpr (SMEM_CSR) return s_nbr[e]; else return __ldg(a.nbr + e);
+  };
 
   double* xin = xs0;
   double* xout = xs1;
-  int out_buf = 1;
+  int out_buf = 1, final_buf = 0, iters = 0, reason = MQO_ITER_CAP;
   for (int t = 1; t <= a.max_iters; ++t) {
-    if (tid < G) {
-      s_chg[tid] = 0ull;
-      s_viol[tid] = 0;
-    }
-    __syncthreads();
-    const bool active = s_active[my_c] != 0;
-    double my_chg = 0.0;
-    if (active) {
-      for (int i = tid; i < cells; i += nt) {
-        const int v = i / G;
-        const int64_t e0 = __ldg(a.off + v), e1 = __ldg(a.off + v + 1);
-        const double xv = xin[i];
-        double acc = 0.0;
-        for (int64_t e = e0; e < e1; ++e) {
-          const double xu = xin[__ldg(a.nbr + e) * G + my_c];
-          acc = KIND == MQO_LAPLACIAN ? ex_add(acc, ex_sub(xv, xu)) : ex_add(acc, xu);
-        }
-        const double g = grad_cta<KIND>(acc, xv, static_cast<double>(e1 - e0), a.param);
-        const double nv = ex_add(ex_mul(a.beta, vs[i]), g);
-        const double nx = clamp_box(ex_add(xv, ex_mul(a.alpha, nv)), a.lo);
-        const double d = fabs(ex_sub(nx, xv));
-        my_chg = my_chg < d ? d : my_chg;
-        vs[i] = nv;
-        xout[i] = nx;
-      }
-    }
-    if (!MIS && active && my_chg > 0.0)
-      atomicMax(&s_chg[my_c], static_cast<unsigned long long>(__double_as_longlong(my_chg)));
-    __syncthreads();
-    const bool check = MIS && (t % a.check_every == 0);
-    if (check && active) {  // mis_fixed_point_check of binarize(x_t) (pga.cpp:91-98)
-      bool bad = false;
-      for (int i = tid; i < cells && !bad; i += nt) {
-        const int v = i / G;
-        int cnt = 0;
-        for (int64_t e = __ldg(a.off + v); e < __ldg(a.off + v + 1); ++e)
-          cnt += xout[__ldg(a.nbr + e) * G + my_c] > 0.5 ? 1 : 0;
-        bad = xout[i] > 0.5 ? (cnt > 0) : (cnt < 1);
-      }
-      if (bad) atomicOr(&s_viol[my_c], 1);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      bool poll = (t & 255) == 0 && *a.stop_flag;  // deadline, pga.cpp:104-107
-      int any = 0;
-      for (int c = 0; c < G; ++c) {
-        if (!s_active[c]) continue;
-        int reason = -1;
-        if (MIS) {
-          if (check && !s_viol[c]) reason = MQO_CHECKER_ACCEPTED;
-        } else if (__longlong_as_double(static_cast<long long>(s_chg[c])) <= a.conv_tol) {
-          reason = MQO_CONVERGED;
-        }
-        if (reason < 0 && (t == a.max_iters || poll)) reason = MQO_ITER_CAP;
-        if (reason >= 0) {
-          s_active[c] = 0;
-          s_final[c] = out_buf;
-          s_iters[c] = t;
-          s_reason[c] = reason;
+    int exceed = 0;
+    for (int v = tid; v < n; v += nt) {
+      const int32_t e0 = row_begin(v), e1 = row_begin(v + 1);
+      const double xv = xin[v];
+      double acc = 0.0;
+      int32_t e = e0;
+      for (; e + 4 <= e1; e += 4) {  // four indices in flight, summed in order
+        const int32_t u0 = nb(e), u1 = nb(e + 1), u2 = nb(e + 2), u3 = nb(e + 3);
+        const double x0 = xin[u0], x1 = xin[u1], x2 = xin[u2], x3 = xin[u3];
+        if constexpr (KIND == MQO_LAPLACIAN) {
+          acc = ex_add(acc, ex_sub(xv, x0));
+          acc = ex_add(acc, ex_sub(xv, x1));
+          acc = ex_add(acc, ex_sub(xv, x2));
+          acc = ex_add(acc, ex_sub(xv, x3));
         } else {
-          any = 1;
+          acc = ex_add(ex_add(ex_add(ex_add(acc, x0), x1), x2), x3);
         }
       }
-      s_any = any;
+      for (; e < e1; ++e) {
+        const double xu = xin[nb(e)];
+        acc = KIND == MQO_LAPLACIAN ? ex_add(acc, ex_sub(xv, xu)) : ex_add(acc, xu);
+      }
+      const double g = grad_cta<KIND>(acc, xv, static_cast<double>(e1 - e0), a.param);
+      const double nv = ex_add(ex_mul(a.beta, vs[v]), g);
+      const double nx = clamp_box(ex_add(xv, ex_mul(a.alpha, nv)), a.lo);
+      if (!MIS && fabs(ex_sub(nx, xv)) > a.conv_tol) exceed = 1;  // max|dx| > tol
+      vs[v] = nv;
+      xout[v] = nx;
     }
-    __syncthreads();
-    if (!s_any) break;
+    exceed = __syncthreads_or(exceed);  // also publishes xout
+    bool stop = false;
+    if (MIS) {
+      if (t % a.check_every == 0) {  // mis_fixed_point_check(binarize(x_t)), pga.cpp:91-98
+        int bad = 0;
+        for (int v = tid; v < n && !bad; v += nt) {
+          const int32_t e1 = row_begin(v + 1);
+          bool any = false;
+          for (int32_t e = row_begin(v); e < e1 && !any; ++e) any = xout[nb(e)] > 0.5;
+          bad = (xout[v] > 0.5) ? any : !any;
+        }
+        if (!__syncthreads_or(bad)) {
+          stop = true;
+          reason = MQO_CHECKER_ACCEPTED;
+        }
+      }
+    } else if (!exceed) {
+      stop = true;
+      reason = MQO_CONVERGED;
+    }
+    if (!stop && (t == a.max_iters || ((t & 255) == 0 && *a.stop_flag))) {
+      stop = true;  // iteration cap or deadline (pga.cpp:104-110)
+      reason = MQO_ITER_CAP;
+    }
+    if (stop) {
+      final_buf = out_buf;
+      iters = t;
+      break;
+    }
     double* tmp = xin;
     xin = xout;
     xout = tmp;
     out_buf ^= 1;
   }
-  // write every chain's final iterate back to the batch state
-  for (int i = tid; i < cells; i += nt) {
-    const int v = i / G, c = i % G;
-    if (b0 + c >= a.B) continue;
-    const double* src = s_final[c] ? xs1 : xs0;
-    a.X[static_cast<int64_t>(v) * a.Bp + b0 + c] = src[i];
-  }
-  if (tid < G && b0 + tid < a.B)
-    a.ctl[b0 + tid] = ChainCtl{0, s_iters[tid], s_reason[tid], a.cur};
+  const double* src = final_buf ? xs1 : xs0;
+  for (int v = tid; v < n; v += nt) a.X[static_cast<int64_t>(v) * a.Bp + b] = src[v];
+  if (tid == 0) a.ctl[b] = ChainCtl{0, iters, reason, a.cur};
 }
 
 using CtaFn = void (*)(CtaArgs);
 
+template <bool S>
 CtaFn cta_fn(int kind) {
   switch (kind) {
-    case MQO_MIS_QUBO: return k_traj_cta<MQO_MIS_QUBO>;
-    case MQO_LAPLACIAN: return k_traj_cta<MQO_LAPLACIAN>;
-    case MQO_PERTURBED_LAPLACIAN: return k_traj_cta<MQO_PERTURBED_LAPLACIAN>;
-    case MQO_ADJACENCY: return k_traj_cta<MQO_ADJACENCY>;
-    case MQO_PERTURBED_BIAS: return k_traj_cta<MQO_PERTURBED_BIAS>;
+    case MQO_MIS_QUBO: return k_traj_cta<MQO_MIS_QUBO, S>;
+    case MQO_LAPLACIAN: return k_traj_cta<MQO_LAPLACIAN, S>;
+    case MQO_PERTURBED_LAPLACIAN: return k_traj_cta<MQO_PERTURBED_LAPLACIAN, S>;
+    case MQO_ADJACENCY: return k_traj_cta<MQO_ADJACENCY, S>;
+    case MQO_PERTURBED_BIAS: return k_traj_cta<MQO_PERTURBED_BIAS, S>;
   }
   throw std::invalid_argument("objective: unknown kind");
 }
@@ -175,21 +167,26 @@ namespace mqo_b200 {
 constexpr size_t kCtaSmemMax = 200 * 1024;
 bool g_cta_disabled = false;  // mqo_tune("cta_traj", 0)
 
-// Chains per CTA for the SMEM trajectory path (one: the most CTAs), or 0
-// if a chain's state (x double-buffered + v, 24 B per vertex) does not fit.
+size_t cta_state_bytes(const mqo_graph* g) { return static_cast<size_t>(g->n) * 24; }
+size_t cta_csr_bytes(const mqo_graph* g) {
+  return 4 * (static_cast<size_t>(g->n) + 1) + 4 * static_cast<size_t>(2 * g->m);
+}
+
+// 1 when the SMEM trajectory path applies (x double-buffered + v, 24 B per
+// vertex, fits), else 0.
 int cta_group(const mqo_batch* b) {
   static const bool disabled = [] {
     const char* e = std::getenv("MQO_NO_CTA_TRAJ");
     return e && *e && *e != '0';
   }();
   if (disabled || g_cta_disabled) return 0;
-  return static_cast<size_t>(b->g->n) * 24 <= kCtaSmemMax && b->g->n > 0 ? 1 : 0;
+  return b->g->n > 0 && cta_state_bytes(b->g) <= kCtaSmemMax ? 1 : 0;
 }
 
 // Runs the trajectories of every chain from the current x with the SMEM
 // kernel; polls `deadline` from the host and raises the mapped stop flag.
 void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt,
-                          double deadline, int G, double (*now)()) {
+                          double deadline, int /*G*/, double (*now)()) {
   // the batch's mapped pinned words: [2] is the stop flag
   int32_t* h_stop = b->h_flag + 2;
   int32_t* d_stop = nullptr;
@@ -199,9 +196,9 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   a.off = b->g->d_off;
   a.nbr = b->g->d_nbr;
   a.n = b->g->n;
+  a.nnz = 2 * b->g->m;
   a.B = b->B;
   a.Bp = b->Bp;
-  a.G = G;
   a.X = b->d_x[b->cur];
   a.ctl = b->d_ctl;
   a.param = obj.param;
@@ -213,22 +210,23 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   a.check_every = opt.check_every;
   a.cur = b->cur;
   a.stop_flag = d_stop;
-  const size_t smem = sizeof(double) * 3 * static_cast<size_t>(a.n) * G;
-  CtaFn fn = cta_fn(obj.kind);
+  const bool smem_csr = cta_state_bytes(b->g) + cta_csr_bytes(b->g) <= kCtaSmemMax;
+  const size_t smem = cta_state_bytes(b->g) + (smem_csr ? cta_csr_bytes(b->g) : 0);
+  CtaFn fn = smem_csr ? cta_fn<true>(obj.kind) : cta_fn<false>(obj.kind);
   MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const int blocks = (b->B + G - 1) / G;
-  const int threads = std::max(G * 32, std::min(512, ((a.n * G + 31) / 32) * 32));
-  fn<<<blocks, threads - threads % G, smem, b->stream>>>(a);
+  const int threads = std::max(32, std::min(512, ((a.n + 31) / 32) * 32));
+  fn<<<b->B, threads, smem, b->stream>>>(a);
   MQO_CUDA(cudaGetLastError());
-  MQO_TRACE("cta trajectories launched: %d CTAs x %d threads, smem %zu", blocks, threads, smem);
+  MQO_TRACE("cta trajectories launched: %d CTAs x %d threads, smem %zu (csr %s)", b->B, threads,
+            smem, smem_csr ? "smem" : "global");
   // wait, raising the stop flag once the deadline has passed
   for (;;) {
     const cudaError_t q = cudaStreamQuery(b->stream);
     if (q == cudaSuccess) break;
     if (q != cudaErrorNotReady) MQO_CUDA(q);
     if (deadline >= 0.0 && now() >= deadline) *reinterpret_cast<volatile int32_t*>(h_stop) = 1;
-    std::this_thread::sleep_for(std::chrono::microseconds(50));
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
   MQO_TRACE("cta trajectories done");
 }
