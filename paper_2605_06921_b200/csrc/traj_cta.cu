@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(512) k_traj_cta(CtaArgs a) {
       stop = true;
       reason = MQO_CONVERGED;
     }
-    if (!stop && (t == a.max_iters || ((t & 255) == 0 && *a.stop_flag))) {
+    // one thread reads the host flag; the block-wide OR keeps every thread's
+    // decision identical
+    const bool deadline_hit = (t & 255) == 0 && __syncthreads_or(tid == 0 ? *a.stop_flag : 0);
+    if (!stop && (t == a.max_iters || deadline_hit)) {
       stop = true;  // iteration cap or deadline (pga.cpp:104-110)
       reason = MQO_ITER_CAP;
     }
