@@ -113,6 +113,7 @@ extern "C" int mqo_graph_free(mqo_graph* g) {
     cudaFree(g->d_off);
     cudaFree(g->d_nbr);
     cudaFree(g->d_order);
+    cudaFree(g->d_cta);
     delete g;
   });
 }

@@ -37,6 +37,7 @@ using namespace mqo_b200;
 
 namespace mqo_b200 {
 extern bool g_cta_disabled;
+extern int g_cta_cluster;
 int cta_group(const mqo_batch* b);
 void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& opt,
                           double deadline, int G, double (*now)());
@@ -861,6 +862,8 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_persistent_cells = static_cast<int64_t>(value);
     else if (k == "cta_traj")
       g_cta_disabled = value == 0.0;
+    else if (k == "cta_cluster")
+      g_cta_cluster = static_cast<int>(value);
     else if (k == "grid_per_sm")
       g_grid_per_sm = std::max(1, static_cast<int>(value));
     else

@@ -150,20 +150,26 @@ def test_trajectory_kats(P):  # test_pga.cpp:77-119
         P.run_trajectory(P.MisQubo(2.0), k3, [0.4, 0.4, 0.4], P.OptimizerConfig(alpha=0.0))
 
 
-PATHS = {"cta": (1, 1 << 22), "persistent": (0, 1 << 22), "perpass": (0, 0)}
+# (cta_traj, persistent_cells, cta_cluster)
+PATHS = {"cta": (1, 1 << 22, 0), "cta_c1": (1, 1 << 22, 1), "cta_c3": (1, 1 << 22, 3),
+         "cta_c16": (1, 1 << 22, 16), "persistent": (0, 1 << 22, 0), "perpass": (0, 0, 0)}
 
 
 @pytest.fixture(params=list(PATHS))
 def traj_path(request, P):
     """Run the trajectory parity tests through each device path: SMEM
-    one-CTA-per-chain, cooperative persistent, launch-per-pass."""
+    cluster-per-chain (automatic cluster size, and forced 1 / 3 / 16 CTAs
+    per chain -- 16 is clamped to the slice count), cooperative persistent,
+    launch-per-pass."""
     from paper_2605_06921_b200 import _lib
-    cta, cells = PATHS[request.param]
+    cta, cells, clu = PATHS[request.param]
     _lib.check(_lib.lib.mqo_tune(b"cta_traj", cta))
     _lib.check(_lib.lib.mqo_tune(b"persistent_cells", cells))
+    _lib.check(_lib.lib.mqo_tune(b"cta_cluster", clu))
     yield request.param
     _lib.check(_lib.lib.mqo_tune(b"cta_traj", 1))
     _lib.check(_lib.lib.mqo_tune(b"persistent_cells", 1 << 22))
+    _lib.check(_lib.lib.mqo_tune(b"cta_cluster", 0))
 
 
 @pytest.mark.parametrize("kind,param,alpha,beta,ce", [
