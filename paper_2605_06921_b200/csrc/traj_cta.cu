@@ -131,12 +131,13 @@ __device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) 
                "d"(v), "r"(mbar)
                : "memory");
 }
-__device__ __forceinline__ void st_async(uint32_t dst, uint4 v, uint32_t mbar) {
-  asm volatile(
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::
-          "r"(dst),
-      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(mbar)
-      : "memory");
+__device__ __forceinline__ void st_async(uint32_t dst, uint32_t v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(v), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
 }
 
 template <int KIND>
@@ -153,18 +154,18 @@ __device__ __forceinline__ double grad_cta(double acc, double x, double deg, dou
 struct SmemPlan {
   size_t xb;       // doubles per x buffer: Z + 2 (slot Z = zero, +1 keeps 16-byte alignment)
   size_t v_off;    // byte offsets ...
-  size_t fl_off;   // uint4 flag records [2][C]
+  size_t fl_off;   // uint32 flag words [2][C][W] (one per warp of every CTA)
   size_t mb_off;   // 2 mbarriers
   size_t lay_off;  // int32: info [32·ns] | rows [ns] | ELL [max_ell]
   size_t total;
 };
-__host__ __device__ inline SmemPlan smem_plan(int S, int C, int max_slices, int max_ell,
+__host__ __device__ inline SmemPlan smem_plan(int S, int C, int W, int max_slices, int max_ell,
                                               bool smem_lay) {
   SmemPlan p{};
   p.xb = static_cast<size_t>(32) * S + 2;
   p.v_off = 2 * p.xb * 8;
   p.fl_off = p.v_off + static_cast<size_t>(256) * max_slices;
-  p.mb_off = p.fl_off + 2 * static_cast<size_t>(C) * 16;
+  p.mb_off = p.fl_off + ((2 * static_cast<size_t>(C) * W * 4 + 15) & ~static_cast<size_t>(15));
   p.lay_off = p.mb_off + 16;
   p.total = p.lay_off;
   if (smem_lay) p.total += 4 * (static_cast<size_t>(33) * max_slices + max_ell);
@@ -172,8 +173,12 @@ __host__ __device__ inline SmemPlan smem_plan(int S, int C, int max_slices, int 
   return p;
 }
 
-template <int KIND, bool SMEM_LAY>
-__global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
+// LOOKAHEAD (clusters, latency-bound): the next group of four neighbours is
+// loaded while the current one is summed; one CTA per chain is bound by SMEM
+// wavefronts instead and keeps the short loop (32 registers: two 1024-thread
+// CTAs per SM).
+template <int KIND, bool SMEM_LAY, bool LOOKAHEAD>
+__global__ void __launch_bounds__(1024, LOOKAHEAD ? 1 : 2) k_traj_cta(CtaArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int n = a.n, S = a.S, C = a.C, Z = 32 * S;
@@ -181,16 +186,16 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
   const int b = blockIdx.x / C;
   const int s0 = a.own[r], s1 = a.own[r + 1], ns = s1 - s0;
   const int i0 = 32 * s0, i1 = min(n, 32 * s1);  // owned (real) slots
-  const SmemPlan P = smem_plan(S, C, a.max_slices, a.max_ell, SMEM_LAY);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, W = nt >> 5;
+  const SmemPlan P = smem_plan(S, C, W, a.max_slices, a.max_ell, SMEM_LAY);
   double* xb0 = reinterpret_cast<double*>(smraw);
   double* xb1 = xb0 + P.xb;
   double* vs = reinterpret_cast<double*>(smraw + P.v_off);    // [32·ns], by slot - i0
-  uint4* fl_in = reinterpret_cast<uint4*>(smraw + P.fl_off);  // [2][C]
+  uint32_t* fl = reinterpret_cast<uint32_t*>(smraw + P.fl_off);  // [2][C][W]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + P.mb_off);
   int32_t* s_info = reinterpret_cast<int32_t*>(smraw + P.lay_off);  // [32·ns]
   int32_t* s_rows = s_info + 32 * ns;                                 // [ns]
   int32_t* s_ell = s_rows + ns;
-  const int tid = threadIdx.x, nt = blockDim.x;
   const int ell0 = __ldg(a.lay + n + s0);  // first ELL word of the owned slices
 
   for (int i = tid; i < Z + 2; i += nt) {
@@ -202,11 +207,12 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
     const int ell1 = s1 < S ? __ldg(a.lay + n + s1) : a.lay_words;
     for (int i = tid; i < 32 * ns; i += nt) s_info[i] = i0 + i < n ? __ldg(a.lay + i0 + i) : 0;
     for (int s = tid; s < ns; s += nt) s_rows[s] = __ldg(a.lay + n + S + s0 + s);
-    for (int w = tid; w < ell1 - ell0; w += nt) s_ell[w] = __ldg(a.lay + ell0 + w);
+    // + the 128-word look-ahead of the last group (next slices / the Z tail)
+    for (int w = tid; w < ell1 - ell0 + 128; w += nt) s_ell[w] = __ldg(a.lay + ell0 + w);
   }
-  if (C > 1 && tid == 0) {
-    mbar_init(smem_addr(&mbar[0]), 1);
-    mbar_init(smem_addr(&mbar[1]), 1);
+  if (C > 1 && tid == 0) {  // one arrival per warp (+ the peers' transaction bytes)
+    mbar_init(smem_addr(&mbar[0]), W);
+    mbar_init(smem_addr(&mbar[1]), W);
     fence_mbar_init();
   }
   __syncthreads();
@@ -226,10 +232,11 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
     if constexpr (SMEM_LAY) return s_ell[w]; else return __ldg(a.lay + w);
   };
 
-  // bytes this CTA receives per iteration: every peer's real slots + flag record
+  // bytes this CTA receives per iteration: every peer's real slots + its flag words
   uint32_t expect = 0;
   for (int p = 0; p < C; ++p)
-    if (p != r) expect += 8u * static_cast<uint32_t>(min(n, 32 * a.own[p + 1]) - 32 * a.own[p]) + 16u;
+    if (p != r)
+      expect += 8u * static_cast<uint32_t>(min(n, 32 * a.own[p + 1]) - 32 * a.own[p]) + 4u * W;
 
   int final_buf = 0, iters = 0, reason = MQO_ITER_CAP, since_check = 0;
   const int last = MIS ? a.max_iters + 1 : a.max_iters;  // MIS: one check-only pass for x_T
@@ -248,10 +255,32 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
       const double xv = xin[i];
       double acc = 0.0;
       uint32_t any = 0;  // a neighbour is selected in x_{t-1}
-      for (int k = 0; k < rows; k += 4) {  // four indices in flight, summed in order
-        const int w = w0 + 32 * k;
-        const int32_t u0 = ell(w), u1 = ell(w + 32), u2 = ell(w + 64), u3 = ell(w + 96);
-        const double x0 = xin[u0], x1 = xin[u1], x2 = xin[u2], x3 = xin[u3];
+      // groups of four neighbours, summed in order; the next group's indices and
+      // values are loaded while this one is summed (the layout's 128-word tail
+      // keeps the look-ahead past the last group in bounds)
+      int w = w0;
+      double x0, x1, x2, x3;
+      if constexpr (LOOKAHEAD) {
+        x0 = xin[ell(w)];
+        x1 = xin[ell(w + 32)];
+        x2 = xin[ell(w + 64)];
+        x3 = xin[ell(w + 96)];
+      }
+      for (int k = 0; k < rows; k += 4) {
+        double y0, y1, y2, y3;
+        if constexpr (LOOKAHEAD) {
+          w += 128;
+          y0 = xin[ell(w)];
+          y1 = xin[ell(w + 32)];
+          y2 = xin[ell(w + 64)];
+          y3 = xin[ell(w + 96)];
+        } else {
+          x0 = xin[ell(w)];
+          x1 = xin[ell(w + 32)];
+          x2 = xin[ell(w + 64)];
+          x3 = xin[ell(w + 96)];
+          w += 128;
+        }
         if constexpr (KIND == MQO_LAPLACIAN) {
           if (k < deg) acc = ex_add(acc, ex_sub(xv, x0));
           if (k + 1 < deg) acc = ex_add(acc, ex_sub(xv, x1));
@@ -261,6 +290,12 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
           acc = ex_add(ex_add(ex_add(ex_add(acc, x0), x1), x2), x3);
         }
         if constexpr (MIS) any = any_gt_half(any, x0, x1, x2, x3);
+        if constexpr (LOOKAHEAD) {
+          x0 = y0;
+          x1 = y1;
+          x2 = y2;
+          x3 = y3;
+        }
       }
       if constexpr (MIS) {
         if ((xv > 0.5) ? any : !any) flag = 1;  // pga.cpp:127-133 on binarize(x_{t-1})
@@ -277,8 +312,10 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
       }
       if (C > 1) {
         const uint32_t la = smem_addr(xout + i), lm = smem_addr(&mbar[out_buf]);
-        for (int p = 0; p < C; ++p)
-          if (p != r) st_async(map_to_rank(la, p), nx, map_to_rank(lm, p));
+        for (int q = 1; q < C; ++q) {
+          const int p = r + q < C ? r + q : r + q - C;
+          st_async(map_to_rank(la, p), nx, map_to_rank(lm, p));
+        }
       }
     }
     bool deadline_now;
@@ -288,24 +325,33 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
       // thread's decision is identical (poll after iterations 256, 512, ...)
       deadline_now = (t & 255) == 0 && __syncthreads_or(tid == 0 ? *a.stop_flag : 0);
     } else {
-      flag = __syncthreads_or(flag);
+      // no CTA barrier: each warp publishes its flag word to every CTA (its
+      // own by a plain store, peers by st.async) and arrives on the local
+      // mbarrier (release: orders its x_t stores for the other warps)
       const uint32_t mb = smem_addr(&mbar[out_buf]);
-      if (tid == 0) {
-        // rank 0 alone polls the deadline so every CTA sees the same bit
-        const uint32_t dl = (r == 0 && (t & 255) == 0 && *a.stop_flag) ? 1u : 0u;
-        const uint4 rec = make_uint4(flag, dl, 0u, 0u);
-        fl_in[out_buf * C + r] = rec;
-        const uint32_t fdst = smem_addr(&fl_in[out_buf * C + r]);
-        for (int p = 0; p < C; ++p)
-          if (p != r) st_async(map_to_rank(fdst, p), rec, map_to_rank(mb, p));
-        mbar_arrive_expect(mb, expect);
+      uint32_t word = __any_sync(0xffffffffu, flag) ? 1u : 0u;
+      if (lane == 0) {
+        // rank 0's warp 0 alone polls the deadline, so every CTA sees the same bit
+        if (r == 0 && warp == 0 && (t & 255) == 0 && *a.stop_flag) word |= 2u;
+        uint32_t* mine = fl + (out_buf * C + r) * W + warp;
+        *mine = word;
+        const uint32_t fdst = smem_addr(mine);
+        for (int q = 1; q < C; ++q) {
+          const int p = r + q < C ? r + q : r + q - C;
+          st_async(map_to_rank(fdst, p), word, map_to_rank(mb, p));
+        }
+        if (warp == 0)
+          mbar_arrive_expect(mb, expect);
+        else
+          mbar_arrive(mb);
       }
       // x_t of mbar[t & 1] is its ((t-1) >> 1)-th phase
       mbar_wait(mb, ((t - 1) >> 1) & 1);
+      const uint32_t* fw = fl + out_buf * C * W;
       uint32_t f = 0;
-      for (int p = 0; p < C; ++p) f |= fl_in[out_buf * C + p].x;
-      flag = f;
-      deadline_now = fl_in[out_buf * C].y != 0;
+      for (int j = lane; j < C * W; j += 32) f |= fw[j];
+      flag = __reduce_or_sync(0xffffffffu, f) & 1u;
+      deadline_now = (fw[0] & 2u) != 0;
     }
     bool stop = false;
     if (MIS) {
@@ -350,16 +396,20 @@ __global__ void __launch_bounds__(1024) k_traj_cta(CtaArgs a) {
 
 using CtaFn = void (*)(CtaArgs);
 
-template <bool S>
-CtaFn cta_fn(int kind) {
+template <bool S, bool L>
+CtaFn cta_fn_kind(int kind) {
   switch (kind) {
-    case MQO_MIS_QUBO: return k_traj_cta<MQO_MIS_QUBO, S>;
-    case MQO_LAPLACIAN: return k_traj_cta<MQO_LAPLACIAN, S>;
-    case MQO_PERTURBED_LAPLACIAN: return k_traj_cta<MQO_PERTURBED_LAPLACIAN, S>;
-    case MQO_ADJACENCY: return k_traj_cta<MQO_ADJACENCY, S>;
-    case MQO_PERTURBED_BIAS: return k_traj_cta<MQO_PERTURBED_BIAS, S>;
+    case MQO_MIS_QUBO: return k_traj_cta<MQO_MIS_QUBO, S, L>;
+    case MQO_LAPLACIAN: return k_traj_cta<MQO_LAPLACIAN, S, L>;
+    case MQO_PERTURBED_LAPLACIAN: return k_traj_cta<MQO_PERTURBED_LAPLACIAN, S, L>;
+    case MQO_ADJACENCY: return k_traj_cta<MQO_ADJACENCY, S, L>;
+    case MQO_PERTURBED_BIAS: return k_traj_cta<MQO_PERTURBED_BIAS, S, L>;
   }
   throw std::invalid_argument("objective: unknown kind");
+}
+CtaFn cta_fn(int kind, bool smem_lay, bool lookahead) {
+  if (smem_lay) return lookahead ? cta_fn_kind<true, true>(kind) : cta_fn_kind<true, false>(kind);
+  return lookahead ? cta_fn_kind<false, true>(kind) : cta_fn_kind<false, false>(kind);
 }
 
 }  // namespace
@@ -395,23 +445,27 @@ void ensure_cta_layout(mqo_graph* g) {
     words += 32LL * rows;
   }
   if (words > INT32_MAX) throw std::length_error("cta layout too large");
-  lay.resize(static_cast<size_t>(words), Z);  // padding -> the zero slot
+  // padding -> the zero slot; + a 128-word tail for the gather look-ahead
+  lay.resize(static_cast<size_t>(words) + 128, Z);
   for (int32_t i = 0; i < n; ++i) {
     const int32_t v = order[i];
     const int64_t base = lay[n + i / 32] + (i & 31);
     for (int64_t e = g->h_off[v], k = 0; e < g->h_off[v + 1]; ++e, ++k)
       lay[static_cast<size_t>(base + 32 * k)] = slot[g->h_nbr[e]];
   }
-  MQO_CUDA(cudaMalloc(&g->d_cta, sizeof(int32_t) * words));
-  MQO_CUDA(cudaMemcpy(g->d_cta, lay.data(), sizeof(int32_t) * words, cudaMemcpyHostToDevice));
-  g->cta_words = words;
+  MQO_CUDA(cudaMalloc(&g->d_cta, sizeof(int32_t) * lay.size()));
+  MQO_CUDA(cudaMemcpy(g->d_cta, lay.data(), sizeof(int32_t) * lay.size(), cudaMemcpyHostToDevice));
+  g->cta_words = words;  // ELL end (the tail follows)
   g->h_cta_base.assign(lay.begin() + n, lay.begin() + n + S);
   g->h_cta_rows.assign(lay.begin() + n + S, lay.begin() + n + 2 * S);
 }
 
+static int cta_threads(int /*C*/, int max_slices) {
+  return std::max(32, std::min(1024, 32 * max_slices));
+}
 static size_t cta_smem_for(const mqo_graph* g, int C, int max_slices, int max_ell, bool smem_lay) {
   const int S = (g->n + 31) / 32;
-  return smem_plan(S, C, max_slices, max_ell, smem_lay).total;
+  return smem_plan(S, C, cta_threads(C, max_slices) / 32, max_slices, max_ell, smem_lay).total;
 }
 
 // 1 when the SMEM trajectory path applies (two x copies + v fit), else 0.
@@ -451,7 +505,7 @@ static void split_slices(const mqo_graph* g, int C, CtaArgs& a) {
     const int e0 = g->h_cta_base[a.own[r]];
     const int e1 = a.own[r + 1] < S ? g->h_cta_base[a.own[r + 1]] : static_cast<int>(g->cta_words);
     a.max_slices = std::max(a.max_slices, a.own[r + 1] - a.own[r]);
-    a.max_ell = std::max(a.max_ell, e1 - e0);
+    a.max_ell = std::max(a.max_ell, e1 - e0 + 128);  // + look-ahead tail
   }
 }
 
@@ -499,10 +553,10 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   const bool smem_lay = cta_smem_for(g, C, a.max_slices, a.max_ell, true) <= kCtaSmemMax;
   const size_t smem = cta_smem_for(g, C, a.max_slices, a.max_ell, smem_lay);
   if (smem > kCtaSmemMax) throw std::logic_error("cta trajectories: state exceeds SMEM");
-  CtaFn fn = smem_lay ? cta_fn<true>(obj.kind) : cta_fn<false>(obj.kind);
+  CtaFn fn = cta_fn(obj.kind, smem_lay, C > 1);
   MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  const int threads = std::max(32, std::min(1024, 32 * a.max_slices));
+  const int threads = cta_threads(C, a.max_slices);
   if (C == 1) {
     fn<<<b->B, threads, smem, b->stream>>>(a);
   } else {
