@@ -128,7 +128,8 @@ struct mqo_graph {
   int64_t* d_off = nullptr;   // n+1
   int32_t* d_nbr = nullptr;   // 2m
   int32_t* d_order = nullptr; // rows by degree descending (stable by id)
-  int32_t* d_cta = nullptr;   // sliced-ELL layout of the SMEM trajectory path (lazy)
+  int32_t* d_cta = nullptr;   // slot layout of the SMEM trajectory path (lazy)
+  int32_t* d_hmax = nullptr;  // max degree over higher neighbours (2-flip filter, lazy)
   int64_t cta_words = 0;
   std::vector<int32_t> h_cta_rows, h_cta_base;  // per-slice rows / ELL base (host copy)
   std::vector<int64_t> h_off;

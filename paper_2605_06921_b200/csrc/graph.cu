@@ -114,6 +114,7 @@ extern "C" int mqo_graph_free(mqo_graph* g) {
     cudaFree(g->d_nbr);
     cudaFree(g->d_order);
     cudaFree(g->d_cta);
+    cudaFree(g->d_hmax);
     delete g;
   });
 }

@@ -1,5 +1,5 @@
 // ls.cu -- K7/K8 discrete local search with the reference's exact
-// sequential semantics (localsearch.cpp), one warp per solution.
+// sequential semantics (localsearch.cpp).
 //
 //   MaxCut  build_gain_table / apply_flip / one_flip_pass / two_flip_pass /
 //           one_two_flip            localsearch.cpp:17-33, 139-190
@@ -8,11 +8,12 @@
 //
 // The reference scans vertices in index order and commits every improving
 // move immediately, so a move's legality depends on every earlier commit.
-// Gains are built by a grid-parallel kernel; the commit loop then runs on
-// one warp per solution that scans 32 (x8 unrolled) vertices per step with
-// a ballot, jumps straight to the first improving lane and applies the
-// move's neighbourhood update across the lanes -- identical commits in
-// identical order, without touching non-improving vertices one by one.
+// Gains are built by a grid-parallel kernel.  1-flip passes are decided
+// grid-parallel in rounds (a vertex's turn only depends on its lower
+// neighbours' decisions; see k_flip_round).  2-flip sweeps test candidates
+// grid-parallel and commit on one warp per solution that jumps from
+// candidate to candidate with ballots and applies each move's neighbourhood
+// update across the lanes -- identical commits in identical order.
 // (1,2)-swap restarts from vertex 0 after every swap (localsearch.cpp:167-
 // 199); the warp instead keeps the scanned prefix clean and re-examines
 // only the 2-hop neighbourhood a swap can change ("dirty" list), which
@@ -68,70 +69,208 @@ __device__ __forceinline__ void warp_flip(const int64_t* __restrict__ off, const
   __syncwarp();
 }
 
-// one_flip_pass (localsearch.cpp:139-157) on a warp; returns the gain.
-__device__ int64_t warp_one_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
-                                      uint8_t* side, int32_t* delta, int lane, int32_t& dmax) {
-  int64_t total = 0;
-  bool improved = true;
-  while (improved) {
-    improved = false;
-    for (int32_t base = 0; base < n; base += 256) {
-      // 8 chunks of 32 in flight, then resolve them in order
-      int32_t d[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int32_t v = base + k * 32 + lane;
-        d[k] = v < n ? *reinterpret_cast<volatile int32_t*>(delta + v) : 0;
-      }
-      unsigned any = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) any |= __ballot_sync(0xffffffffu, d[k] > 0);
-      if (!any) continue;
-      for (int k = 0; k < 8; ++k) {
-        const int32_t cb = base + k * 32;
-        int32_t dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : 0;
-        unsigned mask = __ballot_sync(0xffffffffu, dv > 0);
-        while (mask) {
-          const int i = warp_first(mask);
-          const int32_t v = cb + i;
-          const int32_t gain = __shfl_sync(0xffffffffu, dv, i);
-          total += gain;
-          warp_flip(off, nbr, side, delta, v, lane, dmax);
-          improved = true;
-          dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : 0;
-          mask = __ballot_sync(0xffffffffu, dv > 0) & (i == 31 ? 0u : (~0u << (i + 1)));
-        }
-      }
+// ---- round-parallel one_flip_pass (localsearch.cpp:139-157) -------------
+// Within a pass the reference flips v iff delta_v > 0 at v's turn.  At that
+// turn the only changes to delta_v since the pass began come from flips of
+// its LOWER neighbours (higher ones are scanned later): a flip of u < v adds
+// c_u(v) = -2 if u and v started the pass on the same side, else +2.  So v's
+// decision is fixed once its lower neighbours' are, and rounds can decide in
+// parallel every vertex whose outcome interval
+//   [d0_v + sum_{u flipped} c + sum_{u undecided} min(0, c),
+//    d0_v + sum_{u flipped} c + sum_{u undecided} max(0, c)]
+// lies entirely above 0 (flip) or at or below 0 (keep) -- exactly the
+// sequential scan's decisions, typically in ~10 rounds (BA(1e6, 5)) instead
+// of n dependent steps.  Decisions are final, so reading a neighbour decided
+// earlier in the same round is safe; state bytes are 0 undecided, 1 keep,
+// 2 flip (one byte: a reader never sees a half-written decision).
+__global__ void k_flip_round(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                             int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                             const int32_t* __restrict__ d0_all, uint8_t* st_all,
+                             const int32_t* __restrict__ live, int32_t* undecided) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n;
+    const int32_t v = static_cast<int32_t>(q - s * n);
+    volatile uint8_t* st = st_all + s * n;
+    if (!live[s] || st[v]) continue;
+    const uint8_t* side = side_all + s * n;
+    const uint8_t sv = side[v];
+    int32_t base = d0_all[q], lo = 0, hi = 0;
+    for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
+      const int32_t u = nbr[e];
+      if (u >= v) break;  // rows ascend: the lower neighbours are a prefix
+      const int32_t c = side[u] == sv ? -2 : 2;
+      const uint8_t su = st[u];
+      if (su == 2)
+        base += c;
+      else if (su == 0)
+        (c < 0 ? lo : hi) += c;
     }
+    if (base + lo > 0)
+      st[v] = 2;
+    else if (base + hi <= 0)
+      st[v] = 1;
+    else
+      undecided[s] = 1;
   }
-  return total;
 }
 
-// two_flip_pass (localsearch.cpp:159-181) on a warp.  A vertex v can host a
-// joint move only if delta_v + max(delta) + 2 > 0; dmax is a running upper
-// bound of every delta, so the filter never skips a vertex the reference
-// would act on.  For a candidate v the warp evaluates 32 neighbours at a
-// time against the current state; after a joint flip it resumes right
-// after the flipped neighbour, exactly like the reference's inner loop.
-__device__ int64_t warp_two_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
-                                      uint8_t* side, int32_t* delta, int lane, int32_t& dmax) {
+// Gain of the pass: sum over flipped v of delta_v at its turn
+// (d0_v + sum of c_u(v) over flipped lower neighbours), per body.
+__global__ void k_flip_commit(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                              int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                              const int32_t* __restrict__ d0_all, const uint8_t* __restrict__ st_all,
+                              const int32_t* __restrict__ live, unsigned long long* gain) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q0 = blockIdx.x * static_cast<int64_t>(blockDim.x); q0 < total;
+       q0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t q = q0 + threadIdx.x;
+    int64_t s = -1;
+    int64_t g = 0;
+    if (q < total) {
+      s = q / n;
+      const int32_t v = static_cast<int32_t>(q - s * n);
+      const uint8_t* st = st_all + s * n;
+      if (live[s] && st[v] == 2) {
+        const uint8_t* side = side_all + s * n;
+        const uint8_t sv = side[v];
+        int32_t at = d0_all[q];
+        for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
+          const int32_t u = nbr[e];
+          if (u >= v) break;
+          if (st[u] == 2) at += side[u] == sv ? -2 : 2;
+        }
+        g = at;
+      }
+    }
+    // bodies are contiguous in q: reduce runs of equal s within the warp
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = __shfl_sync(0xffffffffu, s, 0);
+    const bool uniform = __all_sync(0xffffffffu, s == s0);
+    if (uniform) {
+      for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+      if (lane == 0 && g && s0 >= 0) atomicAdd(gain + s0, static_cast<unsigned long long>(g));
+    } else if (g && s >= 0) {
+      atomicAdd(gain + s, static_cast<unsigned long long>(g));
+    }
+  }
+}
+
+__global__ void k_flip_apply(int32_t n, int32_t count, uint8_t* side_all,
+                             const uint8_t* __restrict__ st_all, const int32_t* __restrict__ live) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (st_all[q] == 2 && live[q / n]) side_all[q] ^= 1;
+  }
+}
+
+// ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
+// cand(v) = exists u in N(v), u > v, opposite side, delta_v + delta_u + 2 > 0:
+// the exact "v acts in this sweep if nothing before it changes" test,
+// computed for every vertex of every body in one grid pass.  The warp then
+// visits candidates only.  A joint flip of (v, u) can change cand(w) for a
+// later vertex w only if delta or side changed at some y in
+// Z = {v,u} U N(v) U N(u) with y = w or y in N(w), y > w -- those w > v are
+// re-marked (a superset, resolved by the exact evaluation at the visit).
+// (Resolving a chunk's marks lane-parallel and re-evaluating exactly at
+// marking time were both tried: slower, as each lane then walks rows
+// serially.)
+// hmax[v] = the largest degree among v's higher neighbours bounds delta_u
+// (delta_u <= deg u), so delta_v + hmax[v] + 2 <= 0 rules v out without
+// reading its row -- hubs of a locally optimal cut are skipped in O(1).
+__device__ __forceinline__ bool two_cand(const int64_t* __restrict__ off,
+                                         const int32_t* __restrict__ nbr, const int32_t* hmax,
+                                         const uint8_t* side, const int32_t* delta, int32_t v) {
+  const int32_t dv = *reinterpret_cast<const volatile int32_t*>(delta + v);
+  if (dv + hmax[v] + 2 <= 0) return false;
+  const uint8_t sv = *reinterpret_cast<const volatile uint8_t*>(side + v);
+  for (int64_t e = off[v + 1] - 1, e0 = off[v]; e >= e0; --e) {  // u > v lie at the row's end
+    const int32_t u = nbr[e];
+    if (u <= v) break;
+    if (*reinterpret_cast<const volatile uint8_t*>(side + u) != sv &&
+        dv + *reinterpret_cast<const volatile int32_t*>(delta + u) + 2 > 0)
+      return true;
+  }
+  return false;
+}
+
+__global__ void k_two_cand(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           const int32_t* __restrict__ hmax, int32_t n, int32_t count,
+                           const uint8_t* __restrict__ side_all, const int32_t* __restrict__ delta_all,
+                           const int32_t* __restrict__ live, uint8_t* __restrict__ cand_all) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n;
+    const int32_t v = static_cast<int32_t>(q - s * n);
+    if (!live[s]) continue;
+    cand_all[q] = two_cand(off, nbr, hmax, side_all + s * n, delta_all + s * n, v) ? 1 : 0;
+  }
+}
+
+// hmax (above), once per graph
+__global__ void k_hmax(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
+                       int32_t* __restrict__ hmax) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t h = 0;
+    for (int64_t e = off[v + 1] - 1, e0 = off[v]; e >= e0; --e) {
+      const int32_t u = nbr[e];
+      if (u <= v) break;
+      h = max(h, static_cast<int32_t>(off[u + 1] - off[u]));
+    }
+    hmax[v] = h;
+  }
+}
+
+__device__ void warp_mark_after_flip(const int64_t* off, const int32_t* nbr, uint8_t* cand,
+                                     int32_t t, int32_t v, int lane) {
+  // y over {t} U N(t); mark y and its smaller neighbours w (w > v only)
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+    const int32_t y = a < e0 ? t : nbr[a];
+    if (y > v) cand[y] = 1;
+    for (int64_t c = off[y]; c < off[y + 1]; ++c) {
+      const int32_t w = nbr[c];
+      if (w >= y) break;  // rows ascending: only w < y
+      if (w > v) cand[w] = 1;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void k_two_scan(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                           const int32_t* __restrict__ hmax, int32_t n, int32_t count, uint8_t* side_all, int32_t* delta_all,
+                           uint8_t* cand_all, int32_t* live, int64_t* gains) {
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count || !live[s]) return;
+  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
+  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
+  uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
   int64_t total = 0;
-  bool improved = true;
-  while (improved) {
-    improved = false;
-    // exact max(delta) at the start of every scan: the running bound only
-    // grows, and a stale large value would disable the filter
-    dmax = INT_MIN;
-    for (int32_t v = lane; v < n; v += 32) dmax = max(dmax, *reinterpret_cast<volatile int32_t*>(delta + v));
-    for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    for (int32_t cb = 0; cb < n; cb += 32) {
-      int32_t dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : INT_MIN / 2;
-      unsigned mask = __ballot_sync(0xffffffffu, dv + dmax + 2 > 0);
+  int32_t dmax = INT_MIN;  // unused bound for warp_flip
+  for (int32_t sb = 0; sb < n; sb += 512) {
+    // 512 marks per warp step (16 independent byte loads per lane; a body's
+    // marks need not be aligned): empty stretches cost one round trip
+    bool any16 = false;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int32_t q = sb + 16 * lane + k;
+      any16 |= q < n && *reinterpret_cast<const volatile uint8_t*>(cand + q) != 0;
+    }
+    if (!__any_sync(0xffffffffu, any16)) continue;
+    for (int32_t cb = sb; cb < min(n, sb + 512); cb += 32) {
+      bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+      unsigned mask = __ballot_sync(0xffffffffu, f);
       while (mask) {
         const int i = warp_first(mask);
         const int32_t v = cb + i;
         const int64_t e1 = off[v + 1];
         int64_t e = off[v];
+        // delta_u <= hmax[v] for every higher neighbour u: skip hopeless rows
+        if (*reinterpret_cast<volatile int32_t*>(delta + v) + hmax[v] + 2 <= 0) e = e1;
         while (e < e1) {
           const int64_t my = e + lane;
           bool ok = false;
@@ -156,162 +295,19 @@ __device__ int64_t warp_two_flip_pass(const int64_t* off, const int32_t* nbr, in
           warp_flip(off, nbr, side, delta, v, lane, dmax);
           warp_flip(off, nbr, side, delta, uu, lane, dmax);
           total += jj;
-          improved = true;
-          e += j + 1;  // resume right after uu with the updated state
+          warp_mark_after_flip(off, nbr, cand, v, v, lane);
+          warp_mark_after_flip(off, nbr, cand, uu, v, lane);
+          e += j + 1;
         }
-        dv = cb + lane < n ? *reinterpret_cast<volatile int32_t*>(delta + cb + lane) : INT_MIN / 2;
-        mask = __ballot_sync(0xffffffffu, dv + dmax + 2 > 0) & (i == 31 ? 0u : (~0u << (i + 1)));
+        f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+        mask = __ballot_sync(0xffffffffu, f) & (i == 31 ? 0u : (~0u << (i + 1)));
       }
-    }
-  }
-  return total;
-}
-
-// ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
-// cand(v) = exists u in N(v), u > v, opposite side, delta_v + delta_u + 2 > 0:
-// the exact "v acts in this sweep if nothing before it changes" test,
-// computed for every vertex of every body in one grid pass.  The warp then
-// visits candidates only; a joint flip of (v, u) can make a later vertex w a
-// candidate only if delta or side changed at some y in Z = {v,u} U N(v) U
-// N(u) with y = w or y in N(w), y > w -- those w > v are re-marked (cand = 1,
-// a superset: the exact evaluation rejects false positives).
-__global__ void k_two_cand(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                           int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
-                           const int32_t* __restrict__ delta_all, const int32_t* __restrict__ live,
-                           uint8_t* __restrict__ cand_all) {
-  const int64_t total = static_cast<int64_t>(count) * n;
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = q / n, v = q % n;
-    if (!live[s]) continue;
-    const uint8_t* side = side_all + s * n;
-    const int32_t* delta = delta_all + s * n;
-    const uint8_t sv = side[v];
-    const int32_t dv = delta[v];
-    uint8_t c = 0;
-    for (int64_t e = off[v + 1] - 1; e >= off[v]; --e) {  // u > v lie at the row's end
-      const int32_t u = nbr[e];
-      if (u <= v) break;
-      if (side[u] != sv && dv + delta[u] + 2 > 0) {
-        c = 1;
-        break;
-      }
-    }
-    cand_all[q] = c;
-  }
-}
-
-__device__ void warp_mark_after_flip(const int64_t* off, const int32_t* nbr, uint8_t* cand,
-                                     int32_t t, int32_t v, int lane) {
-  // y over {t} U N(t); mark y and its smaller neighbours w (w > v only)
-  const int64_t e0 = off[t], e1 = off[t + 1];
-  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
-    const int32_t y = a < e0 ? t : nbr[a];
-    if (y > v) cand[y] = 1;
-    for (int64_t c = off[y]; c < off[y + 1]; ++c) {
-      const int32_t w = nbr[c];
-      if (w >= y) break;  // rows ascending: only w < y
-      if (w > v) cand[w] = 1;
-    }
-  }
-  __syncwarp();
-}
-
-__global__ void k_two_scan(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                           int32_t n, int32_t count, uint8_t* side_all, int32_t* delta_all,
-                           uint8_t* cand_all, int32_t* live, int64_t* gains) {
-  const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
-  if (s >= count || !live[s]) return;
-  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
-  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
-  uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
-  int64_t total = 0;
-  int32_t dmax = INT_MIN;  // unused bound for warp_flip
-  for (int32_t cb = 0; cb < n; cb += 32) {
-    bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
-    unsigned mask = __ballot_sync(0xffffffffu, f);
-    while (mask) {
-      const int i = warp_first(mask);
-      const int32_t v = cb + i;
-      const int64_t e1 = off[v + 1];
-      int64_t e = off[v];
-      while (e < e1) {
-        const int64_t my = e + lane;
-        bool ok = false;
-        int32_t u = 0, joint = 0;
-        if (my < e1) {
-          u = nbr[my];
-          const uint8_t sv = *reinterpret_cast<volatile uint8_t*>(side + v);
-          if (u > v && *reinterpret_cast<volatile uint8_t*>(side + u) != sv) {
-            joint = *reinterpret_cast<volatile int32_t*>(delta + v) +
-                    *reinterpret_cast<volatile int32_t*>(delta + u) + 2;
-            ok = joint > 0;
-          }
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, ok);
-        if (!hit) {
-          e += 32;
-          continue;
-        }
-        const int j = warp_first(hit);
-        const int32_t uu = __shfl_sync(0xffffffffu, u, j);
-        const int32_t jj = __shfl_sync(0xffffffffu, joint, j);
-        warp_flip(off, nbr, side, delta, v, lane, dmax);
-        warp_flip(off, nbr, side, delta, uu, lane, dmax);
-        total += jj;
-        warp_mark_after_flip(off, nbr, cand, v, v, lane);
-        warp_mark_after_flip(off, nbr, cand, uu, v, lane);
-        e += j + 1;
-      }
-      f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
-      mask = __ballot_sync(0xffffffffu, f) & (i == 31 ? 0u : (~0u << (i + 1)));
     }
   }
   if (lane == 0) {
     gains[s] += total;
     live[s] = total > 0 ? 1 : 0;  // improved: sweep again
   }
-}
-
-// one_flip_pass on the live bodies; gains[s] receives its gain.
-__global__ void k_one_flip(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                           int32_t n, int32_t count, uint8_t* side_all, int32_t* delta_all,
-                           const int32_t* live, int64_t* gains) {
-  const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
-  if (s >= count || !live[s]) return;
-  int32_t dmax = INT_MIN;
-  const int64_t g = warp_one_flip_pass(off, nbr, n, side_all + static_cast<int64_t>(s) * n,
-                                       delta_all + static_cast<int64_t>(s) * n, lane, dmax);
-  if (lane == 0) gains[s] = g;
-}
-
-__global__ void k_maxcut_ls(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
-                            int32_t count, uint8_t* side_all, int32_t* delta_all, int32_t op,
-                            int64_t* gains) {
-  const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
-  if (s >= count) return;
-  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
-  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
-  int32_t dmax = INT_MIN;
-  for (int32_t v = lane; v < n; v += 32) dmax = max(dmax, delta[v]);
-  for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  int64_t total = 0;
-  if (op == 0) {
-    total = warp_one_flip_pass(off, nbr, n, side, delta, lane, dmax);
-  } else if (op == 1) {
-    total = warp_two_flip_pass(off, nbr, n, side, delta, lane, dmax);
-  } else {  // one_two_flip: alternate until a round gains nothing
-    for (;;) {
-      const int64_t round = warp_one_flip_pass(off, nbr, n, side, delta, lane, dmax) +
-                            warp_two_flip_pass(off, nbr, n, side, delta, lane, dmax);
-      total += round;
-      if (round == 0) break;
-    }
-  }
-  if (lane == 0) gains[s] = total;
 }
 
 }  // namespace
@@ -600,11 +596,12 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   const int32_t n = g->n;
   const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
   const int blocks = (count + kLsWarps - 1) / kLsWarps;
-  int32_t *d_live = nullptr, *d_live2 = nullptr;
+  int32_t *d_live = nullptr, *d_live2 = nullptr, *d_und = nullptr;
   int64_t *d_g1 = nullptr, *d_g2 = nullptr;
   uint8_t* d_cand = nullptr;
   MQO_CUDA(cudaMallocAsync(&d_live, sizeof(int32_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_live2, sizeof(int32_t) * count, st));
+  MQO_CUDA(cudaMallocAsync(&d_und, sizeof(int32_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_g1, sizeof(int64_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_g2, sizeof(int64_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_cand, cells, st));
@@ -614,10 +611,10 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
     MQO_CUDA(cudaMemcpyAsync(d_live2, who.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
     MQO_CUDA(cudaMemsetAsync(d_g2, 0, sizeof(int64_t) * count, st));
     for (int sweep = 0;; ++sweep) {
-      k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_live2,
-                                                 d_cand);
-      k_two_scan<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_cand,
-                                                   d_live2, d_g2);
+      k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
+                                                 delta, d_live2, d_cand);
+      k_two_scan<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
+                                                   delta, d_cand, d_live2, d_g2);
       MQO_CUDA(cudaGetLastError());
       MQO_CUDA(cudaMemcpyAsync(live2.data(), d_live2, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
       MQO_CUDA(cudaStreamSynchronize(st));
@@ -629,13 +626,48 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
     MQO_CUDA(cudaMemcpyAsync(g2.data(), d_g2, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
     MQO_CUDA(cudaStreamSynchronize(st));
   };
+  // one_flip_pass for the bodies in `who`: round-parallel passes (above)
+  // until a pass flips nothing; delta is rebuilt after every pass
   auto one_flip = [&](const std::vector<int32_t>& who) {
-    MQO_CUDA(cudaMemcpyAsync(d_live, who.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
-    MQO_CUDA(cudaMemsetAsync(d_g1, 0, sizeof(int64_t) * count, st));
-    k_one_flip<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_live, d_g1);
-    MQO_CUDA(cudaGetLastError());
-    MQO_CUDA(cudaMemcpyAsync(g1.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
-    MQO_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> plive = who, und(count);
+    std::vector<int64_t> pg(count);
+    std::fill(g1.begin(), g1.end(), 0);
+    for (int pass = 0;; ++pass) {
+      bool any = false;
+      for (int i = 0; i < count; ++i) any |= plive[i] != 0;
+      if (!any) break;
+      MQO_CUDA(cudaMemcpyAsync(d_live, plive.data(), sizeof(int32_t) * count,
+                               cudaMemcpyHostToDevice, st));
+      MQO_CUDA(cudaMemsetAsync(d_cand, 0, cells, st));  // decision bytes
+      MQO_CUDA(cudaMemsetAsync(d_g1, 0, sizeof(int64_t) * count, st));
+      int rounds = 0;
+      for (;;) {  // four rounds per check; surplus rounds skip decided cells
+        for (int r = 0; r < 4; ++r, ++rounds) {
+          if (r == 3) MQO_CUDA(cudaMemsetAsync(d_und, 0, sizeof(int32_t) * count, st));
+          k_flip_round<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta,
+                                                      d_cand, d_live, d_und);
+        }
+        MQO_CUDA(cudaGetLastError());
+        MQO_CUDA(cudaMemcpyAsync(und.data(), d_und, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
+        MQO_CUDA(cudaStreamSynchronize(st));
+        bool left = false;
+        for (int i = 0; i < count; ++i) left |= und[i] != 0;
+        if (!left) break;
+      }
+      k_flip_commit<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_cand,
+                                                   d_live, reinterpret_cast<unsigned long long*>(d_g1));
+      k_flip_apply<<<ls_grid(cells), 256, 0, st>>>(n, count, side, d_cand, d_live);
+      k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta);
+      MQO_CUDA(cudaGetLastError());
+      MQO_CUDA(cudaMemcpyAsync(pg.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+      MQO_CUDA(cudaStreamSynchronize(st));
+      for (int i = 0; i < count; ++i) {
+        if (!plive[i]) continue;
+        g1[i] += pg[i];
+        if (pg[i] == 0) plive[i] = 0;  // a pass without a flip ends one_flip_pass
+      }
+      MQO_TRACE("one_flip pass %d: %d rounds", pass, rounds);
+    }
   };
   if (op == 0) {
     one_flip(live);
@@ -663,6 +695,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   MQO_CUDA(cudaStreamSynchronize(st));
   cudaFreeAsync(d_live, st);
   cudaFreeAsync(d_live2, st);
+  cudaFreeAsync(d_und, st);
   cudaFreeAsync(d_g1, st);
   cudaFreeAsync(d_g2, st);
   cudaFreeAsync(d_cand, st);
@@ -688,6 +721,11 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (op <= 2) {
     k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
     MQO_CUDA(cudaGetLastError());
+    if (!g->d_hmax) {  // once per graph
+      MQO_CUDA(cudaMalloc(&g->d_hmax, sizeof(int32_t) * std::max(n, 1)));
+      k_hmax<<<ls_grid(n), 256, 0, st>>>(g->d_off, g->d_nbr, n, g->d_hmax);
+      MQO_CUDA(cudaGetLastError());
+    }
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
   } else {
     k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.small);

@@ -116,6 +116,9 @@ def test_large_vs_oracle(O, P):
     got, gain = P.one_two_flip(pg, side)
     ref, rgain = O.one_two_flip(og, side)
     assert gain == rgain and (got == ref).all()
+    got, gain = P.one_flip_pass(pg, side)  # round-parallel passes alone
+    ref, rgain = O.one_flip_pass(og, side)
+    assert gain == rgain and (got == ref).all()
     og = O.generate_er(20000, 10 / 20000, 3)
     pg = P.generate(P.ErSpec(20000, 10 / 20000), 3)
     start, _ = O.greedy_maximalize(og, np.zeros(20000, np.uint8))
