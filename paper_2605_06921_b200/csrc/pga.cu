@@ -74,6 +74,7 @@ struct PassArgs {
   double conv_tol;
   int32_t is_mis;
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
+  int32_t q0, Qg;            // this launch's chain group: quads [q0, q0 + Qg) of Q
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -287,17 +288,18 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   int32_t q, r0, rstep;
-  if (a.Q >= 32) {
-    const int wpr = a.Q >> 5;
+  if (a.Qg >= 32) {
+    const int wpr = a.Qg >> 5;
     q = (gwarp % wpr) * 32 + lane;
     r0 = gwarp / wpr;
     rstep = nwarps / wpr;
   } else {
-    const int rpw = 32 / a.Q;
-    q = lane & (a.Q - 1);
-    r0 = gwarp * rpw + lane / a.Q;
+    const int rpw = 32 / a.Qg;
+    q = lane & (a.Qg - 1);
+    r0 = gwarp * rpw + lane / a.Qg;
     rstep = nwarps * rpw;
   }
+  q += a.q0;  // global quad
   my_q = q;
   const int32_t col = q * CPL;
   unsigned amask;
@@ -627,18 +629,19 @@ int sm_count(int device) {
   return cached[device];
 }
 
-// Warps needed so every (row, quad) unit has a thread.
-int64_t warp_tasks(const mqo_batch* b) {
+// Warps needed so every (row, quad) unit of a Qg-quad chain group has a thread.
+int64_t warp_tasks(const mqo_batch* b, int Qg) {
   const int64_t n = b->g->n;
-  if (b->Q >= 32) return n * (b->Q / 32);
-  const int rpw = 32 / b->Q;
+  if (Qg >= 32) return n * (Qg / 32);
+  const int rpw = 32 / Qg;
   return (n + rpw - 1) / rpw;
 }
+int64_t warp_tasks(const mqo_batch* b) { return warp_tasks(b, b->Q); }
 
-// A row spans wpr = Q/32 warps; the thread -> quad map stays fixed only if
+// A row spans wpr = Qg/32 warps; the thread -> quad map stays fixed only if
 // the total warp count is a multiple of wpr.
-int align_blocks(const mqo_batch* b, int64_t blocks) {
-  const int wpr = b->Q >= 32 ? b->Q / 32 : 1;
+int align_blocks(const mqo_batch* b, int64_t blocks, int Qg) {
+  const int wpr = Qg >= 32 ? Qg / 32 : 1;
   if (wpr > kWarps) {
     const int per = wpr / kWarps;
     blocks = std::max<int64_t>(per, blocks / per * per);
@@ -646,12 +649,49 @@ int align_blocks(const mqo_batch* b, int64_t blocks) {
   return static_cast<int>(blocks);
 }
 
+int align_blocks(const mqo_batch* b, int64_t blocks) { return align_blocks(b, blocks, b->Q); }
+
 // Grid of the per-pass kernels: g_grid_per_sm CTAs per SM (grid-stride
 // over rows), never more than the work needs.
-int pass_blocks(const mqo_batch* b) {
-  const int64_t need = (warp_tasks(b) + kWarps - 1) / kWarps;
+int pass_blocks(const mqo_batch* b, int Qg) {
+  const int64_t need = (warp_tasks(b, Qg) + kWarps - 1) / kWarps;
   const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * g_grid_per_sm;
-  return align_blocks(b, std::max<int64_t>(1, std::min(need, cap)));
+  return align_blocks(b, std::max<int64_t>(1, std::min(need, cap)), Qg);
+}
+int pass_blocks(const mqo_batch* b) { return pass_blocks(b, b->Q); }
+
+// Chain tiling of the per-pass kernels.  A pass over all B chains gathers
+// neighbour rows of n·8·B bytes at random; when that working set exceeds
+// L2, almost every gather misses.  Sweeping the graph once per chain group
+// shrinks the working set to n·8·Bg, so gathered row segments stay in L2
+// between neighbours -- at the price of re-reading the CSR per group and of
+// shorter row segments.  Measured (scripts/tune_k1.py --groups): ER(1e5,
+// d=10) MIS, 256 chains: 0.324 -> 0.252 ms/step with 64-chain groups (51 MB
+// slices); BA(1e6,5), 128 chains: no group size helps (a slice that fits L2
+// leaves 8-16 chains per row, whose scattered 32-byte sectors run DRAM far
+// below its streaming rate), so tiling applies only when a slice of >= 32
+// chains fits in half the L2.
+// g_group_quads: quads (4 chains) per group; 0 = automatic, -1 = off.
+int g_group_quads = [] {
+  const char* e = std::getenv("MQO_GROUP_QUADS");
+  return e ? std::atoi(e) : 0;
+}();
+int group_quads(const mqo_batch* b) {
+  const int Q = b->Q;
+  if (g_group_quads < 0 || b->cpl != 4) return Q;
+  int Qg = g_group_quads;
+  if (Qg == 0) {
+    static int l2[64] = {0};
+    const int dev = b->g->device;
+    if (!l2[dev]) MQO_CUDA(cudaDeviceGetAttribute(&l2[dev], cudaDevAttrL2CacheSize, dev));
+    Qg = Q;
+    while (Qg > 8 && static_cast<double>(b->g->n) * 32.0 * Qg > 0.5 * l2[dev]) Qg /= 2;
+    if (static_cast<double>(b->g->n) * 32.0 * Qg > 0.5 * l2[dev]) return Q;  // no slice fits
+  }
+  // a group must tile Q: a power of two <= 32 dividing Q, or a multiple of 32 dividing Q
+  Qg = std::max(1, std::min(Qg, Q));
+  while (Q % Qg != 0 || (Qg < 32 && (Qg & (Qg - 1)) != 0) || (Qg > 32 && Qg % 32 != 0)) --Qg;
+  return Qg;
 }
 
 void validate_objective(const mqo_objective& o) {  // objectives.cpp:27-38
@@ -675,14 +715,15 @@ void validate_optimizer(const mqo_optimizer& c) {  // pga.cpp:9-18
 // Rows whose gathers are marked L2::evict_last: a prefix of the vertex
 // order (hubs come first in preferential-attachment labelings) sized to
 // MQO_HOT_FRAC (default 0.3) of the L2.
-int32_t hot_rows(const mqo_batch* b) {
+int32_t hot_rows(const mqo_batch* b, int Qg) {
   const double frac = g_hot_frac;
   static int l2[64] = {0};
   const int dev = b->g->device;
   if (!l2[dev]) MQO_CUDA(cudaDeviceGetAttribute(&l2[dev], cudaDevAttrL2CacheSize, dev));
-  const double rows = frac * l2[dev] / (8.0 * b->Bp);
+  const double rows = frac * l2[dev] / (8.0 * b->cpl * Qg);
   return static_cast<int32_t>(std::min<double>(b->g->n, std::max(0.0, rows)));
 }
+int32_t hot_rows(const mqo_batch* b) { return hot_rows(b, b->Q); }
 
 PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   PassArgs a{};
@@ -694,6 +735,8 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   a.B = b->B;
   a.Bp = b->Bp;
   a.Q = b->Q;
+  a.q0 = 0;
+  a.Qg = b->Q;
   a.x[0] = b->d_x[0];
   a.x[1] = b->d_x[1];
   a.v = b->d_v;
@@ -733,7 +776,11 @@ void launch_step(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& op
   a.alpha = opt.alpha;
   a.beta = opt.beta;
   if (b->g->n == 0) return;
-  pass_fn<kStep>(obj.kind, b->cpl)<<<pass_blocks(b), kThreads, 0, b->stream>>>(a);
+  PassFn fn = pass_fn<kStep>(obj.kind, b->cpl);
+  a.Qg = group_quads(b);
+  a.hot_rows = hot_rows(b, a.Qg);
+  const int blocks = pass_blocks(b, a.Qg);
+  for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, 0, b->stream>>>(a);
   MQO_CUDA(cudaGetLastError());
   b->cur ^= 1;
 }
@@ -771,7 +818,11 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
   const bool persistent = int64_t(g->n) * b->Bp <= persistent_cells();
   PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl);
   const size_t smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
-  int blocks = pass_blocks(b);
+  if (!persistent) {  // chain tiling (see group_quads)
+    a.Qg = group_quads(b);
+    a.hot_rows = hot_rows(b, a.Qg);
+  }
+  int blocks = pass_blocks(b, a.Qg);
   if (persistent) {
     int per_sm = 0;
     MQO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -808,7 +859,8 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
       for (int32_t q = p; q < chunk_end; ++q) {
         a.p_begin = q;
         a.p_end = q + 1;
-        fn<<<blocks, kThreads, smem, b->stream>>>(a);
+        for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, smem, b->stream>>>(a);
+        a.q0 = 0;
         k_traj_ctl<<<1, 256, 0, b->stream>>>(a);
       }
       MQO_CUDA(cudaGetLastError());
@@ -864,6 +916,8 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_cta_disabled = value == 0.0;
     else if (k == "cta_cluster")
       g_cta_cluster = static_cast<int>(value);
+    else if (k == "group_quads")
+      g_group_quads = static_cast<int>(value);
     else if (k == "grid_per_sm")
       g_grid_per_sm = std::max(1, static_cast<int>(value));
     else

@@ -2,7 +2,7 @@
 
 python scripts/tune_k1.py [--steps 60]
 Prints ms/step, edge-chain updates/s and the algorithmic-bandwidth fraction
-for each (variant, hot_frac) on the bench workload (BA(1e6,5) f_B, 128
+for each (variant, hot_frac, chain-group size) on the bench workload (BA(1e6,5) f_B, 128
 chains) and on config 3 (ER(1e5, d=10) MIS, 256 chains), and checks every
 variant produces bit-identical iterates.
 """
@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--variants", default="0,1,2,3,4")
     ap.add_argument("--fracs", default="0,0.3,0.5,0.7")
     ap.add_argument("--grids", default="8")
+    ap.add_argument("--groups", default="-1",
+                    help="quads per chain group (-1 = untiled, 0 = automatic)")
     ap.add_argument("--traj", action="store_true", help="also time 20-pass trajectories")
     args = ap.parse_args()
     import torch
@@ -42,10 +44,12 @@ def main():
         batch = P.ChainBatch(g, B)
         stream = torch.cuda.ExternalStream(batch.stream)
         ref = None
-        combos = [(int(v), float(f), int(gr)) for v in args.variants.split(",")
-                  for f in args.fracs.split(",") for gr in args.grids.split(",")]
-        for var, frac, grid in combos:
+        combos = [(int(v), float(f), int(gr), int(gq)) for v in args.variants.split(",")
+                  for f in args.fracs.split(",") for gr in args.grids.split(",")
+                  for gq in args.groups.split(",")]
+        for var, frac, grid, gq in combos:
             if True:
+                _lib.check(_lib.lib.mqo_tune(b"group_quads", gq))
                 _lib.check(_lib.lib.mqo_tune(b"k1_variant", var))
                 _lib.check(_lib.lib.mqo_tune(b"hot_frac", frac))
                 _lib.check(_lib.lib.mqo_tune(b"grid_per_sm", grid))
@@ -75,6 +79,7 @@ def main():
                     batch.run_trajectories(spec, tcfg)
                     traj_ms = round((time.time() - t0) * 1e3 / 20, 4)
                 print(json.dumps({"case": name, "variant": var, "hot_frac": frac, "grid": grid,
+                                  "group_quads": gq,
                                   "traj_ms_per_pass_wall": traj_ms,
                                   "ms_per_step": round(ms, 4),
                                   "edge_chain_per_s": nnz * B / ms * 1e3,

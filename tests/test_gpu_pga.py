@@ -101,6 +101,35 @@ def test_batched_steps_vs_oracle(O, P, B, kind, param):
         assert same(gx[c], x) and same(gv[c], v), c
 
 
+@pytest.mark.parametrize("gq", [1, 2, 8])
+@pytest.mark.parametrize("B", [33, 256])
+def test_chain_tiled_steps_vs_oracle(O, P, B, gq):
+    """Chain tiling (one graph sweep per group of gq quads) keeps every
+    iterate bit-identical."""
+    from paper_2605_06921_b200 import _lib
+    og = O.generate_er(300, 0.03, 6)
+    pg = P.generate(P.ErSpec(300, 0.03), 6)
+    rng = np.random.default_rng(B + gq)
+    for kind, param in ((MIS_QUBO, 2.0), (PERTURBED_BIAS, 0.001)):
+        lo = 0.0 if kind == MIS_QUBO else -1.0
+        X = rng.uniform(lo, 1.0, (B, og.n))
+        b = P.ChainBatch(pg, B)
+        b.set_x(X)
+        cfg = P.OptimizerConfig(alpha=0.05, beta=0.7)
+        _lib.check(_lib.lib.mqo_tune(b"group_quads", gq))
+        try:
+            for _ in range(4):
+                b.step(Spec(kind, param), cfg)
+        finally:
+            _lib.check(_lib.lib.mqo_tune(b"group_quads", 0))
+        gx = b.get_x()
+        for c in range(0, B, 7):
+            x, v = X[c].copy(), np.zeros(og.n)
+            for _ in range(4):
+                x, v = O.step(og, kind, param, x, v, 0.05, 0.7)
+            assert same(gx[c], x), (kind, c)
+
+
 def test_hub_rows_ba(O, P):
     """BA(1e5, 5): power-law hub rows (deg in the hundreds), B=128 chains."""
     og = O.generate_ba(100000, 5, 3)
@@ -150,9 +179,10 @@ def test_trajectory_kats(P):  # test_pga.cpp:77-119
         P.run_trajectory(P.MisQubo(2.0), k3, [0.4, 0.4, 0.4], P.OptimizerConfig(alpha=0.0))
 
 
-# (cta_traj, persistent_cells, cta_cluster)
-PATHS = {"cta": (1, 1 << 22, 0), "cta_c1": (1, 1 << 22, 1), "cta_c3": (1, 1 << 22, 3),
-         "cta_c16": (1, 1 << 22, 16), "persistent": (0, 1 << 22, 0), "perpass": (0, 0, 0)}
+# (cta_traj, persistent_cells, cta_cluster, group_quads)
+PATHS = {"cta": (1, 1 << 22, 0, 0), "cta_c1": (1, 1 << 22, 1, 0), "cta_c3": (1, 1 << 22, 3, 0),
+         "cta_c16": (1, 1 << 22, 16, 0), "persistent": (0, 1 << 22, 0, 0),
+         "perpass": (0, 0, 0, 0), "perpass_tiled": (0, 0, 0, 1)}
 
 
 @pytest.fixture(params=list(PATHS))
@@ -160,16 +190,18 @@ def traj_path(request, P):
     """Run the trajectory parity tests through each device path: SMEM
     cluster-per-chain (automatic cluster size, and forced 1 / 3 / 16 CTAs
     per chain -- 16 is clamped to the slice count), cooperative persistent,
-    launch-per-pass."""
+    launch-per-pass (untiled and one sweep per 4-chain group)."""
     from paper_2605_06921_b200 import _lib
-    cta, cells, clu = PATHS[request.param]
+    cta, cells, clu, gq = PATHS[request.param]
     _lib.check(_lib.lib.mqo_tune(b"cta_traj", cta))
     _lib.check(_lib.lib.mqo_tune(b"persistent_cells", cells))
     _lib.check(_lib.lib.mqo_tune(b"cta_cluster", clu))
+    _lib.check(_lib.lib.mqo_tune(b"group_quads", gq))
     yield request.param
     _lib.check(_lib.lib.mqo_tune(b"cta_traj", 1))
     _lib.check(_lib.lib.mqo_tune(b"persistent_cells", 1 << 22))
     _lib.check(_lib.lib.mqo_tune(b"cta_cluster", 0))
+    _lib.check(_lib.lib.mqo_tune(b"group_quads", 0))
 
 
 @pytest.mark.parametrize("kind,param,alpha,beta,ce", [
