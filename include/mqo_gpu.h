@@ -119,6 +119,22 @@ int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph** out);
 int mqo_graph_save(const mqo_graph* g, const char* path, int32_t format);
 int mqo_graph_load(const char* path, int32_t device, mqo_graph** out);
 
+/* Device pre-processing on a graph in HBM.
+ * strip_isolated (graph.hpp:95-104, graph.cpp:180-198): *core = the graph
+ * without its degree-0 vertices (same device); caller-sized arrays of n:
+ * core_to_orig (first *n_core used), orig_to_core (-1 for removed vertices),
+ * removed (ascending, first *n_removed used); any array may be NULL.
+ * Replaces: StripResult strip_isolated(const Graph&). */
+int mqo_graph_strip_isolated(const mqo_graph* g, mqo_graph** core, int32_t* core_to_orig,
+                             int32_t* orig_to_core, int32_t* removed, int32_t* n_core,
+                             int32_t* n_removed);
+/* connected_components (graph.hpp:106, graph.cpp:200-224): comp[v] = index
+ * of v's component, components numbered in the reference's output order
+ * (by smallest vertex); *count = number of components.  The reference's
+ * sorted member lists are the stable grouping of v by comp[v].
+ * Replaces: std::vector<std::vector<Vertex>> connected_components(const Graph&). */
+int mqo_graph_components(const mqo_graph* g, int32_t* comp, int32_t* count);
+
 /* ---- chain batch -------------------------------------------------------
  * A batch of `chains` relaxed states (RelaxedState, objectives.hpp:45-48)
  * plus velocities, the per-chain xoshiro streams and control words, on the

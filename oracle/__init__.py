@@ -121,6 +121,8 @@ class Lib:
             "orc_graph_free": (None, [_P]),
             "orc_graph_info": (None, [_P, _I32, _I64, _I32]),
             "orc_graph_csr": (None, [_P, _I64, _I32]),
+            "orc_strip_isolated": (C.c_int, [_P, C.POINTER(_P), _I32, _I32, _I32, _I32, _I32]),
+            "orc_components": (C.c_int, [_P, _I32, _I32]),
             "orc_adjacency_apply": (C.c_int, [_P, _D, _D]),
             "orc_laplacian_apply": (C.c_int, [_P, _D, _D]),
             "orc_validate_objective": (C.c_int, [C.c_int32, C.c_double]),
@@ -187,6 +189,25 @@ class Lib:
 
     def generate_sbm(self, n, k, p_in, p_out, seed) -> "Graph":
         return self._graph(self.L.orc_generate_sbm, n, k, p_in, p_out, seed)
+
+    def strip_isolated(self, g):
+        """-> (core Graph, removed, core_to_orig, orig_to_core) (graph.cpp:180-198)."""
+        n = g.n
+        c2o, o2c, rem = (np.empty(max(n, 1), np.int32) for _ in range(3))
+        nc, nr = C.c_int32(), C.c_int32()
+        h = _P()
+        self._chk(self.L.orc_strip_isolated(g.h, C.byref(h), _ptr(c2o, _I32), _ptr(o2c, _I32),
+                                            _ptr(rem, _I32), C.byref(nc), C.byref(nr)))
+        return Graph(self, h), rem[: nr.value].copy(), c2o[: nc.value].copy(), o2c[:n].copy()
+
+    def connected_components(self, g):
+        """-> list of sorted member arrays, in the reference's order (graph.cpp:200-224)."""
+        comp = np.empty(max(g.n, 1), np.int32)
+        cnt = C.c_int32()
+        self._chk(self.L.orc_components(g.h, _ptr(comp, _I32), C.byref(cnt)))
+        order = np.argsort(comp[: g.n], kind="stable")
+        bounds = np.searchsorted(comp[: g.n][order], np.arange(cnt.value + 1))
+        return [order[bounds[c]:bounds[c + 1]].astype(np.int32) for c in range(cnt.value)]
 
     # ------------------------------------------------------------ objectives
     def adjacency_apply(self, g, x):

@@ -345,6 +345,61 @@ void orc_graph_csr(void* gp, int64_t* offsets, int32_t* nbrs) {
   memcpy(nbrs, g->nbr, (size_t)(2 * g->m) * sizeof(int32_t));
 }
 
+/* strip_isolated (graph.cpp:180-198): degree-0 vertices removed in index
+ * order; the core is rebuilt from the relabelled edges (v < u). */
+int orc_strip_isolated(void* gp, void** core, int32_t* core_to_orig, int32_t* orig_to_core,
+                       int32_t* removed, int32_t* n_core, int32_t* n_removed) {
+  const graph_t* g = (const graph_t*)gp;
+  int32_t nc = 0, nr = 0;
+  for (int32_t v = 0; v < g->n; ++v) {
+    if (deg(g, v) == 0) {
+      orig_to_core[v] = -1;
+      removed[nr++] = v;
+    } else {
+      orig_to_core[v] = nc;
+      core_to_orig[nc++] = v;
+    }
+  }
+  uint64_t* keys = (uint64_t*)xmalloc((size_t)(g->m > 0 ? g->m : 1) * sizeof(uint64_t));
+  int64_t k = 0;
+  for (int32_t v = 0; v < g->n; ++v)
+    for (int64_t e = g->off[v]; e < g->off[v + 1]; ++e)
+      if (v < g->nbr[e])
+        keys[k++] = ((uint64_t)(uint32_t)orig_to_core[v] << 32) | (uint32_t)orig_to_core[g->nbr[e]];
+  *n_core = nc;
+  *n_removed = nr;
+  return graph_build(nc, k, keys, (graph_t**)core);
+}
+
+/* connected_components (graph.cpp:200-224): DFS from each unseen vertex in
+ * index order; comp[v] = index of v's component (output order). */
+int orc_components(void* gp, int32_t* comp, int32_t* count) {
+  const graph_t* g = (const graph_t*)gp;
+  int32_t* stack = (int32_t*)xmalloc((size_t)(g->n > 0 ? g->n : 1) * sizeof(int32_t));
+  for (int32_t v = 0; v < g->n; ++v) comp[v] = -1;
+  int32_t c = 0;
+  for (int32_t s = 0; s < g->n; ++s) {
+    if (comp[s] >= 0) continue;
+    int32_t top = 0;
+    comp[s] = c;
+    stack[top++] = s;
+    while (top > 0) {
+      const int32_t v = stack[--top];
+      for (int64_t e = g->off[v]; e < g->off[v + 1]; ++e) {
+        const int32_t u = g->nbr[e];
+        if (comp[u] < 0) {
+          comp[u] = c;
+          stack[top++] = u;
+        }
+      }
+    }
+    ++c;
+  }
+  free(stack);
+  *count = c;
+  return ORC_OK;
+}
+
 static int has_edge(const graph_t* g, int32_t u, int32_t v) { /* graph.cpp:58-61 */
   int64_t lo = g->off[u], hi = g->off[u + 1];
   while (lo < hi) {

@@ -97,6 +97,10 @@ int orc_generate_sbm(int32_t n, int32_t k, double p_in, double p_out, uint64_t s
 void orc_graph_free(void* g);
 void orc_graph_info(void* g, int32_t* n, int64_t* m, int32_t* max_degree);
 void orc_graph_csr(void* g, int64_t* offsets, int32_t* nbrs);
+/* strip_isolated / connected_components (graph.cpp:180-224); arrays sized n */
+int orc_strip_isolated(void* g, void** core, int32_t* core_to_orig, int32_t* orig_to_core,
+                       int32_t* removed, int32_t* n_core, int32_t* n_removed);
+int orc_components(void* g, int32_t* comp, int32_t* count);
 int orc_adjacency_apply(void* g, const double* x, double* y);
 int orc_laplacian_apply(void* g, const double* x, double* y);
 

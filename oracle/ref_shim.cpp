@@ -125,6 +125,28 @@ int orc_generate_sbm(int32_t n, int32_t k, double p_in, double p_out, uint64_t s
 
 void orc_graph_free(void* g) { delete static_cast<Graph*>(g); }
 
+int orc_strip_isolated(void* g, void** core, int32_t* core_to_orig, int32_t* orig_to_core,
+                       int32_t* removed, int32_t* n_core, int32_t* n_removed) {
+  return guard([&] {
+    StripResult r = strip_isolated(G(g));
+    std::copy(r.core_to_orig.begin(), r.core_to_orig.end(), core_to_orig);
+    std::copy(r.orig_to_core.begin(), r.orig_to_core.end(), orig_to_core);
+    std::copy(r.removed.begin(), r.removed.end(), removed);
+    *n_core = static_cast<int32_t>(r.core_to_orig.size());
+    *n_removed = static_cast<int32_t>(r.removed.size());
+    *core = new Graph(std::move(r.core));
+  });
+}
+
+int orc_components(void* g, int32_t* comp, int32_t* count) {
+  return guard([&] {
+    const auto comps = connected_components(G(g));
+    for (size_t c = 0; c < comps.size(); ++c)
+      for (Vertex v : comps[c]) comp[v] = static_cast<int32_t>(c);
+    *count = static_cast<int32_t>(comps.size());
+  });
+}
+
 void orc_graph_info(void* g, int32_t* n, int64_t* m, int32_t* max_degree) {
   *n = G(g).n();
   *m = G(g).m();

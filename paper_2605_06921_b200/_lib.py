@@ -58,6 +58,8 @@ SIGNATURES: dict[str, tuple] = {
     "mqo_graph_upload": (C.c_int, [C.c_int32, _I64, _I32, C.c_int32, _PP]),
     "mqo_graph_free": (C.c_int, [_P]),
     "mqo_graph_info": (C.c_int, [_P, _I32, _I64, _I32]),
+    "mqo_graph_strip_isolated": (C.c_int, [_P, _PP, _I32, _I32, _I32, _I32, _I32]),
+    "mqo_graph_components": (C.c_int, [_P, _I32, _I32]),
     "mqo_batch_create": (C.c_int, [_P, C.c_int32, _PP]),
     "mqo_batch_free": (C.c_int, [_P]),
     "mqo_batch_chains": (C.c_int, [_P, _I32, _I32]),

@@ -25,7 +25,8 @@ from ._lib import (ADJACENCY, CHECKER_ACCEPTED, CONVERGED, ITER_CAP, LAPLACIAN, 
                    InvalidArgument, LogicError, MqoError, Objective, Optimizer, check, lib)
 
 __all__ = [
-    "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "generate", "MisQubo", "Laplacian",
+    "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "generate", "StripResult",
+    "strip_isolated", "connected_components", "MisQubo", "Laplacian",
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
@@ -235,6 +236,39 @@ class Graph:
     def neighbors(self, v: int) -> np.ndarray:
         off, nbr = self.csr()
         return nbr[off[v]:off[v + 1]]
+
+
+@dataclass
+class StripResult:  # graph.hpp:95-100
+    core: Graph
+    removed: np.ndarray        # isolated vertices, ascending
+    core_to_orig: np.ndarray   # size core.n()
+    orig_to_core: np.ndarray   # -1 for removed vertices
+
+
+def strip_isolated(g: Graph) -> StripResult:
+    """strip_isolated (graph.hpp:104, graph.cpp:180-198), computed on the
+    graph's device (flag pass + scan + in-place relabelling)."""
+    n = g.n()
+    c2o, o2c, rem = (np.empty(max(n, 1), np.int32) for _ in range(3))
+    nc, nr = C.c_int32(), C.c_int32()
+    h = C.c_void_p()
+    check(lib.mqo_graph_strip_isolated(g._h, C.byref(h), _ptr(c2o, _I32), _ptr(o2c, _I32),
+                                       _ptr(rem, _I32), C.byref(nc), C.byref(nr)))
+    return StripResult(Graph(h, g.device), rem[: nr.value].copy(), c2o[: nc.value].copy(),
+                       o2c[:n].copy())
+
+
+def connected_components(g: Graph) -> list:
+    """connected_components (graph.hpp:106, graph.cpp:200-224) on the graph's
+    device: sorted member arrays, ordered by smallest vertex."""
+    n = g.n()
+    comp = np.empty(max(n, 1), np.int32)
+    cnt = C.c_int32()
+    check(lib.mqo_graph_components(g._h, _ptr(comp, _I32), C.byref(cnt)))
+    order = np.argsort(comp[:n], kind="stable")
+    bounds = np.searchsorted(comp[:n][order], np.arange(cnt.value + 1))
+    return [order[bounds[c]:bounds[c + 1]].astype(np.int32) for c in range(cnt.value)]
 
 
 def generate(spec, seed: int, device: int = 0) -> Graph:

@@ -146,17 +146,13 @@ def run_solve(a) -> dict:
         desc = {"source": "generator", "n": g.n(), "m": g.m(), "spec": a.gen, "seed": a.seed}
     load_secs = time.time() - t0
     cfg = build_config(a, g)
-    off, nbr = g.csr()
+    off, _ = g.csr()
     deg = np.diff(off)
     warnings = []
     if g.m() > 0 and (deg == 0).any():  # strip isolated vertices, solve, re-embed
-        keep = np.flatnonzero(deg > 0)
-        remap = np.full(g.n(), -1, np.int64)
-        remap[keep] = np.arange(len(keep))
-        src = np.repeat(np.arange(g.n()), deg)
-        mask = src < nbr
-        core = P.Graph.from_edges(len(keep), np.stack([remap[src[mask]], remap[nbr[mask]]], 1),
-                                  device=a.device)
+        strip = P.strip_isolated(g)  # on the device (cli_common.cpp:163-198)
+        keep = strip.core_to_orig
+        core = strip.core
         rep = P.solve_pooled(core, cfg)
         body = np.zeros(g.n(), np.uint8)
         body[keep] = rep.best_body

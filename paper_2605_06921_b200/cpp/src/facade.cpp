@@ -209,45 +209,27 @@ Graph generate(const GraphGenSpec& spec) {
   return Graph::adopt(h);
 }
 
-StripResult strip_isolated(const Graph& g) {  // host pre-processing (graph.cpp:180-198)
+StripResult strip_isolated(const Graph& g) {  // graph.cpp:180-198, on the device
+  const size_t n = static_cast<size_t>(g.n());
+  std::vector<int32_t> c2o(std::max<size_t>(n, 1)), o2c(std::max<size_t>(n, 1)),
+      rem(std::max<size_t>(n, 1));
+  int32_t nc = 0, nr = 0;
+  mqo_graph* core = nullptr;
+  check(mqo_graph_strip_isolated(g.handle(), &core, c2o.data(), o2c.data(), rem.data(), &nc, &nr));
   StripResult r;
-  r.orig_to_core.assign(g.n(), -1);
-  for (Vertex v = 0; v < g.n(); ++v) {
-    if (g.degree(v) == 0) {
-      r.removed.push_back(v);
-    } else {
-      r.orig_to_core[v] = static_cast<Vertex>(r.core_to_orig.size());
-      r.core_to_orig.push_back(v);
-    }
-  }
-  std::vector<std::pair<Vertex, Vertex>> e;
-  for (const auto& [u, v] : g.edges()) e.emplace_back(r.orig_to_core[u], r.orig_to_core[v]);
-  r.core = Graph::from_edges(static_cast<Vertex>(r.core_to_orig.size()), std::move(e));
+  r.core = Graph::adopt(core);
+  r.core_to_orig.assign(c2o.begin(), c2o.begin() + nc);
+  r.orig_to_core.assign(o2c.begin(), o2c.begin() + static_cast<std::ptrdiff_t>(n));
+  r.removed.assign(rem.begin(), rem.begin() + nr);
   return r;
 }
 
-std::vector<std::vector<Vertex>> connected_components(const Graph& g) {
-  std::vector<std::vector<Vertex>> comps;
-  std::vector<char> seen(g.n(), 0);
-  std::vector<Vertex> todo;
-  for (Vertex s = 0; s < g.n(); ++s) {
-    if (seen[s]) continue;
-    std::vector<Vertex> comp;
-    seen[s] = 1;
-    todo.push_back(s);
-    while (!todo.empty()) {
-      const Vertex v = todo.back();
-      todo.pop_back();
-      comp.push_back(v);
-      for (Vertex u : g.neighbors(v))
-        if (!seen[u]) {
-          seen[u] = 1;
-          todo.push_back(u);
-        }
-    }
-    std::sort(comp.begin(), comp.end());
-    comps.push_back(std::move(comp));
-  }
+std::vector<std::vector<Vertex>> connected_components(const Graph& g) {  // graph.cpp:200-224
+  std::vector<int32_t> comp(std::max<size_t>(static_cast<size_t>(g.n()), 1));
+  int32_t count = 0;
+  check(mqo_graph_components(g.handle(), comp.data(), &count));
+  std::vector<std::vector<Vertex>> comps(static_cast<size_t>(count));
+  for (Vertex v = 0; v < g.n(); ++v) comps[static_cast<size_t>(comp[v])].push_back(v);
   return comps;
 }
 

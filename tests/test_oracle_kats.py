@@ -239,3 +239,35 @@ def test_presets(O):  # presets.cpp:17-60 rows used by BASELINE configs
     assert O.preset_for(PROBLEM_MIS, 1000, 9.938) == (0.8, 0.3, 0.7, 60)
     assert O.preset_for(PROBLEM_MIS, 100000, 10.0) == (0.8, 0.3, 0.6, 60)
     assert O.preset_for(PROBLEM_MAXCUT, 1000000, 10.0) == (0.0025, 0.8, 0.8, 90)
+
+
+def test_strip_and_components_kats(O):  # test_graph.cpp:201-250
+    core, rem, c2o, o2c = O.strip_isolated(O.from_edges(3, [(0, 1)]))
+    assert core.n == 2 and rem.tolist() == [2] and c2o.tolist() == [0, 1]
+    assert o2c.tolist() == [0, 1, -1]
+    cyc = O.from_edges(5, [(v, (v + 1) % 5) for v in range(5)])
+    core, rem, _, _ = O.strip_isolated(cyc)
+    assert len(rem) == 0 and core.edges() == cyc.edges()
+    star = O.from_edges(4, [(0, v) for v in range(1, 4)])
+    core, rem, _, _ = O.strip_isolated(star)
+    assert len(rem) == 0 and core.n == 4
+    tri = O.from_edges(6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)])
+    comps = O.connected_components(tri)
+    assert [c.tolist() for c in comps] == [[0, 1, 2], [3, 4, 5]]
+    assert len(O.connected_components(O.from_edges(5, []))) == 5
+    assert len(O.connected_components(O.generate_er(50, 0.2, 1))) == 1
+
+
+def test_strip_and_components_vs_reference(O, R):
+    """The C restatement equals the compiled reference on sparse graphs with
+    isolated vertices and many components."""
+    for trial in range(12):
+        n, p = 300 + 37 * trial, 0.8 / (300 + 37 * trial)
+        seed = O.derive_seed(29, trial)
+        og, rg = O.generate_er(n, p, seed), R.generate_er(n, p, seed)
+        a, b = O.strip_isolated(og), R.strip_isolated(rg)
+        assert a[0].edges() == b[0].edges() and a[0].n == b[0].n
+        for x, y in zip(a[1:], b[1:]):
+            assert (x == y).all()
+        ca, cb = O.connected_components(og), R.connected_components(rg)
+        assert len(ca) == len(cb) and all((x == y).all() for x, y in zip(ca, cb))
