@@ -202,7 +202,8 @@ def run_solve(a) -> dict:
             "warnings": warnings, "backend": "b200"}
 
 
-def main(argv=None) -> int:
+def _parser() -> argparse.ArgumentParser:
+    from . import verify
     ap = argparse.ArgumentParser(prog="mqo", description="mQO on the B200 backend")
     sub = ap.add_subparsers(dest="cmd", required=True)
     s = sub.add_parser("solve")
@@ -227,8 +228,25 @@ def main(argv=None) -> int:
     gsub.add_argument("--seed", type=int, default=1)
     gsub.add_argument("--out", required=True)
     gsub.add_argument("--text", action="store_true", help="canonical text instead of binary CSR")
-    a = ap.parse_args(argv)
+    verify.add_parser(sub)
+    return ap
+
+
+def solve_defaults(**overrides) -> argparse.Namespace:
+    """The `solve` flags at their defaults (SolveOptions, cli_common.hpp),
+    with overrides -- for callers that build configs without a command line."""
+    a = _parser().parse_args(["solve"])
+    for k, v in overrides.items():
+        setattr(a, k, v)
+    return a
+
+
+def main(argv=None) -> int:
+    a = _parser().parse_args(argv)
     try:
+        if a.cmd == "verify":
+            from . import verify
+            return verify.cmd_verify(a.suite, a.max_n, a.n, a.p, a.seed)
         if a.cmd == "gen":
             g = P.generate(parse_gen_spec(a.gen), a.seed, device=-1)
             g.save(a.out, text=a.text)

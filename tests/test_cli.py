@@ -81,3 +81,34 @@ def test_solve_strips_isolated_vertices(cuda_ok, tmp_path):
     assert (decode_bits(rec["solution"]["members"], 300) == full).all()
     assert rec["counters"]["iterations"] == rep["total_iterations"]
     assert any("stripped" in w for w in rec["warnings"])
+
+
+def test_verify_rng_matches_reference_stream():
+    """The suites' set-up draws (verify.Rng / derive_seed) follow rng.hpp."""
+    from paper_2605_06921_b200 import verify
+    O = oracle.load("oracle")
+    for seed in (1, 20250801, 2**63 + 5):
+        r, o = verify.Rng(seed), O.rng(seed)
+        assert [r.next_u64() for _ in range(50)] == [o.next_u64() for _ in range(50)]
+        assert r.uniform01() == o.uniform01()
+        for stream in (0, 1, 400, 2**40):
+            assert verify.derive_seed(seed, stream) == O.derive_seed(seed, stream)
+
+
+def test_verify_usage_error():
+    r = cli("verify", "--suite", "nope")
+    assert r.returncode == 2 and "unknown --suite" in r.stderr
+
+
+@pytest.mark.gpu
+def test_verify_suites(cuda_ok):
+    """cmd_verify.cpp's suites on the GPU path (reduced sizes)."""
+    r = cli("verify", "--suite", "fixed-points", "--max-n", "9")
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("[PASS]") == 4 and "all checks passed" in r.stdout
+    r = cli("verify", "--suite", "escapability", "--n", "60", "--p", "0.05")
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("[PASS]") == 5
+    r = cli("verify", "--suite", "exact", "--max-n", "10")
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("[PASS]") == 3
