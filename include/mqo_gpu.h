@@ -35,11 +35,15 @@ enum {
   MQO_ERR_LOGIC = 2,   /* std::logic_error in the reference */
   MQO_ERR_CUDA = 3,
   MQO_ERR_NCCL = 4,
-  MQO_ERR_OTHER = 5
+  MQO_ERR_OTHER = 5,
+  MQO_ERR_PARSE = 6 /* mqo::ParseError (graph_io.hpp:13-21), a std::runtime_error */
 };
 
 /* Thread-local message of the last failing call on this thread. */
 const char* mqo_last_error(void);
+/* 1-based line of the last MQO_ERR_PARSE on this thread (ParseError::line,
+ * graph_io.hpp:17), else 0. */
+int32_t mqo_last_error_line(void);
 /* Library identification, e.g. "mqo_b200 0.1 sm_100a". */
 const char* mqo_version(void);
 
@@ -115,9 +119,26 @@ int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph** out);
 /* Graph files (graph_io.cpp:74-106): format 0 = binary CSR cache
  * ("MQOCSR01" n m offsets neighbours), 1 = the reference's canonical text
  * ("n m" + one "u v" line per edge, u < v).  mqo_graph_load sniffs the
- * format and uploads to `device` (< 0: host-only). */
+ * format -- binary magic, DIMACS by a leading 'c' or 'p' (graph_io.cpp:98),
+ * else canonical -- and uploads to `device` (< 0: host-only); text errors
+ * are MQO_ERR_PARSE with the reference's "line N: ..." message.
+ * Replaces: Graph load_graph_file(path, warnings*) (graph_io.hpp:45),
+ * void write_graph_file(g, path) (46). */
 int mqo_graph_save(const mqo_graph* g, const char* path, int32_t format);
 int mqo_graph_load(const char* path, int32_t device, mqo_graph** out);
+/* Parse an in-memory graph text: format 0 = sniff (as mqo_graph_load),
+ * 1 = canonical (read_canonical, graph_io.hpp:41), 2 = DIMACS edge format
+ * (parse_dimacs, graph_io.hpp:35; *declared_edges = the 'p' line's m, may
+ * be NULL).  Replaces: DimacsResult parse_dimacs(istream&) /
+ * parse_dimacs_text(const string&) (graph_io.hpp:35-36), Graph
+ * read_canonical(istream&) (41). */
+int mqo_graph_parse(const char* text, int64_t len, int32_t format, int32_t device,
+                    int64_t* declared_edges, mqo_graph** out);
+/* Warnings of the last mqo_graph_load / mqo_graph_parse on this thread
+ * (DimacsResult::warnings, e.g. "declared m=2 but parsed m=1 after
+ * deduplication"), '\n'-separated; returns the full length, copies at most
+ * cap-1 bytes + NUL into buf (buf may be NULL when cap == 0). */
+int64_t mqo_graph_load_warnings(char* buf, int64_t cap);
 
 /* Device pre-processing on a graph in HBM.
  * strip_isolated (graph.hpp:95-104, graph.cpp:180-198): *core = the graph

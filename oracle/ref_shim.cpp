@@ -6,13 +6,16 @@
 // the tests can run the reference itself side by side with the plain-C
 // restatement and with the CUDA path.  Every function forwards to the
 // reference API named in its comment; exceptions become status codes.
+#include <algorithm>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "mqo/graph.hpp"
+#include "mqo/graph_io.hpp"
 #include "mqo/localsearch.hpp"
 #include "mqo/objectives.hpp"
 #include "mqo/pga.hpp"
@@ -387,3 +390,60 @@ int orc_preset_for(int32_t problem, int32_t n, double mean_degree, double* alpha
 }
 
 }  // extern "C"
+
+// ---- graph text formats (reference-only probe; used by
+// tests/golden/make_graph_io_golden.py to freeze the reference's behaviour)
+// fmt 1 = read_canonical (graph_io.cpp:74-87), 2 = parse_dimacs_text
+// (18-71), 0 = load_graph_file's sniffing (94-106) applied to the text.
+// Returns 0 ok, 1 ParseError, 2 invalid_argument, 3 other; on success the
+// CSR goes to off/nbr (caller-sized n+1 / 2m; pass NULL first to size).
+extern "C" int ref_parse_graph(const char* text, int64_t len, int32_t fmt, int32_t* n,
+                               int64_t* m, int64_t* declared, int64_t* off, int32_t* nbr,
+                               char* msg, int64_t cap, int32_t* line) {
+  auto put = [&](const std::string& s) {
+    if (msg && cap > 0) {
+      const size_t k = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(msg, s.data(), k);
+      msg[k] = 0;
+    }
+  };
+  *line = 0;
+  try {
+    std::string t(text, static_cast<size_t>(len));
+    Graph g;
+    std::vector<std::string> warnings;
+    *declared = -1;
+    const bool dimacs = fmt == 2 || (fmt == 0 && !t.empty() && (t[0] == 'c' || t[0] == 'p'));
+    if (dimacs) {
+      DimacsResult r = parse_dimacs_text(t);
+      *declared = r.declared_edges;
+      warnings = r.warnings;
+      g = std::move(r.graph);
+    } else {
+      std::istringstream in(t);
+      g = read_canonical(in);
+    }
+    *n = g.n();
+    *m = g.m();
+    if (off) {
+      for (Vertex v = 0; v <= g.n(); ++v) off[v] = v == 0 ? 0 : off[v - 1] + g.degree(v - 1);
+      int64_t k = 0;
+      for (Vertex v = 0; v < g.n(); ++v)
+        for (Vertex u : g.neighbors(v)) nbr[k++] = u;
+    }
+    std::string w;
+    for (size_t i = 0; i < warnings.size(); ++i) w += (i ? "\n" : "") + warnings[i];
+    put(w);
+    return 0;
+  } catch (const ParseError& e) {
+    put(e.what());
+    *line = e.line();
+    return 1;
+  } catch (const std::invalid_argument& e) {
+    put(e.what());
+    return 2;
+  } catch (const std::exception& e) {
+    put(e.what());
+    return 3;
+  }
+}

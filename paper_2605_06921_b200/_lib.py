@@ -12,7 +12,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmqo_b200.so")
 
-MQO_OK, MQO_ERR_INVALID, MQO_ERR_LOGIC, MQO_ERR_CUDA, MQO_ERR_NCCL, MQO_ERR_OTHER = range(6)
+(MQO_OK, MQO_ERR_INVALID, MQO_ERR_LOGIC, MQO_ERR_CUDA, MQO_ERR_NCCL, MQO_ERR_OTHER,
+ MQO_ERR_PARSE) = range(7)
 MIS_QUBO, LAPLACIAN, PERTURBED_LAPLACIAN, ADJACENCY, PERTURBED_BIAS = range(5)
 PROBLEM_MIS, PROBLEM_MAXCUT = 0, 1
 CONVERGED, CHECKER_ACCEPTED, ITER_CAP = 0, 1, 2
@@ -32,6 +33,14 @@ class InvalidArgument(MqoError, ValueError):
 
 class LogicError(MqoError):
     """std::logic_error in the reference."""
+
+
+class ParseError(MqoError):
+    """mqo::ParseError (graph_io.hpp:13-21): ``line`` is the 1-based line."""
+
+    def __init__(self, code: int, msg: str, line: int):
+        super().__init__(code, msg)
+        self.line = line
 
 
 class Objective(C.Structure):
@@ -54,6 +63,9 @@ _U64 = C.POINTER(C.c_uint64)
 # name -> (restype, argtypes)
 SIGNATURES: dict[str, tuple] = {
     "mqo_last_error": (C.c_char_p, []),
+    "mqo_last_error_line": (C.c_int32, []),
+    "mqo_graph_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, C.c_int32, _I64, _PP]),
+    "mqo_graph_load_warnings": (C.c_int64, [C.c_char_p, C.c_int64]),
     "mqo_version": (C.c_char_p, []),
     "mqo_graph_upload": (C.c_int, [C.c_int32, _I64, _I32, C.c_int32, _PP]),
     "mqo_graph_free": (C.c_int, [_P]),
@@ -118,4 +130,6 @@ def check(rc: int) -> None:
         raise InvalidArgument(rc, msg)
     if rc == MQO_ERR_LOGIC:
         raise LogicError(rc, msg)
+    if rc == MQO_ERR_PARSE:
+        raise ParseError(rc, msg, int(lib.mqo_last_error_line()))
     raise MqoError(rc, msg)

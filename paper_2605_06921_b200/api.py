@@ -22,7 +22,8 @@ import numpy as np
 from . import _lib
 from ._lib import (ADJACENCY, CHECKER_ACCEPTED, CONVERGED, ITER_CAP, LAPLACIAN, MIS_QUBO,
                    PERTURBED_BIAS, PERTURBED_LAPLACIAN, PROBLEM_MAXCUT, PROBLEM_MIS,
-                   InvalidArgument, LogicError, MqoError, Objective, Optimizer, check, lib)
+                   InvalidArgument, LogicError, MqoError, Objective, Optimizer, ParseError, check,
+                   lib)
 
 __all__ = [
     "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "generate", "StripResult",
@@ -32,7 +33,8 @@ __all__ = [
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
     "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
     "solve_maxcut", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
-    "InvalidArgument", "LogicError", "MqoError",
+    "InvalidArgument", "LogicError", "MqoError", "ParseError", "DimacsResult", "parse_dimacs_text",
+    "read_canonical", "write_canonical", "load_graph_file", "write_graph_file",
 ]
 
 
@@ -203,7 +205,8 @@ class Graph:
 
     @staticmethod
     def load(path: str, device: int = 0) -> "Graph":
-        """Binary CSR cache or the reference's canonical text (graph_io.cpp:74-106)."""
+        """Binary CSR cache, DIMACS or the reference's canonical text
+        (load_graph_file, graph_io.cpp:94-106)."""
         h = C.c_void_p()
         check(lib.mqo_graph_load(path.encode(), device, C.byref(h)))
         return Graph(h, device)
@@ -236,6 +239,69 @@ class Graph:
     def neighbors(self, v: int) -> np.ndarray:
         off, nbr = self.csr()
         return nbr[off[v]:off[v + 1]]
+
+
+def _load_warnings() -> list:
+    k = lib.mqo_graph_load_warnings(None, 0)
+    if k <= 0:
+        return []
+    buf = C.create_string_buffer(k + 1)
+    lib.mqo_graph_load_warnings(buf, k + 1)
+    return buf.value.decode().split("\n")
+
+
+@dataclass
+class DimacsResult:  # graph_io.hpp:23-28
+    graph: Graph
+    declared_edges: int
+    parsed_edges: int
+    warnings: list
+
+
+def _parse(text, fmt: int, device: int):
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h, dm = C.c_void_p(), C.c_int64()
+    check(lib.mqo_graph_parse(data, len(data), fmt, device, C.byref(dm), C.byref(h)))
+    return Graph(h, device), dm.value
+
+
+def parse_dimacs_text(text, device: int = 0) -> DimacsResult:
+    """parse_dimacs_text (graph_io.hpp:35-36, graph_io.cpp:18-71): `c`
+    comments, one `p edge <n> <m>` header, 1-based `e <u> <v>` lines;
+    duplicates collapse, a declared/parsed m mismatch is a warning; raises
+    :class:`ParseError` with the reference's line numbers and messages."""
+    g, dm = _parse(text, 2, device)
+    return DimacsResult(g, dm, g.m(), _load_warnings())
+
+
+def read_canonical(text, device: int = 0) -> Graph:
+    """read_canonical (graph_io.hpp:41, graph_io.cpp:74-87)."""
+    return _parse(text, 1, device)[0]
+
+
+def write_canonical(g: Graph) -> str:
+    """write_canonical (graph_io.hpp:42, graph_io.cpp:89-92) as a string."""
+    off, nbr = g.csr()
+    src = np.repeat(np.arange(g.n(), dtype=np.int64), np.diff(off))
+    keep = src < nbr
+    lines = [f"{g.n()} {g.m()}"]
+    lines += [f"{u} {v}" for u, v in zip(src[keep].tolist(), nbr[keep].tolist())]
+    return "\n".join(lines) + "\n"
+
+
+def load_graph_file(path: str, warnings: list | None = None, device: int = 0) -> Graph:
+    """load_graph_file (graph_io.hpp:45, graph_io.cpp:94-106): sniffs DIMACS
+    by a leading 'c'/'p' (else canonical; this backend's binary CSR cache by
+    its magic); DIMACS warnings are appended to ``warnings``."""
+    g = Graph.load(path, device)
+    if warnings is not None:
+        warnings.extend(_load_warnings())
+    return g
+
+
+def write_graph_file(g: Graph, path: str) -> None:
+    """write_graph_file (graph_io.hpp:46): canonical text."""
+    g.save(path, text=True)
 
 
 @dataclass

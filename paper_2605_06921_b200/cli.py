@@ -1,6 +1,10 @@
-"""`mqo solve` / `mqo gen` on the B200 backend.
+"""`mqo solve` / `sweep` / `gen` / `verify` on the B200 backend (SURVEY.md
+section 8f rows 2 and 4).
 
     python -m paper_2605_06921_b200.cli solve --problem mis --gen er:1000:10 --seed 1
+    python -m paper_2605_06921_b200.cli sweep --problem maxcut --gen er:2000:6 \
+        --param rho --values 0.6,0.8 --seeds 1,2,3
+    python -m paper_2605_06921_b200.cli gen --kind ba --n 1000 --m-attach 4 --out ba.g
     python -m paper_2605_06921_b200.cli gen --gen ba:1000000:5 --seed 1 --out ba.csr
 
 Flags, defaults and the flow follow the reference CLI
@@ -8,12 +12,15 @@ Flags, defaults and the flow follow the reference CLI
 preset `auto` (nearest Appendix-G row, explicit flags win), isolated vertices
 stripped before solving and re-embedded after, a RunRecord JSON (report_json
 .cpp:108-137: same fields, bitmaps run-length encoded above 512 vertices)
-and exit codes 0 / 2.  Graph files: the reference's canonical text format or
-this backend's binary CSR cache (`gen --out x.csr`).
+CSV rows (report_json.cpp:139-157), `sweep` over rho / lambda / momentum /
+local-search (cmd_sweep.cpp:27-117) and exit codes 0 / 2.  Graph files:
+DIMACS or the reference's canonical text (graph_io.cpp:94-106), or this
+backend's binary CSR cache (`gen --gen ... --out x.csr`).
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures
 import json
 import math
 import sys
@@ -138,8 +145,9 @@ def run_solve(a) -> dict:
     if bool(a.graph) == bool(a.gen):
         raise UsageError("exactly one of --graph and --gen is required")
     t0 = time.time()
+    load_warnings = []
     if a.graph:
-        g = P.Graph.load(a.graph, device=a.device)
+        g = P.load_graph_file(a.graph, load_warnings, device=a.device)
         desc = {"source": "file", "n": g.n(), "m": g.m(), "path": a.graph}
     else:
         g = P.generate(parse_gen_spec(a.gen), a.seed, device=a.device)
@@ -167,7 +175,7 @@ def run_solve(a) -> dict:
         rep.warnings.append(f"stripped {removed} isolated vertices before solving")
     else:
         rep = P.solve_pooled(g, cfg)
-    warnings = rep.warnings
+    warnings = list(rep.warnings) + load_warnings
     o = cfg.objective
     obj = {"name": [k for k, f in OBJECTIVES.items() if type(f(a)) is type(o)][0]}
     if isinstance(o, P.MisQubo):
@@ -187,6 +195,9 @@ def run_solve(a) -> dict:
     sol = ({"kind": "independent_set", "members": encode_bits(rep.best_body)} if a.problem == "mis"
            else {"kind": "cut_partition", "side": encode_bits(rep.best_body)})
     sol["score"] = rep.best_score
+    if rescore(g, a.problem, decode_bits(sol["members" if a.problem == "mis" else "side"],
+                                         g.n())) != rep.best_score:  # report_json.cpp:133-135
+        raise P.LogicError(2, "run record round-trip: re-scored solution != best score")
     return {"schema_version": SCHEMA_VERSION, "problem": a.problem, "graph": desc,
             "config": config, "best_score": rep.best_score,
             "found_solution": rep.found_solution, "solution": sol,
@@ -202,11 +213,131 @@ def run_solve(a) -> dict:
             "warnings": warnings, "backend": "b200"}
 
 
-def _parser() -> argparse.ArgumentParser:
-    from . import verify
-    ap = argparse.ArgumentParser(prog="mqo", description="mQO on the B200 backend")
-    sub = ap.add_subparsers(dest="cmd", required=True)
-    s = sub.add_parser("solve")
+def rescore(g, problem: str, bits: np.ndarray) -> int:
+    """score_solution on a decoded record body (objectives.cpp:143-180):
+    |I| for an independent set (-1 if dependent), the cut otherwise."""
+    off, nbr = g.csr()
+    src = np.repeat(np.arange(g.n()), np.diff(off))
+    if problem == "mis":
+        if (bits[src] & bits[nbr]).any():
+            return -1
+        return int(bits.sum())
+    return int(((bits[src] != bits[nbr]) & (src < nbr)).sum())
+
+
+CSV_HEADER = ("problem,param,value,seed,n,m,best,after_gradient,after_reset_loop,"
+              "after_local_search,resets_accepted,resets_rejected,outer_loops,"
+              "iterations,elapsed_secs")
+
+
+def _g(x: float) -> str:
+    """std::ostream << double (default precision 6)."""
+    return f"{x:g}"
+
+
+def csv_row(param: str, value: str, rec: dict) -> str:
+    """run_record_csv_row (report_json.cpp:145-157)."""
+    ph, c = rec["phases"], rec["counters"]
+    return ",".join(str(v) for v in (
+        rec["problem"], param, value, rec["config"]["seed"], rec["graph"]["n"],
+        rec["graph"]["m"], rec["best_score"], ph["after_gradient"], ph["after_reset_loop"],
+        ph["after_local_search"], c["resets_accepted"], c["resets_rejected"], c["outer_loops"],
+        c["iterations"], _g(rec["timing"]["solve_secs"])))
+
+
+def dump_record(rec: dict) -> str:
+    """nlohmann::json::dump(): keys sorted, no spaces."""
+    return json.dumps(rec, sort_keys=True, separators=(",", ":"))
+
+
+SWEEP_PARAMS = {"rho": ("rho", float), "lambda": ("lam", float),
+                "momentum": ("momentum", float), "local-search": ("no_local_search", None)}
+
+
+def cmd_sweep(a) -> int:
+    """cmd_sweep.cpp:45-117: the grid values x seeds, solved with `--jobs`
+    concurrent solves (each on its own streams of the same GPU), CSV rows in
+    grid order, then one '# mean' line per value."""
+    values = [v for v in a.values.split(",") if v]
+    if not values:
+        raise UsageError("--values is empty")
+    seeds = [int(x) for x in a.seeds.split(",") if x] if a.seeds else [a.seed]
+    if a.param not in SWEEP_PARAMS:
+        raise UsageError("--param must be rho, lambda, momentum or local-search")
+    grid = []
+    for value in values:
+        for seed in seeds:
+            o = argparse.Namespace(**vars(a))
+            field, conv = SWEEP_PARAMS[a.param]
+            if conv is None:
+                if value not in ("on", "off"):
+                    raise UsageError("local-search values are on/off")
+                o.no_local_search = value == "off"
+            else:
+                try:
+                    setattr(o, field, conv(value))
+                except ValueError as e:
+                    raise UsageError(str(e))
+            o.seed = seed
+            grid.append((o, value))
+    workers = max(1, min(a.jobs, len(grid)))
+    with concurrent.futures.ThreadPoolExecutor(workers) as ex:
+        results = list(ex.map(lambda job: run_solve(job[0]), grid))
+    jsonl = None
+    if a.jsonl:
+        try:
+            jsonl = open(a.jsonl, "w")
+        except OSError:
+            raise UsageError(f"cannot open --jsonl file {a.jsonl}")
+    print(CSV_HEADER)
+    totals = {}
+    for (o, value), rec in zip(grid, results):
+        print(csv_row(a.param, value, rec))
+        sm, cnt = totals.get(value, (0, 0))
+        totals[value] = (sm + rec["best_score"], cnt + 1)
+        if jsonl:
+            jsonl.write(dump_record(rec) + "\n")
+    if jsonl:
+        jsonl.close()
+    for value in values:
+        sm, cnt = totals[value]
+        print(f"# mean {a.param}={value} best={_g(sm / cnt)} over {cnt} seeds")
+    return EXIT_OK
+
+
+def cmd_gen(a) -> int:
+    """cmd_basic.cpp:9-43 (`--kind/--n/...`, canonical text to --out or
+    stdout) or a generator spec (`--gen er:n:d`, binary CSR cache unless
+    --text)."""
+    if a.gen:
+        g = P.generate(parse_gen_spec(a.gen), a.seed, device=-1)
+        g.save(a.out, text=a.text)
+        print(json.dumps({"n": g.n(), "m": g.m(), "out": a.out}))
+        return EXIT_OK
+    if a.n is None:
+        raise UsageError("--n is required")
+    if a.kind == "er":
+        if (a.d is None) == (a.p is None):
+            raise UsageError("er needs exactly one of --d and --p")
+        spec = P.ErSpec(a.n, a.p if a.p is not None else a.d / a.n)
+    elif a.kind == "ba":
+        spec = P.BaSpec(a.n, a.m_attach)
+    else:
+        spec = P.SbmSpec(a.n, a.k, a.p_in, a.p_out)
+    try:
+        g = P.generate(spec, a.seed, device=-1)
+    except P.InvalidArgument as e:
+        raise UsageError(str(e))
+    if a.out:
+        P.write_graph_file(g, a.out)
+        print(f"wrote n={g.n()} m={g.m()} to {a.out}", file=sys.stderr)
+    else:
+        sys.stdout.write(P.write_canonical(g))
+    return EXIT_OK
+
+
+def _add_solve_options(s) -> None:
+    """add_solve_options (main.cpp:11-46)."""
     s.add_argument("--problem", choices=["mis", "maxcut"], default="mis")
     s.add_argument("--graph", default="")
     s.add_argument("--gen", default="")
@@ -221,12 +352,35 @@ def _parser() -> argparse.ArgumentParser:
     s.add_argument("--no-local-search", action="store_true")
     s.add_argument("--objective", choices=list(OBJECTIVES), default="")
     s.add_argument("--preset", choices=["auto", "none"], default="auto")
+    s.add_argument("--report", choices=["json", "csv"], default="json")
     s.add_argument("--out", default="")
     s.add_argument("--device", type=int, default=0)
-    gsub = sub.add_parser("gen")
-    gsub.add_argument("--gen", required=True)
+
+
+def _parser() -> argparse.ArgumentParser:
+    from . import verify
+    ap = argparse.ArgumentParser(prog="mqo", description="mQO on the B200 backend")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    _add_solve_options(sub.add_parser("solve", help="run the mQO solver on one instance"))
+    sw = sub.add_parser("sweep", help="sweep one parameter, emit CSV")
+    _add_solve_options(sw)
+    sw.add_argument("--param", required=True, help="rho | lambda | momentum | local-search")
+    sw.add_argument("--values", required=True, help="comma-separated values")
+    sw.add_argument("--seeds", default="", help="comma-separated seeds (default: --seed)")
+    sw.add_argument("--jobs", type=int, default=1, help="parallel solves")
+    sw.add_argument("--jsonl", default="", help="also write one JSON record per run")
+    gsub = sub.add_parser("gen", help="generate a random graph file")
+    gsub.add_argument("--gen", default="", help="generator spec (binary CSR cache unless --text)")
+    gsub.add_argument("--kind", choices=["er", "ba", "sbm"], default="er")
+    gsub.add_argument("--n", type=int, default=None)
+    gsub.add_argument("--d", type=float, default=None)
+    gsub.add_argument("--p", type=float, default=None)
+    gsub.add_argument("--m-attach", type=int, default=1, dest="m_attach")
+    gsub.add_argument("--k", type=int, default=2)
+    gsub.add_argument("--p-in", type=float, default=0.5, dest="p_in")
+    gsub.add_argument("--p-out", type=float, default=0.05, dest="p_out")
     gsub.add_argument("--seed", type=int, default=1)
-    gsub.add_argument("--out", required=True)
+    gsub.add_argument("--out", default="")
     gsub.add_argument("--text", action="store_true", help="canonical text instead of binary CSR")
     verify.add_parser(sub)
     return ap
@@ -248,12 +402,12 @@ def main(argv=None) -> int:
             from . import verify
             return verify.cmd_verify(a.suite, a.max_n, a.n, a.p, a.seed)
         if a.cmd == "gen":
-            g = P.generate(parse_gen_spec(a.gen), a.seed, device=-1)
-            g.save(a.out, text=a.text)
-            print(json.dumps({"n": g.n(), "m": g.m(), "out": a.out}))
-            return EXIT_OK
+            return cmd_gen(a)
+        if a.cmd == "sweep":
+            return cmd_sweep(a)
         rec = run_solve(a)
-        text = json.dumps(rec, sort_keys=True, separators=(",", ":"))
+        text = (dump_record(rec) if a.report == "json"
+                else CSV_HEADER + "\n" + csv_row("-", "-", rec))
         if a.out:
             with open(a.out, "w") as f:
                 f.write(text + "\n")
@@ -262,7 +416,7 @@ def main(argv=None) -> int:
         for w in rec["warnings"]:
             print(f"warning: {w}", file=sys.stderr)
         return EXIT_OK
-    except (UsageError, P.InvalidArgument, P.LogicError, P.MqoError, OSError, ValueError) as e:
+    except (UsageError, P.MqoError, OSError, ValueError) as e:
         print(f"error: {e}", file=sys.stderr)
         return EXIT_USAGE
 

@@ -9,11 +9,16 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
+#include <iterator>
+#include <ostream>
+#include <sstream>
 #include <limits>
 #include <stdexcept>
 #include <string>
 
 #include "mqo/graph.hpp"
+#include "mqo/graph_io.hpp"
 #include "mqo/localsearch.hpp"
 #include "mqo/objectives.hpp"
 #include "mqo/pga.hpp"
@@ -35,6 +40,11 @@ void check(int rc) {
   const std::string msg = mqo_last_error();
   if (rc == MQO_ERR_INVALID) throw std::invalid_argument(msg);
   if (rc == MQO_ERR_LOGIC) throw std::logic_error(msg);
+  if (rc == MQO_ERR_PARSE) {  // the ABI message already reads "line N: ..."
+    const int line = mqo_last_error_line();
+    const std::string prefix = "line " + std::to_string(line) + ": ";
+    throw ParseError(line, msg.rfind(prefix, 0) == 0 ? msg.substr(prefix.size()) : msg);
+  }
   throw std::runtime_error(msg);
 }
 
@@ -713,6 +723,68 @@ Preset preset_for(Problem problem, Vertex n, double mean_degree) {
     }
   }
   return out;
+}
+
+// --------------------------------------------------------------- graph_io
+namespace {
+
+std::vector<std::string> load_warnings() {
+  std::vector<std::string> out;
+  const int64_t k = mqo_graph_load_warnings(nullptr, 0);
+  if (k <= 0) return out;
+  std::string buf(static_cast<size_t>(k) + 1, '\0');
+  mqo_graph_load_warnings(buf.data(), k + 1);
+  buf.resize(static_cast<size_t>(k));
+  std::istringstream in(buf);
+  for (std::string w; std::getline(in, w);) out.push_back(w);
+  return out;
+}
+
+Graph parse_text(const std::string& text, int32_t format, int64_t* declared) {
+  mqo_graph* h = nullptr;
+  check(mqo_graph_parse(text.data(), static_cast<int64_t>(text.size()), format, g_device,
+                        declared, &h));
+  return Graph::adopt(h);
+}
+
+}  // namespace
+
+DimacsResult parse_dimacs_text(const std::string& text) {
+  DimacsResult r;
+  r.graph = parse_text(text, 2, &r.declared_edges);
+  r.parsed_edges = r.graph.m();
+  r.warnings = load_warnings();
+  return r;
+}
+
+DimacsResult parse_dimacs(std::istream& in) {
+  return parse_dimacs_text(std::string(std::istreambuf_iterator<char>(in), {}));
+}
+
+Graph read_canonical(std::istream& in) {
+  return parse_text(std::string(std::istreambuf_iterator<char>(in), {}), 1, nullptr);
+}
+
+void write_canonical(const Graph& g, std::ostream& out) {
+  out << g.n() << ' ' << g.m() << '\n';
+  for (const auto& [u, v] : g.edges()) out << u << ' ' << v << '\n';
+}
+
+Graph load_graph_file(const std::string& path, std::vector<std::string>* warnings) {
+  mqo_graph* h = nullptr;
+  const int rc = mqo_graph_load(path.c_str(), g_device, &h);
+  check(rc);
+  if (warnings) {
+    const auto w = load_warnings();
+    warnings->insert(warnings->end(), w.begin(), w.end());
+  }
+  return Graph::adopt(h);
+}
+
+void write_graph_file(const Graph& g, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open output file: " + path);
+  write_canonical(g, out);
 }
 
 }  // namespace mqo

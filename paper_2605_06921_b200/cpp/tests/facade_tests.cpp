@@ -6,12 +6,15 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
 #include <functional>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "mqo/graph.hpp"
+#include "mqo/graph_io.hpp"
 #include "mqo/localsearch.hpp"
 #include "mqo/objectives.hpp"
 #include "mqo/pga.hpp"
@@ -125,6 +128,59 @@ static void test_graph() {
   const auto sr = strip_isolated(Graph::from_edges(5, {{0, 2}}));
   CHECK(sr.core.n() == 2 && sr.removed == (std::vector<Vertex>{1, 3, 4}));
   CHECK(connected_components(path(4)).size() == 1);
+}
+
+// test_graph.cpp:132-189
+static void test_graph_io() {
+  {
+    const auto r = parse_dimacs_text("c a comment\np edge 3 3\ne 1 2\ne 2 3\ne 1 3\n");
+    CHECK(r.graph.n() == 3 && r.graph.m() == 3 && r.warnings.empty());
+  }
+  {
+    const auto r = parse_dimacs_text("p edge 3 2\ne 1 2\ne 2 1\n");
+    CHECK(r.graph.n() == 3 && r.graph.m() == 1);
+    CHECK(r.warnings.size() == 1 && r.warnings[0].find("declared m=2") != std::string::npos);
+  }
+  {
+    bool ok = false;
+    try {
+      parse_dimacs_text("e 1 2\n");
+    } catch (const ParseError& e) {
+      ok = std::string(e.what()) == "line 1: edge before 'p edge <n> <m>' header" && e.line() == 1;
+    }
+    CHECK(ok);
+    int line = 0;
+    try {
+      parse_dimacs_text("p edge 3 2\ne 1 2\ne 1 9\n");
+    } catch (const ParseError& e) {
+      line = e.line();
+    }
+    CHECK(line == 3);
+    CHECK_THROWS_AS(parse_dimacs_text("p edge 3 1\ne 1 1\n"), ParseError);
+    CHECK_THROWS_AS(parse_dimacs_text("p edge 3 1\nq 1 2\n"), ParseError);
+    CHECK_THROWS_AS(parse_dimacs_text("p edge 3 1\ne one two\n"), ParseError);
+  }
+  {
+    const Graph g = er(37, 0.2, 21);
+    std::stringstream buffer;
+    write_canonical(g, buffer);
+    const Graph back = read_canonical(buffer);
+    CHECK(back.n() == g.n() && back.edges() == g.edges());
+  }
+  {
+    const Graph g = er(12, 0.3, 31);
+    const std::string canon = "/tmp/mqo_b200_test_canonical.g";
+    write_graph_file(g, canon);
+    CHECK(load_graph_file(canon).edges() == g.edges());
+    const std::string dimacs = "/tmp/mqo_b200_test_dimacs.g";
+    {
+      std::ofstream out(dimacs);
+      out << "c tiny triangle\np edge 3 3\ne 1 2\ne 2 3\ne 1 3\n";
+    }
+    std::vector<std::string> warnings;
+    const Graph k3 = load_graph_file(dimacs, &warnings);
+    CHECK(k3.n() == 3 && k3.m() == 3 && warnings.empty());
+  }
 }
 
 static void test_objectives() {
@@ -324,7 +380,8 @@ static void test_solver() {
 
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> suites = {
-      {"graph", test_graph},         {"objectives", test_objectives}, {"pga", test_pga},
+      {"graph", test_graph},         {"graph_io", test_graph_io},
+      {"objectives", test_objectives}, {"pga", test_pga},
       {"localsearch", test_localsearch}, {"solver", test_solver}};
   for (const auto& [name, fn] : suites) {
     const int before = g_fail;

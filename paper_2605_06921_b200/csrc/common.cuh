@@ -20,6 +20,15 @@ namespace mqo_b200 {
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
+void set_error_line(int32_t line);
+
+// graph_io.hpp:13-21: a parse failure with the offending 1-based line
+// (a std::runtime_error in the reference; MQO_ERR_PARSE at the ABI).
+struct ParseError : std::runtime_error {
+  int32_t line;
+  ParseError(int32_t l, const std::string& what)
+      : std::runtime_error("line " + std::to_string(l) + ": " + what), line(l) {}
+};
 
 // MQO_TRACE=1: one stderr line per engine / trajectory stage (debugging).
 bool trace_on();
@@ -51,6 +60,10 @@ int guard(F&& f) {
   try {
     f();
     return MQO_OK;
+  } catch (const ParseError& e) {
+    set_error(e.what());
+    set_error_line(e.line);
+    return MQO_ERR_PARSE;
   } catch (const std::invalid_argument& e) {
     set_error(e.what());
     return MQO_ERR_INVALID;

@@ -16,7 +16,12 @@
 namespace mqo_b200 {
 
 static thread_local std::string g_last_error;
-void set_error(const std::string& msg) { g_last_error = msg; }
+static thread_local int32_t g_last_error_line = 0;
+void set_error(const std::string& msg) {
+  g_last_error = msg;
+  g_last_error_line = 0;
+}
+void set_error_line(int32_t line) { g_last_error_line = line; }
 double trace_clock() {
   timespec ts;
   clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -35,6 +40,7 @@ bool trace_on() {
 using namespace mqo_b200;
 
 extern "C" const char* mqo_last_error(void) { return g_last_error.c_str(); }
+extern "C" int32_t mqo_last_error_line(void) { return g_last_error_line; }
 extern "C" const char* mqo_version(void) { return "mqo_b200 0.1 sm_100a"; }
 
 extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t* neighbors,

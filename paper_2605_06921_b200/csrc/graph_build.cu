@@ -4,6 +4,7 @@
 // reference, so a (spec, seed) pair yields the identical CSR; the result is
 // uploaded to HBM by mqo_graph_upload.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -236,10 +237,168 @@ extern "C" int mqo_graph_save(const mqo_graph* g, const char* path, int32_t form
   });
 }
 
-extern "C" int mqo_graph_load(const char* path, int32_t device, mqo_graph** out) {
+// ------------------------------------------------------- text formats
+// graph_io.cpp:18-87, re-stated over an in-memory buffer: istream `>>`
+// semantics for the tokens (whitespace-separated, an integer read stops at
+// its first non-digit), the reference's ParseError messages and line numbers.
+namespace {
+
+thread_local std::string g_load_warnings;
+
+struct Cursor {
+  const char* p;
+  const char* end;
+  static bool ws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r' || c == '\v' || c == '\f'; }
+  void skip_ws() { while (p < end && ws(*p)) ++p; }
+  // operator>>(int64_t&): skip whitespace, optional sign, >= 1 digit; overflow fails
+  bool read_i64(int64_t& out) {
+    skip_ws();
+    const char* q = p;
+    bool neg = false;
+    if (q < end && (*q == '+' || *q == '-')) neg = *q++ == '-';
+    if (q >= end || *q < '0' || *q > '9') return false;
+    unsigned long long v = 0;
+    const unsigned long long lim = neg ? 9223372036854775808ull : 9223372036854775807ull;
+    for (; q < end && *q >= '0' && *q <= '9'; ++q) {
+      const unsigned d = static_cast<unsigned>(*q - '0');
+      if (v > (lim - d) / 10) return false;
+      v = v * 10 + d;
+    }
+    p = q;
+    out = neg ? static_cast<int64_t>(0ull - v) : static_cast<int64_t>(v);
+    return true;
+  }
+  bool read_i32(int32_t& out) {  // operator>>(int&): out-of-range fails
+    int64_t v = 0;
+    if (!read_i64(v) || v < INT32_MIN || v > INT32_MAX) return false;
+    out = static_cast<int32_t>(v);
+    return true;
+  }
+  std::string read_token() {
+    skip_ws();
+    const char* q = p;
+    while (p < end && !ws(*p)) ++p;
+    return std::string(q, p);
+  }
+};
+
+// read_canonical (graph_io.cpp:74-87)
+void parse_canonical(const char* text, size_t len, int32_t& n, std::vector<int64_t>& off,
+                     std::vector<int32_t>& nbr) {
+  Cursor c{text, text + len};
+  int64_t m = 0;
+  if (!c.read_i32(n) || !c.read_i64(m)) throw ParseError(1, "missing 'n m' header");
+  // edges.reserve(static_cast<size_t>(m)) (graph_io.cpp:79) throws for m < 0
+  if (m < 0) throw std::length_error("vector::reserve");
+  std::vector<int32_t> eu, ev;
+  if (m > 0) {
+    eu.reserve(static_cast<size_t>(std::min<int64_t>(m, int64_t(1) << 32)));
+    ev.reserve(eu.capacity());
+  }
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t u = 0, v = 0;
+    if (!c.read_i64(u) || !c.read_i64(v))
+      throw ParseError(static_cast<int32_t>(i + 2), "truncated edge list");
+    eu.push_back(static_cast<int32_t>(u));  // static_cast<Vertex>, as the reference
+    ev.push_back(static_cast<int32_t>(v));
+  }
+  build_from_edges(n, static_cast<int64_t>(eu.size()), eu.data(), ev.data(), off, nbr);
+}
+
+// parse_dimacs (graph_io.cpp:18-66)
+void parse_dimacs(const char* text, size_t len, int32_t& n, std::vector<int64_t>& off,
+                  std::vector<int32_t>& nbr, int64_t& declared_m) {
+  const char* p = text;
+  const char* end = text + len;
+  int32_t lineno = 0;
+  bool have_header = false;
+  n = 0;
+  declared_m = 0;
+  std::vector<int32_t> eu, ev;
+  while (p < end) {
+    const char* eol = static_cast<const char*>(std::memchr(p, '\n', static_cast<size_t>(end - p)));
+    if (!eol) eol = end;
+    ++lineno;
+    Cursor c{p, eol};
+    p = eol < end ? eol + 1 : end;
+    const std::string tag = c.read_token();
+    if (tag.empty()) continue;  // blank line
+    if (tag == "c") continue;
+    if (tag == "p") {
+      if (have_header) throw ParseError(lineno, "duplicate 'p' line");
+      const std::string fmt = c.read_token();
+      int64_t dm = 0;
+      if (fmt.empty() || !c.read_i32(n) || !c.read_i64(dm))
+        throw ParseError(lineno, "malformed 'p' line, expected 'p edge <n> <m>'");
+      if (n < 0 || dm < 0) throw ParseError(lineno, "negative n or m");
+      declared_m = dm;
+      have_header = true;
+      continue;
+    }
+    if (tag == "e") {
+      if (!have_header) throw ParseError(lineno, "edge before 'p edge <n> <m>' header");
+      int64_t u = 0, v = 0;
+      if (!c.read_i64(u) || !c.read_i64(v)) throw ParseError(lineno, "malformed 'e' line");
+      if (u < 1 || u > n || v < 1 || v > n) throw ParseError(lineno, "vertex index outside [1, n]");
+      if (u == v) throw ParseError(lineno, "self-loop");
+      eu.push_back(static_cast<int32_t>(u - 1));
+      ev.push_back(static_cast<int32_t>(v - 1));
+      continue;
+    }
+    throw ParseError(lineno, "unrecognized line tag '" + tag + "'");
+  }
+  if (!have_header) throw ParseError(lineno, "missing 'p edge <n> <m>' header");
+  build_from_edges(n, static_cast<int64_t>(eu.size()), eu.data(), ev.data(), off, nbr);
+  const int64_t parsed = static_cast<int64_t>(nbr.size() / 2);
+  if (parsed != declared_m)
+    g_load_warnings = "declared m=" + std::to_string(declared_m) + " but parsed m=" +
+                      std::to_string(parsed) + " after deduplication";
+}
+
+bool looks_dimacs(const char* text, size_t len) {  // graph_io.cpp:97-98: peek()
+  return len > 0 && (text[0] == 'c' || text[0] == 'p');
+}
+
+}  // namespace
+
+extern "C" int mqo_graph_parse(const char* text, int64_t len, int32_t format, int32_t device,
+                               int64_t* declared_edges, mqo_graph** out) {
   std::vector<int64_t> off;
   std::vector<int32_t> nbr;
   int32_t n = 0;
+  g_load_warnings.clear();
+  const int rc = guard([&] {
+    if ((!text && len > 0) || len < 0 || !out) throw std::invalid_argument("mqo_graph_parse: bad arguments");
+    if (format < 0 || format > 2) throw std::invalid_argument("mqo_graph_parse: unknown format");
+    const bool dimacs = format == 2 || (format == 0 && looks_dimacs(text, static_cast<size_t>(len)));
+    int64_t dm = 0;
+    if (dimacs)
+      parse_dimacs(text, static_cast<size_t>(len), n, off, nbr, dm);
+    else
+      parse_canonical(text, static_cast<size_t>(len), n, off, nbr);
+    if (declared_edges) *declared_edges = dimacs ? dm : static_cast<int64_t>(nbr.size() / 2);
+  });
+  if (rc) return rc;
+  return mqo_graph_upload(n, off.data(), nbr.data(), device, out);
+}
+
+extern "C" int64_t mqo_graph_load_warnings(char* buf, int64_t cap) {
+  const int64_t len = static_cast<int64_t>(g_load_warnings.size());
+  if (buf && cap > 0) {
+    const int64_t k = std::min(len, cap - 1);
+    std::memcpy(buf, g_load_warnings.data(), static_cast<size_t>(k));
+    buf[k] = 0;
+  }
+  return len;
+}
+
+extern "C" int mqo_graph_load(const char* path, int32_t device, mqo_graph** out) {
+  std::vector<int64_t> off;
+  std::vector<int32_t> nbr;
+  std::string text;
+  int32_t n = 0;
+  bool is_text = false;
+  g_load_warnings.clear();
   const int rc = guard([&] {
     if (!path || !out) throw std::invalid_argument("mqo_graph_load: null argument");
     FILE* f = std::fopen(path, "rb");
@@ -262,27 +421,17 @@ extern "C" int mqo_graph_load(const char* path, int32_t device, mqo_graph** out)
       if (!ok) throw std::invalid_argument("graph file: truncated binary CSR");
       return;
     }
-    // read_canonical (graph_io.cpp:74-87)
+    std::fseek(f, 0, SEEK_END);
+    const long size = std::ftell(f);
     std::rewind(f);
-    long long nn = 0, mm = 0;
-    if (std::fscanf(f, "%lld %lld", &nn, &mm) != 2) {
-      std::fclose(f);
-      throw std::invalid_argument("line 1: missing 'n m' header");
-    }
-    std::vector<int32_t> eu(static_cast<size_t>(mm)), ev(static_cast<size_t>(mm));
-    for (long long i = 0; i < mm; ++i) {
-      long long u = 0, v = 0;
-      if (std::fscanf(f, "%lld %lld", &u, &v) != 2) {
-        std::fclose(f);
-        throw std::invalid_argument("line " + std::to_string(i + 2) + ": truncated edge list");
-      }
-      eu[i] = static_cast<int32_t>(u);
-      ev[i] = static_cast<int32_t>(v);
-    }
+    text.resize(size > 0 ? static_cast<size_t>(size) : 0);
+    const bool ok = text.empty() || std::fread(&text[0], 1, text.size(), f) == text.size();
     std::fclose(f);
-    n = static_cast<int32_t>(nn);
-    build_from_edges(n, mm, eu.data(), ev.data(), off, nbr);
+    if (!ok) throw std::runtime_error(std::string("cannot read graph file: ") + path);
+    is_text = true;
   });
   if (rc) return rc;
+  if (is_text)
+    return mqo_graph_parse(text.data(), static_cast<int64_t>(text.size()), 0, device, nullptr, out);
   return mqo_graph_upload(n, off.data(), nbr.data(), device, out);
 }

@@ -112,3 +112,93 @@ def test_verify_suites(cuda_ok):
     r = cli("verify", "--suite", "exact", "--max-n", "10")
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("[PASS]") == 3
+
+
+def test_gen_reference_flags_match_oracle(tmp_path):
+    """cmd_basic.cpp:9-43: `gen --kind ...` writes the canonical text of
+    the reference generator's graph (stdout or --out)."""
+    O = oracle.load("oracle")
+    r = cli("gen", "--kind", "ba", "--n", "60", "--m-attach", "3", "--seed", "77")
+    assert r.returncode == 0, r.stderr
+    og = O.generate_ba(60, 3, 77)
+    off, nbr = og.csr()
+    src = np.repeat(np.arange(60), np.diff(off))
+    m = src < nbr
+    want = f"60 {og.m}\n" + "".join(f"{u} {v}\n" for u, v in zip(src[m], nbr[m]))
+    assert r.stdout == want
+    out = tmp_path / "er.g"
+    r = cli("gen", "--kind", "er", "--n", "80", "--d", "4", "--seed", "3", "--out", str(out))
+    assert r.returncode == 0 and "wrote n=80" in r.stderr
+    og = O.generate_er(80, 4 / 80, 3)
+    assert out.read_text().splitlines()[0] == f"80 {og.m}"
+    assert cli("gen", "--kind", "er", "--n", "80").returncode == 2           # neither --d nor --p
+    assert cli("gen", "--kind", "ba", "--n", "5", "--m-attach", "9").returncode == 2
+
+
+def test_sweep_usage_errors():
+    base = ("sweep", "--gen", "er:100:3")
+    assert cli(*base, "--param", "alpha", "--values", "1").returncode == 2
+    assert cli(*base, "--param", "rho", "--values", ",").returncode == 2
+    assert cli(*base, "--param", "local-search", "--values", "maybe").returncode == 2
+    assert cli(*base, "--param", "rho", "--values", "abc").returncode == 2
+
+
+def test_csv_row_format():
+    from paper_2605_06921_b200.cli import CSV_HEADER, csv_row
+    rec = {"problem": "mis", "config": {"seed": 3}, "graph": {"n": 10, "m": 12},
+           "best_score": 4, "phases": {"after_gradient": 3, "after_reset_loop": 4,
+                                       "after_local_search": 4},
+           "counters": {"resets_accepted": 5, "resets_rejected": 6, "outer_loops": 1,
+                        "iterations": 1234},
+           "timing": {"solve_secs": 0.123456789}}
+    assert CSV_HEADER.count(",") == csv_row("rho", "0.6", rec).count(",")
+    assert csv_row("rho", "0.6", rec) == "mis,rho,0.6,3,10,12,4,3,4,4,5,6,1,1234,0.123457"
+
+
+@pytest.mark.gpu
+def test_sweep_rows_match_single_solves(cuda_ok, tmp_path):
+    """cmd_sweep.cpp: every grid cell is exactly `solve` with that value and
+    seed (also with --jobs 2), rows in grid order, '# mean' per value."""
+    common = ("--problem", "maxcut", "--gen", "er:300:4", "--max-outer", "1",
+              "--budget-secs", "600")
+    jl = tmp_path / "s.jsonl"
+    r = cli("sweep", *common, "--param", "rho", "--values", "0.5,0.8", "--seeds", "1,2",
+            "--jobs", "2", "--jsonl", str(jl))
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    assert lines[0].startswith("problem,param,value,seed")
+    rows = [ln.split(",") for ln in lines[1:5]]
+    assert [(x[2], x[3]) for x in rows] == [("0.5", "1"), ("0.5", "2"), ("0.8", "1"), ("0.8", "2")]
+    recs = [json.loads(x) for x in jl.read_text().splitlines()]
+    for row, rec in zip(rows, recs):
+        single = cli("solve", *common, "--rho", row[2], "--seed", row[3])
+        one = json.loads(single.stdout)
+        assert int(row[6]) == rec["best_score"] == one["best_score"]
+        assert one["counters"]["iterations"] == rec["counters"]["iterations"] == int(row[13])
+        assert one["solution"] == rec["solution"]
+    means = [ln for ln in lines if ln.startswith("# mean")]
+    assert len(means) == 2 and means[0].startswith("# mean rho=0.5 best=")
+
+
+@pytest.mark.gpu
+def test_solve_dimacs_file_and_csv(cuda_ok, tmp_path):
+    """--graph with a DIMACS file (warnings carried into the record) and
+    --report csv."""
+    O = oracle.load("oracle")
+    og = O.generate_er(120, 0.05, 9)
+    off, nbr = og.csr()
+    src = np.repeat(np.arange(120), np.diff(off))
+    m = src < nbr
+    path = tmp_path / "g.dimacs"
+    path.write_text(f"c test\np edge 120 {og.m + 1}\n" +
+                    "".join(f"e {u + 1} {v + 1}\n" for u, v in zip(src[m], nbr[m])))
+    r = cli("solve", "--graph", str(path), "--max-outer", "1", "--budget-secs", "600")
+    assert r.returncode == 0, r.stderr
+    rec = json.loads(r.stdout)
+    assert rec["graph"] == {"source": "file", "n": 120, "m": og.m, "path": str(path)}
+    assert f"declared m={og.m + 1} but parsed m={og.m} after deduplication" in rec["warnings"]
+    r2 = cli("solve", "--graph", str(path), "--max-outer", "1", "--budget-secs", "600",
+             "--report", "csv")
+    hdr, row = r2.stdout.splitlines()
+    assert hdr.startswith("problem,param") and row.split(",")[:7] == [
+        "mis", "-", "-", "1", "120", str(og.m), str(rec["best_score"])]
