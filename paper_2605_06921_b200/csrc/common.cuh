@@ -175,6 +175,7 @@ struct mqo_batch {
   int32_t* d_valid = nullptr;           // [Bp]
   int32_t* d_pick = nullptr;            // [Bp] pool index drawn per chain
   uint8_t* d_state8 = nullptr;          // [n][Bp] harvest / local-search states
+  uint32_t* d_sides = nullptr;          // [n][4*ceil(B/128)] MaxCut side bits, chain-minor
   int32_t* d_lastw = nullptr;           // [Bp][n] reset scratch
   int32_t* d_jdraw = nullptr;           // [Bp][n] reset draws j_i
   int32_t* d_counter = nullptr;         // [4] device counters

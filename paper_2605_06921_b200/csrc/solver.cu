@@ -450,34 +450,83 @@ __global__ void k_pack(const uint8_t* __restrict__ st, const double* __restrict_
   }
 }
 
-// cut_value (objectives.cpp:163-171) from packed sides.
-__global__ void k_cut(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
-                      int32_t B, const uint64_t* __restrict__ bodies, int64_t W,
-                      int64_t* __restrict__ cut) {
-  const int64_t total = static_cast<int64_t>(n) * B;
-  unsigned long long local = 0;
-  int lastb = -1;
-  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
-       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int b = static_cast<int>(q / n);
-    const int64_t v = q % n;
-    if (b != lastb) {
-      if (local && lastb >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(cut + lastb), local);
-      local = 0;
-      lastb = b;
+// cut_value (objectives.cpp:163-171) for all chains at once, vertex-major.
+// K5a: side bits chain-minor -- one ballot per (vertex, 32 chains) over a
+// coalesced row of X (side_v = [x_v > 0], objectives.cpp:153-157, the same
+// predicate k_pack uses); words per vertex padded to a multiple of 4 so a
+// 128-chain slice is one 16-byte load.
+__global__ void k_side_bits(const double* __restrict__ X, int32_t n, int32_t B, int32_t Bp,
+                            int32_t words, uint32_t* __restrict__ sides) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = static_cast<int64_t>(n) * words;
+  for (int64_t q = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; q < total;
+       q += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t v = q / words;
+    const int c = static_cast<int>(q % words) * 32 + lane;
+    const bool on = c < B && X[v * Bp + c] > 0.0;
+    const uint32_t bits = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) sides[q] = bits;
+  }
+}
+
+// K5b: one warp per row v (grid-stride), 128 chains per pass: lane l counts
+// chains l, l+32, l+64, l+96.  The row's neighbour ids are loaded 32 at a
+// time (coalesced) and broadcast by shuffle; every edge (v, u > v) costs one
+// 16-byte broadcast load of u's side bits and an XOR -- the CSR is read
+// once per 128 chains instead of once per chain.
+__global__ void k_cut_vm(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                         int32_t n, int32_t B, int32_t words, const uint32_t* __restrict__ sides,
+                         int64_t* __restrict__ cut) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int c4 = 0; c4 < words; c4 += 4) {
+    uint32_t cnt[4] = {0, 0, 0, 0};
+    for (int64_t v = warp; v < n; v += nwarps) {
+      const uint4 sv = __ldg(reinterpret_cast<const uint4*>(sides + v * words + c4));
+      const int64_t e0 = off[v], e1 = off[v + 1];
+      for (int64_t base = e0; base < e1; base += 32) {
+        const int32_t mine = base + lane < e1 ? __ldg(nbr + base + lane) : -1;
+        const int k = e1 - base < 32 ? static_cast<int>(e1 - base) : 32;
+#pragma unroll 8
+        for (int j = 0; j < k; ++j) {
+          const int32_t u = __shfl_sync(0xffffffffu, mine, j);
+          if (u > v) {
+            const uint4 su = __ldg(reinterpret_cast<const uint4*>(sides + int64_t(u) * words + c4));
+            cnt[0] += ((sv.x ^ su.x) >> lane) & 1u;
+            cnt[1] += ((sv.y ^ su.y) >> lane) & 1u;
+            cnt[2] += ((sv.z ^ su.z) >> lane) & 1u;
+            cnt[3] += ((sv.w ^ su.w) >> lane) & 1u;
+          }
+        }
+      }
     }
-    const uint64_t* body = bodies + static_cast<int64_t>(b) * W;
-    const int sv = (body[v >> 6] >> (63 - (v & 63))) & 1;
-    for (int64_t e = off[v]; e < off[v + 1]; ++e) {
-      const int32_t u = nbr[e];
-      if (u > v) local += sv != static_cast<int>((body[u >> 6] >> (63 - (u & 63))) & 1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int chain = (c4 + k) * 32 + lane;
+      if (chain < B && cnt[k])
+        atomicAdd(reinterpret_cast<unsigned long long*>(cut + chain),
+                  static_cast<unsigned long long>(cnt[k]));
     }
   }
-  if (local && lastb >= 0) atomicAdd(reinterpret_cast<unsigned long long*>(cut + lastb), local);
 }
 
 int grid_for(int64_t work, int threads = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, 148 * 32)));
+}
+
+// Cut values of the current iterates into d_scores (zeroed by the caller).
+void launch_cut(mqo_batch* b, const double* X) {
+  const mqo_graph* g = b->g;
+  const int32_t words = ((b->B + 31) / 32 + 3) / 4 * 4;
+  if (!b->d_sides)
+    MQO_CUDA(cudaMalloc(&b->d_sides, sizeof(uint32_t) * std::max<int64_t>(1, int64_t(g->n) * words)));
+  k_side_bits<<<grid_for(int64_t(g->n) * words * 32), 256, 0, b->stream>>>(X, g->n, b->B, b->Bp,
+                                                                          words, b->d_sides);
+  MQO_CUDA(cudaGetLastError());
+  k_cut_vm<<<148 * 8, 256, 0, b->stream>>>(g->d_off, g->d_nbr, g->n, b->B, words, b->d_sides,
+                                           b->d_scores);
+  MQO_CUDA(cudaGetLastError());
 }
 
 void ensure_solver_buffers(mqo_batch* b) {
@@ -520,6 +569,7 @@ void free_solver_buffers(mqo_batch* b) {
   cudaFree(b->d_valid);
   cudaFree(b->d_pick);
   cudaFree(b->d_state8);
+  cudaFree(b->d_sides);
   cudaFree(b->d_lastw);
   cudaFree(b->d_jdraw);
   cudaFree(b->d_counter);
@@ -652,11 +702,7 @@ void harvest_device(mqo_batch* b, int32_t problem) {
     k_pack<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, b->stream>>>(
         b->d_state8, X, problem == MQO_PROBLEM_MIS, n, b->B, b->Bp, b->d_bodies, W, b->d_scores);
     MQO_CUDA(cudaGetLastError());
-    if (problem == MQO_PROBLEM_MAXCUT) {
-      k_cut<<<grid_for(int64_t(n) * b->B), 256, 0, b->stream>>>(g->d_off, g->d_nbr, n, b->B,
-                                                                b->d_bodies, W, b->d_scores);
-      MQO_CUDA(cudaGetLastError());
-    }
+    if (problem == MQO_PROBLEM_MAXCUT) launch_cut(b, X);
   }
 }
 
@@ -817,9 +863,7 @@ extern "C" int mqo_extract(mqo_batch* b, int32_t problem, int64_t* scores, int32
       const int64_t warps = W * b->B;
       k_pack<<<static_cast<int>((warps * 32 + 255) / 256), 256, 0, b->stream>>>(
           b->d_state8, X, problem == MQO_PROBLEM_MIS, n, b->B, b->Bp, b->d_bodies, W, b->d_scores);
-      if (problem == MQO_PROBLEM_MAXCUT)
-        k_cut<<<grid_for(int64_t(n) * b->B), 256, 0, b->stream>>>(g->d_off, g->d_nbr, n, b->B,
-                                                                  b->d_bodies, W, b->d_scores);
+      if (problem == MQO_PROBLEM_MAXCUT) launch_cut(b, X);
       MQO_CUDA(cudaGetLastError());
     }
     std::vector<int32_t> dep(b->B);

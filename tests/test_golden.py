@@ -79,7 +79,7 @@ def test_generators_product_host(name):
 
 
 def test_from_edges_product_host():
-    from paper_2605_06921_b200 import Graph, InvalidArgument
+    from paper_2605_06921_b200 import Graph, InvalidArgument, ParseError  # noqa: F401
     z = load("graphs")
     off, nbr = z["er1000_off"], z["er1000_nbr"]
     edges = [(v, int(u)) for v in range(1000) for u in nbr[off[v]:off[v + 1]]]
@@ -202,7 +202,7 @@ def test_engine_reports(O, name):
 
 def test_graph_files_roundtrip(tmp_path):
     """Binary CSR cache and the reference's canonical text format."""
-    from paper_2605_06921_b200 import Graph, InvalidArgument
+    from paper_2605_06921_b200 import Graph, InvalidArgument, ParseError  # noqa: F401
     z = load("graphs")
     g = Graph.from_csr(z["er2000_off"], z["er2000_nbr"], device=-1)
     for text in (False, True):
@@ -213,5 +213,5 @@ def test_graph_files_roundtrip(tmp_path):
     lines = open(str(tmp_path / "g.txt")).read().split("\n")
     assert lines[0] == f"{g.n()} {g.m()}"
     (tmp_path / "bad.txt").write_text("5 2\n0 1\n")
-    with pytest.raises(InvalidArgument, match="truncated"):
+    with pytest.raises(ParseError, match="line 3: truncated edge list"):  # graph_io.cpp:83
         Graph.load(str(tmp_path / "bad.txt"), device=-1)

@@ -133,9 +133,9 @@ def _harvest_ref(O, og, problem, x):
     return body, score
 
 
-@pytest.mark.parametrize("problem", [0, 1])
-def test_harvest(O, P, problem):
-    n, B = 2000, 40
+@pytest.mark.parametrize("problem,B", [(0, 40), (1, 40), (1, 3), (1, 200)])
+def test_harvest(O, P, problem, B):
+    n = 2000
     og = O.generate_er(n, 6.0 / n, 4)
     pg = P.generate(P.ErSpec(n, 6.0 / n), 4)
     rng = np.random.default_rng(problem)
@@ -150,8 +150,9 @@ def test_harvest(O, P, problem):
                             max_iters=60)
     b.run_trajectories(spec, cfg)
     Xt = b.get_x()
-    Xt[:5] = X[:5]  # raw random states: MIS sets are dependent
-    Xt[5] = 0.0     # empty set: greedy from nothing
+    k = min(5, B - 1)
+    Xt[:k] = X[:k]  # raw random states: MIS sets are dependent
+    Xt[k] = 0.0     # empty set: greedy from nothing
     b.set_x(Xt)
     scores, valid, packed = b.harvest(problem)
     bodies = P.unpack_bodies(packed, n)
