@@ -333,11 +333,16 @@ typedef struct {
 
 /* Optional communicator for sharding the B chains over ranks (one process
  * per GPU).  allgather: every rank contributes `bytes` from `send`; `recv`
- * receives world * bytes in rank order.  Return 0 on success. */
+ * receives world * bytes in rank order.  allreduce_max_u64 (in place,
+ * element-wise max over ranks) and broadcast (`bytes` of `buf` from rank
+ * `root` to all) are used by mqo_solve_replicas; either may be NULL, and is
+ * then emulated with allgather.  Return 0 on success. */
 typedef struct {
   void* ctx;
   int32_t rank, world;
   int (*allgather)(void* ctx, const void* send, void* recv, size_t bytes);
+  int (*allreduce_max_u64)(void* ctx, uint64_t* data, size_t count);
+  int (*broadcast)(void* ctx, void* buf, size_t bytes, int32_t root);
 } mqo_comm;
 
 /* solve_pooled (solver.hpp:80): runs the engine on `g`'s device.
@@ -347,6 +352,19 @@ typedef struct {
  * solve_mis / solve_maxcut are solve_pooled with the reference's guards. */
 int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
                      mqo_run_report* report, uint8_t* best_body);
+
+/* "Mode R": every rank runs an independent pooled
+ * solver over its chain shard [r*ceil(B/world), ...) -- chain b keeps stream
+ * derive_seed(seed, b+1) -- with no exchange while solving; then ONE
+ * allreduce-max over the packed key (score << 16 | 0xFFFF - rank) selects
+ * the best rank (ties: lowest rank) and its body is broadcast.  The report
+ * is the winner's with trajectories / iterations / resets summed and phase
+ * maxima taken over ranks; rank_scores (may be NULL) receives every rank's
+ * best score.  Cheaper than mqo_solve_pooled's per-round merge, but not
+ * equal to the single-GPU B-chain run (each rank keeps its own pool).
+ * With comm == NULL it is mqo_solve_pooled. */
+int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                       mqo_run_report* report, uint8_t* best_body, int64_t* rank_scores);
 
 /* init_state on the host for one stream (the EXACT init path), usable on a
  * host-only graph: x[n] out, *st advanced like Rng. */

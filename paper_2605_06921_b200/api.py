@@ -32,7 +32,7 @@ __all__ = [
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
     "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
-    "solve_maxcut", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
+    "solve_maxcut", "solve_replicas", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
     "InvalidArgument", "LogicError", "MqoError", "ParseError", "DimacsResult", "parse_dimacs_text",
     "read_canonical", "write_canonical", "load_graph_file", "write_graph_file",
 ]
@@ -609,12 +609,59 @@ class _RunReport(C.Structure):
 class _Comm(C.Structure):
     _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
                 ("allgather", C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
-                                          C.c_size_t))]
+                                          C.c_size_t)),
+                ("allreduce_max_u64", C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64),
+                                                  C.c_size_t)),
+                ("broadcast", C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t,
+                                          C.c_int32))]
+
+
+def _make_comm(comm) -> _Comm:
+    """Wraps a Python communicator (.rank, .world, .allgather(bytes) -> bytes,
+    optionally .allreduce_max(list[int]) -> list[int] and .broadcast(bytes,
+    root) -> bytes) as an mqo_comm; the callbacks stay alive with the struct."""
+    def _ag(ctx, send, recv, nbytes):
+        try:
+            out = comm.allgather(C.string_at(send, nbytes))
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # surfaced as an engine error
+            return 1
+
+    def _ar(ctx, data, count):
+        try:
+            vals = comm.allreduce_max([data[i] for i in range(count)])
+            for i in range(count):
+                data[i] = int(vals[i])
+            return 0
+        except Exception:
+            return 1
+
+    def _bc(ctx, buf, nbytes, root):
+        try:
+            out = comm.broadcast(C.string_at(buf, nbytes), root)
+            C.memmove(buf, out, nbytes)
+            return 0
+        except Exception:
+            return 1
+
+    c = _Comm()
+    c.ctx, c.rank, c.world = None, comm.rank, comm.world
+    c.allgather = _Comm._fields_[3][1](_ag)
+    # NULL callbacks are emulated with allgather by the engine
+    c.allreduce_max_u64 = (_Comm._fields_[4][1](_ar) if hasattr(comm, "allreduce_max")
+                           else _Comm._fields_[4][1]())
+    c.broadcast = (_Comm._fields_[5][1](_bc) if hasattr(comm, "broadcast")
+                   else _Comm._fields_[5][1]())
+    return c
 
 
 lib.mqo_solve_pooled.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), C.POINTER(_Comm),
                                  C.POINTER(_RunReport), _U8]
 lib.mqo_solve_pooled.restype = C.c_int
+lib.mqo_solve_replicas.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), C.POINTER(_Comm),
+                                   C.POINTER(_RunReport), _U8, _I64]
+lib.mqo_solve_replicas.restype = C.c_int
 lib.mqo_init_state_host.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, _D]
 lib.mqo_init_state_host.restype = C.c_int
 
@@ -686,21 +733,28 @@ def solve_pooled(g: Graph, cfg: SolverConfig, comm=None) -> RunReport:
     adapter; chains are then sharded over the ranks."""
     rep = _RunReport()
     body = np.zeros(max(g.n(), 1), np.uint8)
-    cptr = None
-    if comm is not None:
-        def _ag(ctx, send, recv, nbytes):
-            try:
-                data = C.string_at(send, nbytes)
-                out = comm.allgather(data)
-                C.memmove(recv, out, len(out))
-                return 0
-            except Exception:  # surfaced as an engine error
-                return 1
-        c = _Comm()
-        c.ctx, c.rank, c.world = None, comm.rank, comm.world
-        c.allgather = _Comm._fields_[3][1](_ag)  # kept alive by `c` for the call
-        cptr = C.byref(c)
-    check(lib.mqo_solve_pooled(g._h, C.byref(cfg.to_c()), cptr, C.byref(rep), _ptr(body, _U8)))
+    c = _make_comm(comm) if comm is not None else None  # kept alive for the call
+    check(lib.mqo_solve_pooled(g._h, C.byref(cfg.to_c()), C.byref(c) if c else None,
+                               C.byref(rep), _ptr(body, _U8)))
+    return _report(rep, body, g)
+
+
+def solve_replicas(g: Graph, cfg: SolverConfig, comm=None):
+    """Mode R (include/mqo_gpu.h mqo_solve_replicas):
+    every rank solves its chain shard independently; one allreduce-max picks
+    the best rank, whose body is broadcast.  Returns (RunReport, per-rank
+    best scores)."""
+    rep = _RunReport()
+    body = np.zeros(max(g.n(), 1), np.uint8)
+    c = _make_comm(comm) if comm is not None else None
+    world = comm.world if comm is not None else 1
+    scores = np.zeros(world, np.int64)
+    check(lib.mqo_solve_replicas(g._h, C.byref(cfg.to_c()), C.byref(c) if c else None,
+                                 C.byref(rep), _ptr(body, _U8), _ptr(scores, _I64)))
+    return _report(rep, body, g), scores
+
+
+def _report(rep, body, g) -> "RunReport":
     warns = [m for bit, m in WARNINGS.items() if rep.warnings & bit]
     return RunReport(rep.score, body[: g.n()].copy(), bool(rep.found_solution), rep.after_gradient,
                      rep.after_reset_loop, rep.after_local_search, rep.outer_loops,

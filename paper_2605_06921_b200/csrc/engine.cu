@@ -155,6 +155,29 @@ struct Comm {
     if (c->allgather(c->ctx, send, recv, bytes) != 0)
       throw std::runtime_error("mqo_comm.allgather failed");
   }
+  void allreduce_max(uint64_t* data, size_t count) const {
+    if (world() == 1) return;
+    if (c->allreduce_max_u64) {
+      if (c->allreduce_max_u64(c->ctx, data, count) != 0)
+        throw std::runtime_error("mqo_comm.allreduce_max_u64 failed");
+      return;
+    }
+    std::vector<uint64_t> all(count * world());
+    allgather(data, all.data(), count * sizeof(uint64_t));
+    for (int r = 0; r < world(); ++r)
+      for (size_t i = 0; i < count; ++i) data[i] = std::max(data[i], all[r * count + i]);
+  }
+  void broadcast(void* buf, size_t bytes, int root) const {
+    if (world() == 1) return;
+    if (c->broadcast) {
+      if (c->broadcast(c->ctx, buf, bytes, root) != 0)
+        throw std::runtime_error("mqo_comm.broadcast failed");
+      return;
+    }
+    std::vector<uint8_t> all(bytes * world());
+    allgather(buf, all.data(), bytes);
+    std::memcpy(buf, all.data() + bytes * root, bytes);
+  }
 };
 
 struct Engine {
@@ -165,6 +188,7 @@ struct Engine {
   int32_t n;
   int64_t W;
   int B_global, B_local, first_chain;
+  int chain_offset = 0;  // single-process engines: first global chain (Mode R shards)
   mqo_batch* batch = nullptr;
   TopKPool pool;
   Entry best;
@@ -432,7 +456,8 @@ struct Engine {
     if (B_local < 1) throw std::invalid_argument("solver: more ranks than chains");
     if (mqo_batch_create(g, B_local, &batch) != MQO_OK) throw CudaError(mqo_last_error());
     try {
-      if (mqo_batch_seed_streams(batch, cfg.seed, 1 + static_cast<uint64_t>(first_chain)) != MQO_OK)
+      if (mqo_batch_seed_streams(batch, cfg.seed,
+                                 1 + static_cast<uint64_t>(first_chain + chain_offset)) != MQO_OK)
         throw CudaError(mqo_last_error());
       loop();
     } catch (...) {
@@ -529,6 +554,64 @@ extern "C" int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, cons
       for (int32_t v = 0; v < g->n; ++v)
         best_body[v] = e.best.body.empty() ? 0 : (e.best.body[v >> 6] >> (63 - (v & 63))) & 1;
     }
+  });
+}
+
+extern "C" int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                                  mqo_run_report* report, uint8_t* best_body,
+                                  int64_t* rank_scores) {
+  return guard([&] {
+    if (!g || !cfg || !report) throw std::invalid_argument("mqo_solve_replicas: null argument");
+    if (g->device >= 0) MQO_CUDA(cudaSetDevice(g->device));
+    const Comm cm{comm};
+    const int world = cm.world(), rank = cm.rank();
+    validate(*cfg);
+    const int per = (cfg->pool_batch + world - 1) / world;
+    const int first = std::min(cfg->pool_batch, rank * per);
+    const int local = std::max(0, std::min(cfg->pool_batch, first + per) - first);
+    if (local < 1) throw std::invalid_argument("solver: more ranks than chains");
+    Engine e;  // an independent single-process solver over this rank's shard
+    e.g = g;
+    e.cfg = *cfg;
+    e.cfg.pool_batch = local;
+    e.comm = Comm{nullptr};
+    e.chain_offset = first;
+    e.run();
+    // the one exchange: argmax over ranks (a single tiny all-reduce)
+    const int64_t sc = e.rep.found_solution ? e.best.score : -1;
+    uint64_t key = (static_cast<uint64_t>(sc + 1) << 16) | static_cast<uint64_t>(0xFFFF - rank);
+    cm.allreduce_max(&key, 1);
+    const int winner = 0xFFFF - static_cast<int>(key & 0xFFFF);
+    // counters: the winner's report, sums / maxima over ranks
+    mqo_run_report mine = e.rep;
+    std::vector<mqo_run_report> all(world);
+    cm.allgather(&mine, all.data(), sizeof(mqo_run_report));
+    mqo_run_report r = all[winner];
+    r.outer_loops = r.trajectories = 0;
+    r.resets_accepted = r.resets_rejected = r.total_iterations = 0;
+    r.elapsed_secs = 0.0;
+    r.warnings = 0;
+    for (const auto& a : all) {
+      r.trajectories += a.trajectories;
+      r.resets_accepted += a.resets_accepted;
+      r.resets_rejected += a.resets_rejected;
+      r.total_iterations += a.total_iterations;
+      r.outer_loops = std::max(r.outer_loops, a.outer_loops);
+      r.after_gradient = std::max(r.after_gradient, a.after_gradient);
+      r.after_reset_loop = std::max(r.after_reset_loop, a.after_reset_loop);
+      r.after_local_search = std::max(r.after_local_search, a.after_local_search);
+      r.elapsed_secs = std::max(r.elapsed_secs, a.elapsed_secs);
+      r.warnings |= a.warnings;
+    }
+    r.n_warnings = __builtin_popcount(static_cast<unsigned>(r.warnings));
+    if (rank_scores)
+      for (int q = 0; q < world; ++q) rank_scores[q] = all[q].found_solution ? all[q].score : -1;
+    std::vector<uint64_t> body(e.W > 0 ? e.W : 1, 0);
+    if (rank == winner && !e.best.body.empty()) std::copy(e.best.body.begin(), e.best.body.end(), body.begin());
+    cm.broadcast(body.data(), sizeof(uint64_t) * body.size(), winner);
+    *report = r;
+    if (best_body)
+      for (int32_t v = 0; v < g->n; ++v) best_body[v] = (body[v >> 6] >> (63 - (v & 63))) & 1;
   });
 }
 

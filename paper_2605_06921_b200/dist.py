@@ -1,11 +1,13 @@
 """Multi-GPU plumbing for the solver engine: a torch.distributed adapter for
 the engine's communicator (include/mqo_gpu.h `mqo_comm`).
 
-One process per GPU; the engine shards the B chains over the ranks and, at
-every merge, all-gathers the per-chain records and the candidate bodies
-("Mode P").  The payloads are tiny (B x 32 bytes of
-records plus at most a few packed bodies), so a plain all-gather is used:
-NCCL over NVLink on GPUs, gloo on CPU (tests).
+One process per GPU; the engine shards the B chains over the ranks.
+"Mode P" (solve_pooled): at every merge it all-gathers the per-chain records
+and the candidate bodies -- tiny payloads (B x 32
+bytes of records plus at most a few packed bodies).  "Mode R"
+(solve_replicas): no exchange while solving, then one all-reduce (MAX) of
+a packed (score, rank) key and a broadcast of the winning body.  NCCL over
+NVLink on GPUs, gloo on CPU (tests).
 """
 from __future__ import annotations
 
@@ -44,6 +46,21 @@ class TorchComm:
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t, group=self.group)
         return b"".join(o.cpu().numpy().tobytes() for o in out)
+
+
+    def allreduce_max(self, values):
+        """Element-wise max over ranks of non-negative int64 keys."""
+        torch = self.torch
+        t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return [int(v) for v in t.cpu().tolist()]
+
+    def broadcast(self, data: bytes, root: int) -> bytes:
+        torch = self.torch
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(self.device)
+        self.dist.broadcast(t, src=self.dist.get_global_rank(self.group, root)
+                            if self.group is not None else root, group=self.group)
+        return t.cpu().numpy().tobytes()
 
 
 def shard(b_global: int, world: int, rank: int) -> range:

@@ -40,7 +40,10 @@ def _worker(rank, world, port, q):
     order = [int(r[0]) - 100 for r in allrec if r[0] >= 100]
     t = torch.tensor([1.5 + rank], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    q.put((rank, got, order, float(t.item()), list(mine)))
+    # Mode R exchange: argmax key all-reduce + broadcast of the winner's body
+    key = c.allreduce_max([(10 << 16) | (0xFFFF - rank), 7 * rank])
+    body = c.broadcast(bytes([rank]) * 9 if rank == 1 else bytes(9), 1)
+    q.put((rank, got, order, float(t.item()), list(mine), key, body))
     dist.destroy_process_group()
 
 
@@ -56,8 +59,9 @@ def test_gloo_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, got, order, tmax, mine in res:
-        assert got == b"\x01" * 5 + b"\x02" * 5
+    for rank, got, order, tmax, mine, key, body in res:
+        assert key == [(10 << 16) | 0xFFFF, 7]  # ties -> the lowest rank
+        assert body == b"\x01" * 9
         assert order == list(range(7))  # global chain order restored
         assert tmax == 2.5
     assert res[0][4] == [0, 1, 2, 3] and res[1][4] == [4, 5, 6]

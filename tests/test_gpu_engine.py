@@ -205,3 +205,84 @@ dist.destroy_process_group()
     assert r0 == dict(score=r.best_score, it=r.total_iterations, acc=r.resets_accepted,
                       rej=r.resets_rejected, body=r.best_body.tolist(),
                       stop=r.last_trajectory_stop)
+
+
+class _LoopbackComm:
+    """A one-process stand-in for rank `rank` of `world`: every collective
+    sees only this rank's contribution (used to obtain one rank's local
+    Mode-R result in isolation)."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+    def allgather(self, data):
+        return data * self.world
+
+    def allreduce_max(self, values):
+        return values
+
+    def broadcast(self, data, root):
+        return data
+
+
+def _replica_cfg(P):
+    return P.SolverConfig(objective=P.PerturbedBias(0.001),
+                          optimizer=P.OptimizerConfig(0.0025, 0.8), reset_fraction=0.8,
+                          reset_rounds=4, seed=3, time_budget_secs=600, max_outer_loops=1,
+                          pool_batch=7, pool_keep=2)
+
+
+def test_engine_replicas_mode(P, tmp_path):
+    """Mode R (mqo_solve_replicas): each rank's shard is an independent
+    pooled solve over its global chain streams; one allreduce-max picks the
+    best rank (ties: lowest) and its body is broadcast to every rank."""
+    g = P.generate(P.ErSpec(500, 0.02), 3)
+    cfg = _replica_cfg(P)
+    # rank 0's shard (chains 0..3) is the single-process solve with 4 chains
+    r0, s0 = P.solve_replicas(g, cfg, comm=_LoopbackComm(0, 2))
+    import dataclasses
+    ref0 = P.solve_pooled(g, dataclasses.replace(cfg, pool_batch=4))
+    assert s0[0] == ref0.best_score and (r0.best_body == ref0.best_body).all()
+    assert r0.total_iterations == 2 * ref0.total_iterations  # loopback: both "ranks" are rank 0
+    r1, s1 = P.solve_replicas(g, cfg, comm=_LoopbackComm(1, 2))
+    # no comm: Mode R is solve_pooled
+    rs, ss = P.solve_replicas(g, cfg)
+    full = P.solve_pooled(g, cfg)
+    assert ss[0] == full.best_score and (rs.best_body == full.best_body).all()
+    script = tmp_path / "replicas.py"
+    script.write_text(f"""
+import os, sys, json, datetime
+sys.path.insert(0, {ROOT!r})
+import torch.distributed as dist
+import paper_2605_06921_b200 as P
+from paper_2605_06921_b200.dist import TorchComm
+dist.init_process_group("gloo", timeout=datetime.timedelta(seconds=120))
+g = P.generate(P.ErSpec(500, 0.02), 3)
+cfg = P.SolverConfig(objective=P.PerturbedBias(0.001), optimizer=P.OptimizerConfig(0.0025, 0.8),
+                     reset_fraction=0.8, reset_rounds=4, seed=3, time_budget_secs=600,
+                     max_outer_loops=1, pool_batch=7, pool_keep=2)
+r, scores = P.solve_replicas(g, cfg, comm=TorchComm())
+out = dict(score=r.best_score, body=r.best_body.tolist(), scores=scores.tolist(),
+           it=r.total_iterations)
+open(os.environ["OUT"] + str(dist.get_rank()), "w").write(json.dumps(out))
+dist.destroy_process_group()
+""")
+    env = dict(os.environ, OUT=str(tmp_path / "q"), MQO_PERSISTENT_CELLS="0")
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    proc = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           "--nproc-per-node=2", "--master-addr=127.0.0.1",
+                           f"--master-port={port}", str(script)], env=env, timeout=400,
+                          capture_output=True, text=True)
+    assert proc.returncode == 0, proc.stderr[-4000:]
+    import json
+    q0 = json.loads((tmp_path / "q0").read_text())
+    q1 = json.loads((tmp_path / "q1").read_text())
+    assert q0 == q1
+    assert q0["scores"] == [int(s0[0]), int(s1[0])]
+    win = r0 if s0[0] >= s1[0] else r1
+    assert q0["score"] == max(s0[0], s1[0]) and q0["body"] == win.best_body.tolist()
+    assert q0["it"] == (r0.total_iterations + r1.total_iterations) // 2
