@@ -99,6 +99,24 @@ void launch_project(mqo_batch* b, double* x, int32_t problem) {
 }
 }  // namespace mqo_b200
 
+namespace mqo_b200 {
+// The per-round work (reset scratch, local-search workspaces) uses
+// cudaMallocAsync; with the default pool's release threshold of 0 every
+// stream synchronisation hands the memory back and the next round maps it
+// again.  Keep it (MQO_POOL_RELEASE=1 restores the driver default).
+void keep_pool_memory(int device) {
+  static const bool release = [] {
+    const char* e = std::getenv("MQO_POOL_RELEASE");
+    return e && *e == '1';
+  }();
+  if (release) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+}  // namespace mqo_b200
+
 extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
   return guard([&] {
     if (!g || !out) throw std::invalid_argument("mqo_batch_create: null argument");
@@ -112,6 +130,7 @@ extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
     b->Bp = b->Q * b->cpl;
     try {
       MQO_CUDA(cudaSetDevice(g->device));
+      keep_pool_memory(g->device);
       MQO_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
       const size_t state = sizeof(double) * std::max<int64_t>(1, int64_t(g->n) * b->Bp);
       MQO_CUDA(cudaMalloc(&b->d_x[0], state));

@@ -189,6 +189,11 @@ struct Engine {
   int64_t W;
   int B_global, B_local, first_chain;
   int chain_offset = 0;  // single-process engines: first global chain (Mode R shards)
+  uint64_t* stage = nullptr;  // pinned staging for local-search bodies
+  size_t stage_words = 0;
+  ~Engine() {
+    if (stage) cudaFreeHost(stage);
+  }
   mqo_batch* batch = nullptr;
   TopKPool pool;
   Entry best;
@@ -378,23 +383,31 @@ struct Engine {
     uint64_t* d_packed = nullptr;
     int64_t* d_out = nullptr;
     cudaStream_t st = batch->stream;
-    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * W * count, st));
-    MQO_CUDA(cudaMallocAsync(&d_out, sizeof(int64_t) * count, st));
-    for (int i = 0; i < count; ++i)
-      MQO_CUDA(cudaMemcpyAsync(d_packed + static_cast<int64_t>(i) * W, members[i].body.data(),
-                               sizeof(uint64_t) * W, cudaMemcpyHostToDevice, st));
+    MQO_TRACE("polish: %d bodies", count);
+    // one pinned staging buffer: [count][W] bodies + [count] outputs
+    const size_t words = static_cast<size_t>(count) * W;
+    if (stage_words < words + count) {
+      if (stage) cudaFreeHost(stage);
+      stage = nullptr;
+      MQO_CUDA(cudaMallocHost(&stage, sizeof(uint64_t) * (words + count)));
+      stage_words = words + count;
+    }
+    for (int i = 0; i < count; ++i) std::copy(members[i].body.begin(), members[i].body.end(), stage + i * W);
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * (words + count), st));
+    d_out = reinterpret_cast<int64_t*>(d_packed + words);
+    MQO_CUDA(cudaMemcpyAsync(d_packed, stage, sizeof(uint64_t) * words, cudaMemcpyHostToDevice, st));
     const int op = problem == MQO_PROBLEM_MIS ? MQO_LS_ONE_TWO_SWAP : MQO_LS_ONE_TWO_FLIP;
     local_search_device(batch, op, count, d_packed, d_out, st);
-    std::vector<int64_t> out(count);
-    for (int i = 0; i < count; ++i)
-      MQO_CUDA(cudaMemcpyAsync(members[i].body.data(), d_packed + static_cast<int64_t>(i) * W,
-                               sizeof(uint64_t) * W, cudaMemcpyDeviceToHost, st));
-    MQO_CUDA(cudaMemcpyAsync(out.data(), d_out, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    MQO_CUDA(cudaMemcpyAsync(stage, d_packed, sizeof(uint64_t) * (words + count),
+                             cudaMemcpyDeviceToHost, st));
     cudaFreeAsync(d_packed, st);
-    cudaFreeAsync(d_out, st);
     MQO_CUDA(cudaStreamSynchronize(st));
-    for (int i = 0; i < count; ++i)
+    MQO_TRACE("polish: %d bodies done", count);
+    const int64_t* out = reinterpret_cast<const int64_t*>(stage + words);
+    for (int i = 0; i < count; ++i) {
+      std::copy(stage + i * W, stage + (i + 1) * W, members[i].body.begin());
       members[i].score = problem == MQO_PROBLEM_MIS ? out[i] : members[i].score + out[i];
+    }
   }
 
   // Phase-3 polish with the pool members dealt round-robin over the ranks,

@@ -734,6 +734,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     MQO_CUDA(cudaMemcpyAsync(flags.data(), w.small, sizeof(int32_t) * count,
                              cudaMemcpyDeviceToHost, st));
     MQO_CUDA(cudaStreamSynchronize(st));
+    MQO_TRACE("one_two_swap: tightness checked");
     for (int i = 0; i < count; ++i) {
       if (flags[i] & 1) {
         cudaFreeAsync(w.bytes, st);
@@ -753,10 +754,25 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
     MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
     MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (trace_on()) {
+      cudaEventCreate(&ev[0]);
+      cudaEventCreate(&ev[1]);
+      cudaEventRecord(ev[0], st);
+    }
     k_mis_swap<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
                                                  w.dflag, w.dlist, w.freed, w.small,
                                                  g->max_degree, d_out);
     MQO_CUDA(cudaGetLastError());
+    if (trace_on()) {
+      cudaEventRecord(ev[1], st);
+      cudaEventSynchronize(ev[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      MQO_TRACE("k_mis_swap: %.3f ms (%d bodies)", ms, count);
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
+    }
     MQO_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t) * count, st));
   }
   k_pack_bytes<<<ls_grid(int64_t(count) * W), 256, 0, st>>>(w.bytes, W, n, count, d_packed,
@@ -768,6 +784,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (w.dflag) cudaFreeAsync(w.dflag, st);
   if (w.dlist) cudaFreeAsync(w.dlist, st);
   if (w.freed) cudaFreeAsync(w.freed, st);
+  MQO_TRACE("local search op %d queued", op);
 }
 
 }  // namespace mqo_b200
