@@ -415,8 +415,14 @@ class ChainBatch:
     def project(self, problem: int) -> None:
         check(lib.mqo_project(self._h, problem))
 
-    def gradient(self, spec) -> np.ndarray:
-        out = np.empty((self.chains, self.g.n()), np.float64)
+    def gradient(self, spec, out: np.ndarray | None = None) -> np.ndarray:
+        """[B][n] gradients; `out` (C-contiguous float64, e.g. a view of
+        pinned memory) avoids the pageable staging copy."""
+        if out is None:
+            out = np.empty((self.chains, self.g.n()), np.float64)
+        elif out.shape != (self.chains, self.g.n()) or out.dtype != np.float64 \
+                or not out.flags.c_contiguous:
+            raise InvalidArgument(1, "gradient: out must be C-contiguous float64 [B][n]")
         o = _obj(spec)
         check(lib.mqo_gradient(self._h, C.byref(o), _ptr(out, _D)))
         return out

@@ -19,6 +19,7 @@
 // only the 2-hop neighbourhood a swap can change ("dirty" list), which
 // finds exactly the vertex the restarted scan would find.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -27,6 +28,12 @@ using namespace mqo_b200;
 namespace {
 
 constexpr int kLsWarps = 4;  // solutions per CTA (one warp each)
+constexpr int64_t kSwapSmemMax = 227 * 1024;  // opt-in dynamic SMEM per CTA
+// MQO_LS_SMEM=0 disables the SMEM-resident local-search variants (A/B runs)
+const bool g_swap_smem = [] {
+  const char* e = std::getenv("MQO_LS_SMEM");
+  return !(e && *e == '0');
+}();
 
 __device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 1; }
 
@@ -445,20 +452,84 @@ __device__ void warp_apply_swap(const int64_t* off, const int32_t* nbr, const in
   warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, w, frontier, lane);
 }
 
-// one_two_swap (localsearch.cpp:88-137) on one warp per solution.
-__global__ void k_mis_swap(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
-                           int32_t count, uint8_t* sel_all, int32_t* tight_all, uint8_t* dflag_all,
-                           int32_t* dlist_all, int32_t* freed_all, int32_t* dcount_all,
-                           int32_t max_degree, int64_t* swaps_out) {
+// Bytes of the SMEM-resident variant of k_mis_swap: the CSR and one body's
+// state (one warp per CTA); 16-byte aligned sections.
+__host__ __device__ inline int64_t swap_smem_bytes(int32_t n, int64_t nnz, int32_t max_degree) {
+  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+  return al(8 * (int64_t(n) + 1)) + al(4 * nnz) + al(4 * int64_t(n)) + al(4 * int64_t(n)) +
+         al(4 * (int64_t(max_degree) + 1)) + al(int64_t(n)) + al(int64_t(n) + 4) + 16;
+}
+
+__device__ __forceinline__ void cta_copy(void* dst, const void* src, int64_t bytes) {
+  // bytes and both pointers 4-byte aligned; 16-byte moves where both allow
+  const int64_t head = (reinterpret_cast<uintptr_t>(src) & 15) == 0 ? bytes / 16 : 0;
+  const int4* s16 = static_cast<const int4*>(src);
+  int4* d16 = static_cast<int4*>(dst);
+  for (int64_t i = threadIdx.x; i < head; i += blockDim.x) d16[i] = __ldg(s16 + i);
+  const int32_t* s4 = static_cast<const int32_t*>(src);
+  int32_t* d4 = static_cast<int32_t*>(dst);
+  for (int64_t i = head * 4 + threadIdx.x; i < bytes / 4; i += blockDim.x) d4[i] = s4[i];
+}
+
+// one_two_swap (localsearch.cpp:88-137) on one warp per solution.  With
+// `smem` (graphs whose CSR + one body's state fit shared memory; one warp
+// per CTA) the CSR, selection, tightness and dirty list are staged in SMEM
+// first: the scan is a chain of dependent loads, ~30-cycle SMEM latency
+// instead of ~300+ for L2.  Generic pointers serve both placements.
+__global__ void k_mis_swap(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
+                           int32_t n, int32_t count, uint8_t* sel_all, int32_t* tight_all,
+                           uint8_t* dflag_all, int32_t* dlist_all, int32_t* freed_all,
+                           int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out,
+                           int32_t smem) {
+  extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  const int s = smem ? blockIdx.x : blockIdx.x * kLsWarps + (threadIdx.x >> 5);
   if (s >= count) return;
-  uint8_t* sel = sel_all + static_cast<int64_t>(s) * n;
+  uint8_t* sel_g = sel_all + static_cast<int64_t>(s) * n;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  uint8_t* sel = sel_g;
   int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
   uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
   int32_t* dlist = dlist_all + static_cast<int64_t>(s) * n;
   int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
   int32_t* dcount = dcount_all + s;
+  if (smem) {
+    auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+    const int64_t nnz = off_g[n];
+    unsigned char* p = sm;
+    int64_t* o = reinterpret_cast<int64_t*>(p);
+    p += al(8 * (int64_t(n) + 1));
+    int32_t* nb = reinterpret_cast<int32_t*>(p);
+    p += al(4 * nnz);
+    int32_t* ti = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* dl = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* fr = reinterpret_cast<int32_t*>(p);
+    p += al(4 * (int64_t(max_degree) + 1));
+    uint8_t* se = p;
+    p += al(n);
+    uint8_t* df = p;
+    p += al(int64_t(n) + 4);
+    int32_t* dc = reinterpret_cast<int32_t*>(p);
+    cta_copy(o, off_g, 8 * (int64_t(n) + 1));
+    cta_copy(nb, nbr_g, 4 * nnz);
+    cta_copy(ti, tight, 4 * int64_t(n));
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) se[i] = sel_g[i];
+    for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) df[i] = 0;
+    if (threadIdx.x == 0) *dc = 0;
+    __syncthreads();
+    if (threadIdx.x >= 32) return;  // the other warps only helped stage
+    off = o;
+    nbr = nb;
+    sel = se;
+    tight = ti;
+    dflag = df;
+    dlist = dl;
+    freed = fr;
+    dcount = dc;
+  }
   int32_t frontier = 0;
   int64_t swaps = 0;
   for (;;) {
@@ -531,6 +602,10 @@ __global__ void k_mis_swap(const int64_t* __restrict__ off, const int32_t* __res
     ++swaps;
   }
   if (lane == 0) swaps_out[s] = swaps;
+  if (smem) {
+    __syncwarp();
+    for (int64_t i = lane; i < n; i += 32) sel_g[i] = sel[i];
+  }
 }
 
 // packed [count][W] <-> bytes [count][n]
@@ -760,9 +835,23 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
       cudaEventCreate(&ev[1]);
       cudaEventRecord(ev[0], st);
     }
-    k_mis_swap<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
-                                                 w.dflag, w.dlist, w.freed, w.small,
-                                                 g->max_degree, d_out);
+    const int64_t sbytes = swap_smem_bytes(n, 2 * g->m, g->max_degree);
+    const bool smem = sbytes <= kSwapSmemMax && g_swap_smem;
+    if (smem) {
+      static bool attr = false;
+      if (!attr) {
+        MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kSwapSmemMax)));
+        attr = true;
+      }
+      k_mis_swap<<<count, 256, static_cast<size_t>(sbytes), st>>>(
+          g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.freed, w.small,
+          g->max_degree, d_out, 1);
+    } else {
+      k_mis_swap<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
+                                                   w.dflag, w.dlist, w.freed, w.small,
+                                                   g->max_degree, d_out, 0);
+    }
     MQO_CUDA(cudaGetLastError());
     if (trace_on()) {
       cudaEventRecord(ev[1], st);
