@@ -75,6 +75,7 @@ struct PassArgs {
   int32_t is_mis;
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
   int32_t q0, Qg;            // this launch's chain group: quads [q0, q0 + Qg) of Q
+  int32_t gblocks;           // > 0: groups fused in one launch, gblocks CTAs each
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -285,8 +286,15 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
                                           const uint8_t* qmask, bool write, Acc<CPL>& acc,
                                           int32_t& my_q) {
   const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // Fused chain groups: CTAs [g*gblocks, (g+1)*gblocks) sweep group g.  The
+  // block scheduler dispatches CTAs in index order, so the groups still run
+  // one after another (one L2-sized X slice live at a time, two at the
+  // seams) without a launch boundary -- and its tail -- between them.
+  const int vblock = a.gblocks > 0 ? blockIdx.x % a.gblocks : blockIdx.x;
+  const int vgrid = a.gblocks > 0 ? a.gblocks : gridDim.x;
+  const int32_t qbase = a.q0 + (a.gblocks > 0 ? (blockIdx.x / a.gblocks) * a.Qg : 0);
+  const int gwarp = (vblock * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (vgrid * blockDim.x) >> 5;
   int32_t q, r0, rstep;
   if (a.Qg >= 32) {
     const int wpr = a.Qg >> 5;
@@ -299,7 +307,7 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
     r0 = gwarp * rpw + lane / a.Qg;
     rstep = nwarps * rpw;
   }
-  q += a.q0;  // global quad
+  q += qbase;  // global quad
   my_q = q;
   const int32_t col = q * CPL;
   unsigned amask;
@@ -752,6 +760,25 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   return a;
 }
 
+// One pass over every chain group: a single launch of Q/Qg x `blocks` CTAs
+// (MQO_FUSE_GROUPS=0: one launch per group, the earlier form).
+bool g_fuse_groups = [] {
+  const char* e = std::getenv("MQO_FUSE_GROUPS");
+  return !(e && *e == '0');
+}();
+template <class F>
+void launch_groups(const mqo_batch* b, PassArgs& a, int blocks, size_t smem, F fn) {
+  if (g_fuse_groups && a.Qg < b->Q) {
+    a.q0 = 0;
+    a.gblocks = blocks;
+    fn<<<blocks * (b->Q / a.Qg), kThreads, smem, b->stream>>>(a);
+    a.gblocks = 0;
+    return;
+  }
+  for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, smem, b->stream>>>(a);
+  a.q0 = 0;
+}
+
 // Problems up to this many (vertex, chain) cells run the persistent kernel.
 int64_t g_persistent_cells = [] {
   const char* e = std::getenv("MQO_PERSISTENT_CELLS");
@@ -780,7 +807,7 @@ void launch_step(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& op
   a.Qg = group_quads(b);
   a.hot_rows = hot_rows(b, a.Qg);
   const int blocks = pass_blocks(b, a.Qg);
-  for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, 0, b->stream>>>(a);
+  launch_groups(b, a, blocks, 0, fn);
   MQO_CUDA(cudaGetLastError());
   b->cur ^= 1;
 }
@@ -859,8 +886,7 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
       for (int32_t q = p; q < chunk_end; ++q) {
         a.p_begin = q;
         a.p_end = q + 1;
-        for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, smem, b->stream>>>(a);
-        a.q0 = 0;
+        launch_groups(b, a, blocks, smem, fn);
         k_traj_ctl<<<1, 256, 0, b->stream>>>(a);
       }
       MQO_CUDA(cudaGetLastError());
@@ -912,6 +938,8 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_hot_frac = value;
     else if (k == "persistent_cells")
       g_persistent_cells = static_cast<int64_t>(value);
+    else if (k == "fuse_groups")
+      g_fuse_groups = value != 0.0;
     else if (k == "cta_traj")
       g_cta_disabled = value == 0.0;
     else if (k == "cta_cluster")

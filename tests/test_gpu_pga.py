@@ -101,11 +101,12 @@ def test_batched_steps_vs_oracle(O, P, B, kind, param):
         assert same(gx[c], x) and same(gv[c], v), c
 
 
+@pytest.mark.parametrize("fuse", [1, 0])
 @pytest.mark.parametrize("gq", [1, 2, 8])
 @pytest.mark.parametrize("B", [33, 256])
-def test_chain_tiled_steps_vs_oracle(O, P, B, gq):
-    """Chain tiling (one graph sweep per group of gq quads) keeps every
-    iterate bit-identical."""
+def test_chain_tiled_steps_vs_oracle(O, P, B, gq, fuse):
+    """Chain tiling (one graph sweep per group of gq quads; all groups in one
+    launch or one launch per group) keeps every iterate bit-identical."""
     from paper_2605_06921_b200 import _lib
     og = O.generate_er(300, 0.03, 6)
     pg = P.generate(P.ErSpec(300, 0.03), 6)
@@ -117,11 +118,13 @@ def test_chain_tiled_steps_vs_oracle(O, P, B, gq):
         b.set_x(X)
         cfg = P.OptimizerConfig(alpha=0.05, beta=0.7)
         _lib.check(_lib.lib.mqo_tune(b"group_quads", gq))
+        _lib.check(_lib.lib.mqo_tune(b"fuse_groups", fuse))
         try:
             for _ in range(4):
                 b.step(Spec(kind, param), cfg)
         finally:
             _lib.check(_lib.lib.mqo_tune(b"group_quads", 0))
+            _lib.check(_lib.lib.mqo_tune(b"fuse_groups", 1))
         gx = b.get_x()
         for c in range(0, B, 7):
             x, v = X[c].copy(), np.zeros(og.n)
