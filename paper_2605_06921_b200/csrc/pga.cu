@@ -560,9 +560,13 @@ double g_hot_frac = [] {
   const char* e = std::getenv("MQO_HOT_FRAC");
   return e ? std::atof(e) : 0.5;
 }();
+// CTAs per SM of the per-pass grids; 0 = automatic: 8 for a sweep over all
+// chains, 4 per group for chain-tiled sweeps (profiles/r08_tune_grid.txt:
+// ER(1e5) MIS x256 tiled: 0.2673 -> 0.2568 ms per trajectory pass; BA(1e6)
+// x128 untiled: 8 is best).
 int g_grid_per_sm = [] {
   const char* e = std::getenv("MQO_GRID_PER_SM");
-  return e ? std::atoi(e) : 8;
+  return e ? std::atoi(e) : 0;
 }();
 int k1_variant() { return g_k1_variant; }
 
@@ -663,7 +667,8 @@ int align_blocks(const mqo_batch* b, int64_t blocks) { return align_blocks(b, bl
 // over rows), never more than the work needs.
 int pass_blocks(const mqo_batch* b, int Qg) {
   const int64_t need = (warp_tasks(b, Qg) + kWarps - 1) / kWarps;
-  const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * g_grid_per_sm;
+  const int per_sm = g_grid_per_sm > 0 ? g_grid_per_sm : (Qg < b->Q ? 4 : 8);
+  const int64_t cap = static_cast<int64_t>(sm_count(b->g->device)) * per_sm;
   return align_blocks(b, std::max<int64_t>(1, std::min(need, cap)), Qg);
 }
 int pass_blocks(const mqo_batch* b) { return pass_blocks(b, b->Q); }
@@ -947,7 +952,7 @@ extern "C" int mqo_tune(const char* key, double value) {
     else if (k == "group_quads")
       g_group_quads = static_cast<int>(value);
     else if (k == "grid_per_sm")
-      g_grid_per_sm = std::max(1, static_cast<int>(value));
+      g_grid_per_sm = std::max(0, static_cast<int>(value));
     else
       throw std::invalid_argument("mqo_tune: unknown key");
   });
