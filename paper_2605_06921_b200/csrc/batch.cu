@@ -143,6 +143,7 @@ extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
       MQO_CUDA(cudaMalloc(&b->d_viol, sizeof(uint32_t) * 3 * b->Bp));
       MQO_CUDA(cudaMalloc(&b->d_chg, sizeof(unsigned long long) * 3 * b->Bp));
       MQO_CUDA(cudaMalloc(&b->d_flag, sizeof(int32_t) * 4));
+      MQO_CUDA(cudaMalloc(&b->d_qmask, std::max(1, b->Q)));
       MQO_CUDA(cudaHostAlloc(&b->h_flag, sizeof(int32_t) * 4, cudaHostAllocMapped));
       b->h_flag[2] = 0;
       MQO_CUDA(cudaStreamSynchronize(b->stream));
@@ -167,6 +168,7 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
     cudaFree(b->d_viol);
     cudaFree(b->d_chg);
     cudaFree(b->d_flag);
+    cudaFree(b->d_qmask);
     free_solver_buffers(b);
     if (b->h_flag) cudaFreeHost(b->h_flag);
     if (b->stream) cudaStreamDestroy(b->stream);

@@ -164,6 +164,7 @@ struct mqo_batch {
   uint32_t* d_viol = nullptr;           // [3][Bp] MIS checker accumulators
   unsigned long long* d_chg = nullptr;  // [3][Bp] max |dx| accumulators (bits)
   int32_t* d_flag = nullptr;            // misc device flags [4]
+  uint8_t* d_qmask = nullptr;           // [Q] active-chain mask per quad
   int32_t* h_flag = nullptr;            // pinned mirror [4]
   int coop_blocks = 0;                  // resident CTAs for the persistent kernel
   // solver state (solver.cu)

@@ -76,6 +76,8 @@ struct PassArgs {
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
   int32_t q0, Qg;            // this launch's chain group: quads [q0, q0 + Qg) of Q
   int32_t gblocks;           // > 0: groups fused in one launch, gblocks CTAs each
+  uint8_t* qmask;            // [Q] active-chain mask per quad (per-launch path)
+  int32_t cpl;
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -456,25 +458,18 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   uint8_t* s_qmask = reinterpret_cast<uint8_t*>(s_viol + a.Bp);
   const int32_t p = a.p_begin;
   const int slot = p % 3;
-  for (int q = threadIdx.x; q < a.Q; q += blockDim.x) {
-    unsigned m = 0;
-    for (int c = 0; c < CPL; ++c) {
-      const int b = q * CPL + c;
-      m |= (b < a.B && a.ctl[b].active) ? (1u << c) : 0u;
-    }
-    s_qmask[q] = static_cast<uint8_t>(m);
-  }
-  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
-    s_viol[b] = 0u;
-    s_chg[b] = 0ull;
-  }
+  // the active-quad masks come from k_traj_ctl / k_qmask (one global read
+  // per thread instead of a per-CTA rebuild from ChainCtl)
+  (void)s_qmask;
+  for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) s_viol[b] = 0u;
+  (void)s_chg;
   __syncthreads();
   const double* X = a.x[(a.base + p - 1) & 1];
   double* Xo = a.x[(a.base + p) & 1];
   const bool write = !MIS || p <= a.T;
   Acc<CPL> acc;
   int32_t q = 0;
-  pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
+  pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, a.qmask, write, acc, q);
   fold_to_smem<CPL>(acc, q, s_viol);
   __syncthreads();
   for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
@@ -482,6 +477,24 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
     uint32_t* gv = a.viol + slot * a.Bp + b;
     if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
   }
+}
+
+// Active-chain mask per quad from ChainCtl (one CTA; after a __syncthreads
+// that orders the ctl writes of the same CTA).
+__device__ __forceinline__ void qmask_from_ctl(const ChainCtl* ctl, int32_t B, int32_t Q,
+                                               int32_t cpl, uint8_t* qmask) {
+  for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+    unsigned m = 0;
+    for (int c = 0; c < cpl; ++c) {
+      const int b = q * cpl + c;
+      m |= (b < B && ctl[b].active) ? (1u << c) : 0u;
+    }
+    qmask[q] = static_cast<uint8_t>(m);
+  }
+}
+
+__global__ void k_qmask(const ChainCtl* ctl, int32_t B, int32_t Q, int32_t cpl, uint8_t* qmask) {
+  qmask_from_ctl(ctl, B, Q, cpl, qmask);
 }
 
 // K2 for the per-launch path: one CTA takes pass p's stop decisions
@@ -520,6 +533,7 @@ __global__ void k_traj_ctl(PassArgs a) {
   if (local) atomicAdd(&s_count, local);
   __syncthreads();
   if (threadIdx.x == 0) a.flag[0] = s_count;
+  qmask_from_ctl(a.ctl, a.B, a.Q, a.cpl, a.qmask);
 }
 
 // Chains still running at the end: IterCap at iterate T (pga.cpp:109-110).
@@ -762,6 +776,8 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   a.base = b->cur;
   a.is_mis = obj.kind == MQO_MIS_QUBO;
   a.hot_rows = hot_rows(b);
+  a.cpl = b->cpl;
+  a.qmask = b->d_qmask;
   return a;
 }
 
@@ -855,6 +871,8 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
     a.hot_rows = hot_rows(b, a.Qg);
   }
   int blocks = pass_blocks(b, a.Qg);
+  if (!persistent)
+    k_qmask<<<1, 256, 0, b->stream>>>(b->d_ctl, b->B, b->Q, b->cpl, b->d_qmask);
   if (persistent) {
     int per_sm = 0;
     MQO_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
