@@ -225,6 +225,15 @@ def rescore(g, problem: str, bits: np.ndarray) -> int:
     return int(((bits[src] != bits[nbr]) & (src < nbr)).sum())
 
 
+def solution_from_record(record: dict, n: int) -> tuple:
+    """solution_from_record (report_json.cpp:139-154): (kind, bits uint8[n],
+    score); fields other than the ones it reads are ignored."""
+    j = record["solution"]
+    kind = j["kind"]
+    bits = decode_bits(j["members"] if kind == "independent_set" else j["side"], n)
+    return kind, bits, int(j["score"])
+
+
 CSV_HEADER = ("problem,param,value,seed,n,m,best,after_gradient,after_reset_loop,"
               "after_local_search,resets_accepted,resets_rejected,outer_loops,"
               "iterations,elapsed_secs")
