@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -147,6 +148,8 @@ struct mqo_graph {
   std::vector<int32_t> h_cta_rows, h_cta_base;  // per-slice rows / ELL base (host copy)
   std::vector<int64_t> h_off;
   std::vector<int32_t> h_nbr;
+  std::mutex lazy_mu;  // guards the lazily built fields (d_cta, d_hmax): a graph may be
+                       // shared by solves running on several host threads
 };
 
 struct mqo_batch {

@@ -796,10 +796,16 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (op <= 2) {
     k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
     MQO_CUDA(cudaGetLastError());
-    if (!g->d_hmax) {  // once per graph
-      MQO_CUDA(cudaMalloc(&g->d_hmax, sizeof(int32_t) * std::max(n, 1)));
-      k_hmax<<<ls_grid(n), 256, 0, st>>>(g->d_off, g->d_nbr, n, g->d_hmax);
-      MQO_CUDA(cudaGetLastError());
+    {
+      std::lock_guard<std::mutex> lock(g->lazy_mu);
+      if (!g->d_hmax) {  // once per graph, complete before any stream uses it
+        int32_t* h = nullptr;
+        MQO_CUDA(cudaMalloc(&h, sizeof(int32_t) * std::max(n, 1)));
+        k_hmax<<<ls_grid(n), 256, 0, st>>>(g->d_off, g->d_nbr, n, h);
+        MQO_CUDA(cudaGetLastError());
+        MQO_CUDA(cudaStreamSynchronize(st));
+        g->d_hmax = h;
+      }
     }
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
   } else {
@@ -838,12 +844,8 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     const int64_t sbytes = swap_smem_bytes(n, 2 * g->m, g->max_degree);
     const bool smem = sbytes <= kSwapSmemMax && g_swap_smem;
     if (smem) {
-      static bool attr = false;
-      if (!attr) {
-        MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kSwapSmemMax)));
-        attr = true;
-      }
+      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSwapSmemMax)));
       k_mis_swap<<<count, 256, static_cast<size_t>(sbytes), st>>>(
           g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.freed, w.small,
           g->max_degree, d_out, 1);

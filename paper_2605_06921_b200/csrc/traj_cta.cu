@@ -422,6 +422,7 @@ int g_cta_cluster = 0;        // mqo_tune("cta_cluster", C): 0 = automatic
 
 // Builds (once per graph) the slot layout described at CtaArgs.
 void ensure_cta_layout(mqo_graph* g) {
+  std::lock_guard<std::mutex> lock(g->lazy_mu);
   if (g->d_cta) return;
   const int32_t n = g->n;
   const int32_t S = (n + 31) / 32;
@@ -554,8 +555,11 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   const size_t smem = cta_smem_for(g, C, a.max_slices, a.max_ell, smem_lay);
   if (smem > kCtaSmemMax) throw std::logic_error("cta trajectories: state exceeds SMEM");
   CtaFn fn = cta_fn(obj.kind, smem_lay, C > 1);
+  // the cap, not this launch's size: the attribute is per function, and
+  // solves on other host threads launch the same kernel with other sizes
   MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kCtaSmemMax)));
   const int threads = cta_threads(C, a.max_slices);
   if (C == 1) {
     fn<<<b->B, threads, smem, b->stream>>>(a);

@@ -286,3 +286,27 @@ dist.destroy_process_group()
     win = r0 if s0[0] >= s1[0] else r1
     assert q0["score"] == max(s0[0], s1[0]) and q0["body"] == win.best_body.tolist()
     assert q0["it"] == (r0.total_iterations + r1.total_iterations) // 2
+
+
+def test_concurrent_solves_on_host_threads(P):
+    """Solves on several host threads (shared graphs, different graphs,
+    SMEM-path kernels with different shared-memory sizes, local search)
+    give exactly the serial results."""
+    import concurrent.futures
+    g1 = P.generate(P.ErSpec(600, 0.02), 5)
+    g2 = P.generate(P.ErSpec(100, 0.5), 6)
+    jobs = []
+    for s in range(3):
+        jobs.append((g1, P.SolverConfig(objective=P.MisQubo(2.0), optimizer=P.OptimizerConfig(0.8, 0.3),
+                                        reset_fraction=0.6, reset_rounds=5, seed=10 + s,
+                                        time_budget_secs=600, max_outer_loops=1)))
+        jobs.append((g2, P.SolverConfig(objective=P.PerturbedBias(0.001),
+                                        optimizer=P.OptimizerConfig(0.0025, 0.8), reset_fraction=0.8,
+                                        reset_rounds=5, seed=20 + s, time_budget_secs=600,
+                                        max_outer_loops=1)))
+    serial = [P.solve_pooled(g, c) for g, c in jobs]
+    with concurrent.futures.ThreadPoolExecutor(len(jobs)) as ex:
+        conc = list(ex.map(lambda j: P.solve_pooled(*j), jobs))
+    for a, b in zip(serial, conc):
+        assert (a.best_score, a.total_iterations) == (b.best_score, b.total_iterations)
+        assert (a.best_body == b.best_body).all()
