@@ -173,6 +173,127 @@ __global__ void k_flip_apply(int32_t n, int32_t count, uint8_t* side_all,
   }
 }
 
+// ---- one_flip_pass in one CTA per body (small graphs) -------------------
+// The round-parallel pass above, with side / pass-start gains / decision
+// bytes of one body in shared memory (6n bytes), every round separated by a
+// CTA barrier instead of a kernel launch and a host round trip, and the
+// passes repeated inside the kernel until one flips nothing
+// (localsearch.cpp:139-157).  Leaves side and the gain table of the final
+// state in global memory (one_two_flip's 2-flip sweep reads it).
+constexpr int kFlipCtaThreads = 1024;
+constexpr int64_t kFlipCtaSmemMax = 226 * 1024;  // + static SMEM stays under the 227 KB cap
+__host__ __device__ inline int64_t flip_cta_smem(int32_t n) { return (6 * int64_t(n) + 15) / 16 * 16; }
+__host__ __device__ inline int64_t flip_cta_smem_csr(int32_t n, int64_t nnz) {
+  return flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
+}
+
+// `csr`: the CSR is staged in shared memory too (it fits next to the body
+// state); every row walk is then ~30-cycle SMEM loads instead of L2 trips.
+__global__ void __launch_bounds__(kFlipCtaThreads, 1)
+    k_one_flip_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
+                   uint8_t* side_all, int32_t* delta_all, const int32_t* __restrict__ live,
+                   int64_t* __restrict__ gains, int32_t csr) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  int32_t* d0 = reinterpret_cast<int32_t*>(sm);
+  uint8_t* sd = sm + 4 * int64_t(n);
+  volatile uint8_t* st = sd + n;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  if (csr && live[blockIdx.x]) {
+    int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
+    int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+    const int64_t nnz = off_g[n];
+    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
+    for (int64_t i = threadIdx.x; i < nnz; i += blockDim.x) nb[i] = nbr_g[i];
+    off = o;
+    nbr = nb;
+  }
+  __shared__ unsigned long long s_gain;
+  __shared__ int s_flips;
+  const int s = blockIdx.x;
+  uint8_t* side = side_all + int64_t(s) * n;
+  int32_t* delta = delta_all + int64_t(s) * n;
+  if (!live[s]) {
+    if (threadIdx.x == 0) gains[s] = 0;
+    return;
+  }
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) sd[v] = side[v];
+  __syncthreads();
+  long long total = 0;
+  for (;;) {
+    // build_gain_table (localsearch.cpp:17-26) of the pass-start sides
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+      const uint8_t sv = sd[v];
+      int32_t same = 0;
+      for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) same += sd[nbr[e]] == sv ? 1 : -1;
+      d0[v] = same;
+      st[v] = 0;
+    }
+    if (threadIdx.x == 0) {
+      s_gain = 0ull;
+      s_flips = 0;
+    }
+    __syncthreads();
+    // decision rounds (k_flip_round)
+    for (;;) {
+      int und = 0;
+      for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+        if (st[v]) continue;
+        const uint8_t sv = sd[v];
+        int32_t base = d0[v], lo = 0, hi = 0;
+        for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
+          const int32_t u = nbr[e];
+          if (u >= v) break;
+          const int32_t c = sd[u] == sv ? -2 : 2;
+          const uint8_t su = st[u];
+          if (su == 2)
+            base += c;
+          else if (su == 0)
+            (c < 0 ? lo : hi) += c;
+        }
+        if (base + lo > 0)
+          st[v] = 2;
+        else if (base + hi <= 0)
+          st[v] = 1;
+        else
+          und = 1;
+      }
+      if (!__syncthreads_or(und)) break;
+    }
+    // the pass's gain (k_flip_commit), then apply its flips
+    long long g = 0;
+    int flips = 0;
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+      if (st[v] != 2) continue;
+      ++flips;
+      const uint8_t sv = sd[v];
+      int32_t at = d0[v];
+      for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
+        const int32_t u = nbr[e];
+        if (u >= v) break;
+        if (st[u] == 2) at += sd[u] == sv ? -2 : 2;
+      }
+      g += at;
+    }
+    if (g) atomicAdd(&s_gain, static_cast<unsigned long long>(g));
+    if (flips) atomicAdd(&s_flips, flips);
+    __syncthreads();
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+      if (st[v] == 2) sd[v] ^= 1;
+    const bool any = s_flips != 0;
+    total += static_cast<long long>(s_gain);
+    __syncthreads();
+    if (!any) break;  // a pass without a flip ends one_flip_pass
+  }
+  // write back the sides and the gain table of the final state (after the
+  // last pass flipped nothing, d0 is that table)
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+    side[v] = sd[v];
+    delta[v] = d0[v];
+  }
+  if (threadIdx.x == 0) gains[s] = total;
+}
+
 // ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
 // cand(v) = exists u in N(v), u > v, opposite side, delta_v + delta_u + 2 > 0:
 // the exact "v acts in this sweep if nothing before it changes" test,
@@ -703,7 +824,26 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   };
   // one_flip_pass for the bodies in `who`: round-parallel passes (above)
   // until a pass flips nothing; delta is rebuilt after every pass
+  // one CTA per body: when the body state fits SMEM, and the graph is small
+  // or there are enough bodies to spread over the SMs (one large body runs
+  // faster on the grid-wide rounds below)
+  const bool flip_cta = g_swap_smem && flip_cta_smem(n) <= kFlipCtaSmemMax && (n <= 8192 || count >= 16);
+  const bool flip_csr = flip_cta_smem_csr(n, 2 * g->m) <= kFlipCtaSmemMax;
+  const int64_t flip_bytes = flip_csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n);
   auto one_flip = [&](const std::vector<int32_t>& who) {
+    if (flip_cta) {  // small graphs: every pass of a body inside one CTA
+      MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kFlipCtaSmemMax)));
+      MQO_CUDA(cudaMemcpyAsync(d_live, who.data(), sizeof(int32_t) * count,
+                               cudaMemcpyHostToDevice, st));
+      k_one_flip_cta<<<count, kFlipCtaThreads, static_cast<size_t>(flip_bytes), st>>>(
+          g->d_off, g->d_nbr, n, side, delta, d_live, d_g1, flip_csr ? 1 : 0);
+      MQO_CUDA(cudaGetLastError());
+      MQO_CUDA(cudaMemcpyAsync(g1.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+      MQO_CUDA(cudaStreamSynchronize(st));
+      MQO_TRACE("one_flip (CTA path)");
+      return;
+    }
     std::vector<int32_t> plive = who, und(count);
     std::vector<int64_t> pg(count);
     std::fill(g1.begin(), g1.end(), 0);
