@@ -34,6 +34,12 @@ const bool g_swap_smem = [] {
   const char* e = std::getenv("MQO_LS_SMEM");
   return !(e && *e == '0');
 }();
+// 2-flip sweep look-ahead: warps per body (MQO_SCAN_CTA=8|16|32; 0 = one
+// warp per body without look-ahead)
+const int g_scan_cta = [] {
+  const char* e = std::getenv("MQO_SCAN_CTA");
+  return e ? std::atoi(e) : 16;
+}();
 
 __device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 1; }
 
@@ -438,6 +444,156 @@ __global__ void k_two_scan(const int64_t* __restrict__ off, const int32_t* __res
   }
 }
 
+
+// The same sweep with speculative look-ahead: a CTA of kScanWarps warps per
+// body.  Warp 0 collects the next kScanWarps candidates in scan order (the
+// current vertex, resumed after its last joint flip, then the following
+// marked vertices); warp k evaluates candidate k against the current state
+// -- the first u in its row with opposite side and delta_v + delta_u + 2 > 0
+// -- all in parallel; then the first candidate with a hit is committed and
+// the batch ends there.  Every candidate before it saw exactly the state the
+// sequential scan would have shown it (nothing was committed in between), so
+// the commits and their order are the reference's; the serial chain of
+// dependent loads is paid once per batch instead of once per candidate.
+template <int kScanWarps>
+__global__ void __launch_bounds__(32 * kScanWarps)
+    k_two_scan_cta(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                   const int32_t* __restrict__ hmax, int32_t n, int32_t count, uint8_t* side_all,
+                   int32_t* delta_all, uint8_t* cand_all, int32_t* live, int64_t* gains) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = blockIdx.x;
+  if (s >= count || !live[s]) return;
+  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
+  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
+  uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
+  __shared__ int32_t c_v[kScanWarps], r_u[kScanWarps], r_joint[kScanWarps];
+  __shared__ int64_t c_e0[kScanWarps], r_e[kScanWarps];
+  __shared__ int32_t s_k, s_pos;
+  __shared__ int64_t s_epos;
+  int64_t total = 0;
+  int32_t dmax = INT_MIN;
+  if (threadIdx.x == 0) {
+    s_pos = 0;
+    s_epos = -1;
+  }
+  __syncthreads();
+  for (;;) {
+    // A. collect the batch (warp 0)
+    if (warp == 0) {
+      int k = 0;
+      int32_t from = s_pos;
+      if (s_epos >= 0) {  // resume the current vertex's row
+        if (lane == 0) {
+          c_v[0] = s_pos;
+          c_e0[0] = s_epos;
+        }
+        k = 1;
+        from = s_pos + 1;
+      }
+      for (int32_t cb = from; cb < n && k < kScanWarps; cb += 32) {
+        if (((cb - from) & 511) == 0) {  // empty 512-mark stretches cost one round trip
+          bool any16 = false;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int32_t q = cb + 16 * lane + t;
+            any16 |= q < n && *reinterpret_cast<const volatile uint8_t*>(cand + q) != 0;
+          }
+          if (!__any_sync(0xffffffffu, any16)) {
+            cb += 512 - 32;
+            continue;
+          }
+        }
+        const bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+        unsigned mask = __ballot_sync(0xffffffffu, f);
+        while (mask && k < kScanWarps) {
+          const int i = warp_first(mask);
+          if (lane == 0) {
+            c_v[k] = cb + i;
+            c_e0[k] = -1;
+          }
+          ++k;
+          mask &= mask - 1;
+        }
+      }
+      if (lane == 0) s_k = k;
+    }
+    __syncthreads();
+    const int K = s_k;
+    if (K == 0) break;
+    // B. evaluate candidate `warp` against the current state (read only)
+    if (warp < K) {
+      const int32_t v = c_v[warp];
+      const int64_t e1 = off[v + 1];
+      int64_t e = c_e0[warp] >= 0 ? c_e0[warp] : off[v];
+      const int32_t dv = delta[v];
+      const uint8_t sv = side[v];
+      int32_t hit_u = -1, hit_j = 0;
+      int64_t hit_e = -1;
+      if (dv + hmax[v] + 2 <= 0) e = e1;  // delta_u <= hmax[v] for every higher u
+      while (e < e1) {
+        const int64_t my = e + lane;
+        bool ok = false;
+        int32_t u = 0, joint = 0;
+        if (my < e1) {
+          u = nbr[my];
+          if (u > v && side[u] != sv) {
+            joint = dv + delta[u] + 2;
+            ok = joint > 0;
+          }
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, ok);
+        if (hit) {
+          const int j = warp_first(hit);
+          hit_u = __shfl_sync(0xffffffffu, u, j);
+          hit_j = __shfl_sync(0xffffffffu, joint, j);
+          hit_e = e + j;
+          break;
+        }
+        e += 32;
+      }
+      if (lane == 0) {
+        r_u[warp] = hit_u;
+        r_joint[warp] = hit_j;
+        r_e[warp] = hit_e;
+      }
+    }
+    __syncthreads();
+    // C. commit the first hit (warp 0), advance
+    if (warp == 0) {
+      int first = -1;
+      for (int k = 0; k < K; ++k)
+        if (r_u[k] >= 0) {
+          first = k;
+          break;
+        }
+      if (first < 0) {
+        if (lane == 0) {
+          s_pos = c_v[K - 1] + 1;
+          s_epos = -1;
+        }
+      } else {
+        const int32_t v = c_v[first], u = r_u[first];
+        warp_flip(off, nbr, side, delta, v, lane, dmax);
+        warp_flip(off, nbr, side, delta, u, lane, dmax);
+        total += r_joint[first];
+        warp_mark_after_flip(off, nbr, cand, v, v, lane);
+        warp_mark_after_flip(off, nbr, cand, u, v, lane);
+        if (lane == 0) {
+          s_pos = v;
+          s_epos = r_e[first] + 1;
+        }
+      }
+      __threadfence_block();
+    }
+    __syncthreads();
+    if (s_pos >= n) break;
+  }
+  if (threadIdx.x == 0) {
+    gains[s] += total;
+    live[s] = total > 0 ? 1 : 0;  // improved: sweep again
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -809,8 +965,18 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
     for (int sweep = 0;; ++sweep) {
       k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
                                                  delta, d_live2, d_cand);
-      k_two_scan<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
-                                                   delta, d_cand, d_live2, d_g2);
+      if (g_scan_cta == 16)
+        k_two_scan_cta<16><<<count, 32 * 16, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
+                                                      side, delta, d_cand, d_live2, d_g2);
+      else if (g_scan_cta == 32)
+        k_two_scan_cta<32><<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
+                                                      side, delta, d_cand, d_live2, d_g2);
+      else if (g_scan_cta)
+        k_two_scan_cta<8><<<count, 32 * 8, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
+                                                    side, delta, d_cand, d_live2, d_g2);
+      else
+        k_two_scan<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
+                                                     delta, d_cand, d_live2, d_g2);
       MQO_CUDA(cudaGetLastError());
       MQO_CUDA(cudaMemcpyAsync(live2.data(), d_live2, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
       MQO_CUDA(cudaStreamSynchronize(st));
