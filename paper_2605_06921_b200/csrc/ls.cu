@@ -34,6 +34,11 @@ const bool g_swap_smem = [] {
   const char* e = std::getenv("MQO_LS_SMEM");
   return !(e && *e == '0');
 }();
+// MQO_SWAP_CTA=0: (1,2)-swap on one warp per body (k_mis_swap)
+const bool g_swap_cta = [] {
+  const char* e = std::getenv("MQO_SWAP_CTA");
+  return !(e && *e == '0');
+}();
 // 2-flip sweep look-ahead: warps per body (MQO_SCAN_CTA=8|16|32; 0 = one
 // warp per body without look-ahead)
 const int g_scan_cta = [] {
@@ -729,6 +734,90 @@ __device__ void warp_apply_swap(const int64_t* off, const int32_t* nbr, const in
   warp_mark_dirty(off, nbr, sel, dflag, dlist, dcount, w, frontier, lane);
 }
 
+// The sequential part of a (1,2)-swap on one warp (selects, freed
+// neighbours re-added greedily in (degree, id) order); the re-added vertices
+// are left in freed[0..*nadd).  The dirty marking is done afterwards by the
+// whole CTA (cta_mark_dirty), against the final selection: only selected
+// vertices need re-examination, and every vertex whose swap pair could
+// have changed is within two hops of x, u, w or a re-added vertex.
+__device__ void warp_swap_core(const int64_t* off, const int32_t* nbr, uint8_t* sel,
+                               int32_t* tight, int32_t* freed, int32_t x, int32_t u, int32_t w,
+                               int lane, int32_t* nadd) {
+  warp_select(off, nbr, sel, tight, x, -1, lane);
+  warp_select(off, nbr, sel, tight, u, +1, lane);
+  warp_select(off, nbr, sel, tight, w, +1, lane);
+  int32_t nf = 0;
+  if (lane == 0) {
+    for (int64_t e = off[x]; e < off[x + 1]; ++e) {
+      const int32_t z = nbr[e];
+      if (!sel[z] && tight[z] == 0) {
+        const int64_t dz = off[z + 1] - off[z];
+        int32_t k = nf++;
+        while (k > 0) {
+          const int32_t p = freed[k - 1];
+          const int64_t dp = off[p + 1] - off[p];
+          if (dp < dz || (dp == dz && p < z)) break;
+          freed[k] = p;
+          --k;
+        }
+        freed[k] = z;
+      }
+    }
+  }
+  nf = __shfl_sync(0xffffffffu, nf, 0);
+  __syncwarp();
+  int32_t na = 0;
+  for (int32_t i = 0; i < nf; ++i) {
+    const int32_t z = freed[i];
+    const bool add = !*reinterpret_cast<volatile uint8_t*>(sel + z) &&
+                     *reinterpret_cast<volatile int32_t*>(tight + z) == 0;
+    if (add) {
+      warp_select(off, nbr, sel, tight, z, +1, lane);
+      if (lane == 0) freed[na] = z;  // na <= i: compaction in place
+      ++na;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) *nadd = na;
+}
+
+// Dirty marks for the 2-hop neighbourhood of t by the whole CTA: warps over
+// s in {t} U N(t), lanes over y in {s} U N(s).
+__device__ void cta_mark_dirty(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+                               uint8_t* dflag, int32_t* dlist, int32_t* dcount, int32_t t,
+                               int32_t frontier) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + warp; a < e1; a += nw) {
+    const int32_t sv = a < e0 ? t : nbr[a];
+    const int64_t c0 = off[sv], c1 = off[sv + 1];
+    for (int64_t c = c0 - 1 + lane; c < c1; c += 32) {
+      const int32_t y = c < c0 ? sv : nbr[c];
+      if (y >= frontier || !*reinterpret_cast<const volatile uint8_t*>(sel + y)) continue;
+      unsigned* word = reinterpret_cast<unsigned*>(reinterpret_cast<uintptr_t>(dflag + y) & ~uintptr_t(3));
+      const unsigned shift = (reinterpret_cast<uintptr_t>(dflag + y) & 3) * 8;
+      const unsigned old = atomicOr(word, 1u << shift);
+      if (!((old >> shift) & 0xFF)) dlist[atomicAdd(dcount, 1)] = y;
+    }
+  }
+}
+
+// A full swap by the CTA: the core on warp 0, then the marks by everyone.
+__device__ void cta_apply_swap(const int64_t* off, const int32_t* nbr, uint8_t* sel, int32_t* tight,
+                               uint8_t* dflag, int32_t* dlist, int32_t* dcount, int32_t* freed,
+                               int32_t x, int32_t u, int32_t w, int32_t frontier, int32_t* s_nadd) {
+  if ((threadIdx.x >> 5) == 0)
+    warp_swap_core(off, nbr, sel, tight, freed, x, u, w, threadIdx.x & 31, s_nadd);
+  __syncthreads();
+  const int32_t na = *s_nadd;
+  cta_mark_dirty(off, nbr, sel, dflag, dlist, dcount, x, frontier);
+  cta_mark_dirty(off, nbr, sel, dflag, dlist, dcount, u, frontier);
+  cta_mark_dirty(off, nbr, sel, dflag, dlist, dcount, w, frontier);
+  for (int32_t i = 0; i < na; ++i)
+    cta_mark_dirty(off, nbr, sel, dflag, dlist, dcount, freed[i], frontier);
+  __syncthreads();
+}
+
 // Bytes of the SMEM-resident variant of k_mis_swap: the CSR and one body's
 // state (one warp per CTA); 16-byte aligned sections.
 __host__ __device__ inline int64_t swap_smem_bytes(int32_t n, int64_t nnz, int32_t max_degree) {
@@ -885,6 +974,154 @@ __global__ void k_mis_swap(const int64_t* __restrict__ off_g, const int32_t* __r
   }
 }
 
+// one_two_swap with a whole CTA per body (W warps): the two searches --
+// the lowest swappable vertex in the dirty list, and the first swappable
+// vertex at or after the frontier -- are evaluated by all W*32 threads
+// (block-wide minimum; the frontier scan advances W*32 vertices per step),
+// and warp 0 applies each swap exactly as k_mis_swap does.  The dirty list
+// is compacted into a second buffer (entries are unique, so its order is
+// irrelevant: only the minimum is used).  Same swaps, same order.
+__host__ __device__ inline int64_t swap_cta_smem_bytes(int32_t n, int64_t nnz, int32_t max_degree) {
+  return swap_smem_bytes(n, nnz, max_degree) + (4 * int64_t(n) + 15) / 16 * 16;
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W)
+    k_mis_swap_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
+                   int32_t count, uint8_t* sel_all, int32_t* tight_all, uint8_t* dflag_all,
+                   int32_t* dlist_all, int32_t* dlist2_all, int32_t* freed_all,
+                   int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out, int32_t smem) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int32_t s_best, s_bu, s_bw, s_keep, s_nadd;
+  const int lane = threadIdx.x & 31;
+  const int s = blockIdx.x;
+  if (s >= count) return;
+  uint8_t* sel_g = sel_all + static_cast<int64_t>(s) * n;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  uint8_t* sel = sel_g;
+  int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
+  uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
+  int32_t* dl[2] = {dlist_all + static_cast<int64_t>(s) * n, dlist2_all + static_cast<int64_t>(s) * n};
+  int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
+  int32_t* dcount = dcount_all + s;
+  if (smem) {
+    auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+    const int64_t nnz = off_g[n];
+    unsigned char* p = sm;
+    int64_t* o = reinterpret_cast<int64_t*>(p);
+    p += al(8 * (int64_t(n) + 1));
+    int32_t* nb = reinterpret_cast<int32_t*>(p);
+    p += al(4 * nnz);
+    int32_t* ti = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* d0 = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* fr = reinterpret_cast<int32_t*>(p);
+    p += al(4 * (int64_t(max_degree) + 1));
+    uint8_t* se = p;
+    p += al(n);
+    uint8_t* df = p;
+    p += al(int64_t(n) + 4);
+    int32_t* dc = reinterpret_cast<int32_t*>(p);
+    p += 16;
+    int32_t* d1 = reinterpret_cast<int32_t*>(p);
+    cta_copy(o, off_g, 8 * (int64_t(n) + 1));
+    cta_copy(nb, nbr_g, 4 * nnz);
+    cta_copy(ti, tight, 4 * int64_t(n));
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) se[i] = sel_g[i];
+    for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) df[i] = 0;
+    if (threadIdx.x == 0) *dc = 0;
+    off = o;
+    nbr = nb;
+    sel = se;
+    tight = ti;
+    dflag = df;
+    dl[0] = d0;
+    dl[1] = d1;
+    freed = fr;
+    dcount = dc;
+  }
+  __syncthreads();
+  int cur = 0;
+  int32_t frontier = 0;
+  int64_t swaps = 0;
+  for (;;) {
+    // 1. lowest swappable vertex among the dirty ones (below the frontier)
+    const int32_t nd = *reinterpret_cast<volatile int32_t*>(dcount);
+    if (threadIdx.x == 0) {
+      s_best = INT_MAX;
+      s_keep = 0;
+    }
+    __syncthreads();
+    int32_t mx = INT_MAX, mu = 0, mw = 0;
+    for (int32_t k = threadIdx.x; k < nd; k += blockDim.x) {
+      const int32_t x = dl[cur][k];
+      int32_t pu = 0, pw = 0;
+      if (lane_swap_pair(off, nbr, sel, tight, x, pu, pw)) {
+        dl[cur ^ 1][atomicAdd(&s_keep, 1)] = x;  // re-checked after the next swap
+        if (x < mx) {
+          mx = x;
+          mu = pu;
+          mw = pw;
+        }
+      } else {
+        dflag[x] = 0;
+      }
+    }
+    if (mx != INT_MAX) atomicMin(&s_best, mx);
+    __syncthreads();
+    if (mx != INT_MAX && mx == s_best) {
+      s_bu = mu;
+      s_bw = mw;
+    }
+    if (threadIdx.x == 0) *dcount = s_keep;
+    cur ^= 1;
+    __syncthreads();
+    if (s_best != INT_MAX) {
+      cta_apply_swap(off, nbr, sel, tight, dflag, dl[cur], dcount, freed, s_best, s_bu, s_bw,
+                     frontier, &s_nadd);
+      ++swaps;
+      continue;
+    }
+    // 2. first swappable vertex at or after the frontier, W*32 per step
+    if (threadIdx.x == 0) s_best = INT_MAX;
+    __syncthreads();
+    int32_t found = INT_MAX;
+    for (int32_t base = frontier; base < n; base += blockDim.x) {
+      const int32_t x = base + threadIdx.x;
+      int32_t pu = 0, pw = 0;
+      if (x < n && lane_swap_pair(off, nbr, sel, tight, x, pu, pw)) {
+        atomicMin(&s_best, x);
+        mx = x;
+        mu = pu;
+        mw = pw;
+      } else {
+        mx = INT_MAX;
+      }
+      __syncthreads();
+      found = s_best;
+      if (found != INT_MAX) {
+        if (mx == found) {
+          s_bu = mu;
+          s_bw = mw;
+        }
+        break;
+      }
+      __syncthreads();  // every thread has read s_best before the next step's atomicMin
+    }
+    __syncthreads();
+    if (found == INT_MAX) break;
+    frontier = found + 1;
+    cta_apply_swap(off, nbr, sel, tight, dflag, dl[cur], dcount, freed, found, s_bu, s_bw, frontier,
+                   &s_nadd);
+    ++swaps;
+  }
+  if (threadIdx.x == 0) swaps_out[s] = swaps;
+  if (smem)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sel_g[i] = sel[i];
+}
+
 // packed [count][W] <-> bytes [count][n]
 __global__ void k_unpack(const uint64_t* __restrict__ packed, int64_t W, int32_t n, int32_t count,
                          uint8_t* __restrict__ out) {
@@ -928,6 +1165,7 @@ struct LsWork {
   int32_t* ints = nullptr;    // [count][n] delta / tight
   uint8_t* dflag = nullptr;   // [count][n+4]
   int32_t* dlist = nullptr;   // [count][n]
+  int32_t* dlist2 = nullptr;  // [count][n] (compaction target of the CTA swap kernel)
   int32_t* freed = nullptr;   // [count][max_degree+1]
   int32_t* small = nullptr;   // [count] counters / flags
   int64_t* out64 = nullptr;   // [count]
@@ -1149,7 +1387,16 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     }
     const int64_t sbytes = swap_smem_bytes(n, 2 * g->m, g->max_degree);
     const bool smem = sbytes <= kSwapSmemMax && g_swap_smem;
-    if (smem) {
+    const int64_t cbytes = swap_cta_smem_bytes(n, 2 * g->m, g->max_degree);
+    if (g_swap_cta) {  // a CTA of 16 warps per body
+      const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
+      MQO_CUDA(cudaMallocAsync(&w.dlist2, sizeof(int32_t) * cells, st));
+      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSwapSmemMax - 1024)));
+      k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
+          g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
+          w.small, g->max_degree, d_out, csm ? 1 : 0);
+    } else if (smem) {
       MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSwapSmemMax)));
       k_mis_swap<<<count, 256, static_cast<size_t>(sbytes), st>>>(
@@ -1180,6 +1427,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   cudaFreeAsync(w.small, st);
   if (w.dflag) cudaFreeAsync(w.dflag, st);
   if (w.dlist) cudaFreeAsync(w.dlist, st);
+  if (w.dlist2) cudaFreeAsync(w.dlist2, st);
   if (w.freed) cudaFreeAsync(w.freed, st);
   MQO_TRACE("local search op %d queued", op);
 }
