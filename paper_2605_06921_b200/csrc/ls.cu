@@ -460,6 +460,41 @@ __global__ void k_two_scan(const int64_t* __restrict__ off, const int32_t* __res
 // sequential scan would have shown it (nothing was committed in between), so
 // the commits and their order are the reference's; the serial chain of
 // dependent loads is paid once per batch instead of once per candidate.
+// apply_flip (localsearch.cpp:28-33) by a whole CTA; ends with a barrier.
+__device__ __forceinline__ void cta_flip(const int64_t* __restrict__ off,
+                                         const int32_t* __restrict__ nbr, uint8_t* side,
+                                         int32_t* delta, int32_t v) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    side[v] ^= 1;
+    delta[v] = -delta[v];
+  }
+  __syncthreads();
+  const uint8_t sv = side[v];
+  for (int64_t e = off[v] + threadIdx.x, e1 = off[v + 1]; e < e1; e += blockDim.x) {
+    const int32_t u = nbr[e];
+    delta[u] += side[u] == sv ? 2 : -2;
+  }
+  __syncthreads();
+}
+
+// warp_mark_after_flip by a whole CTA: warps over y in {t} U N(t), lanes
+// over y's lower neighbours w (marks y and w when > v).
+__device__ __forceinline__ void cta_mark_after_flip(const int64_t* off, const int32_t* nbr,
+                                                    uint8_t* cand, int32_t t, int32_t v) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + warp; a < e1; a += nw) {
+    const int32_t y = a < e0 ? t : nbr[a];
+    if (lane == 0 && y > v) cand[y] = 1;
+    for (int64_t c = off[y] + lane, c1 = off[y + 1]; c < c1; c += 32) {
+      const int32_t w = nbr[c];
+      if (w >= y) break;  // rows ascending: only w < y
+      if (w > v) cand[w] = 1;
+    }
+  }
+}
+
 template <int kScanWarps>
 __global__ void __launch_bounds__(32 * kScanWarps)
     k_two_scan_cta(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
@@ -476,7 +511,6 @@ __global__ void __launch_bounds__(32 * kScanWarps)
   __shared__ int32_t s_k, s_pos;
   __shared__ int64_t s_epos;
   int64_t total = 0;
-  int32_t dmax = INT_MIN;
   if (threadIdx.x == 0) {
     s_pos = 0;
     s_epos = -1;
@@ -563,32 +597,31 @@ __global__ void __launch_bounds__(32 * kScanWarps)
       }
     }
     __syncthreads();
-    // C. commit the first hit (warp 0), advance
-    if (warp == 0) {
-      int first = -1;
-      for (int k = 0; k < K; ++k)
-        if (r_u[k] >= 0) {
-          first = k;
-          break;
-        }
-      if (first < 0) {
-        if (lane == 0) {
-          s_pos = c_v[K - 1] + 1;
-          s_epos = -1;
-        }
-      } else {
-        const int32_t v = c_v[first], u = r_u[first];
-        warp_flip(off, nbr, side, delta, v, lane, dmax);
-        warp_flip(off, nbr, side, delta, u, lane, dmax);
-        total += r_joint[first];
-        warp_mark_after_flip(off, nbr, cand, v, v, lane);
-        warp_mark_after_flip(off, nbr, cand, u, v, lane);
-        if (lane == 0) {
-          s_pos = v;
-          s_epos = r_e[first] + 1;
-        }
+    // C. commit the first hit with the whole CTA, advance
+    int first = -1;
+    for (int k = 0; k < K; ++k)
+      if (r_u[k] >= 0) {
+        first = k;
+        break;
       }
-      __threadfence_block();
+    if (first < 0) {
+      if (threadIdx.x == 0) {
+        s_pos = c_v[K - 1] + 1;
+        s_epos = -1;
+      }
+    } else {
+      const int32_t v = c_v[first], u = r_u[first];
+      const int64_t ehit = r_e[first];
+      total += r_joint[first];
+      cta_flip(off, nbr, side, delta, v);
+      cta_flip(off, nbr, side, delta, u);
+      cta_mark_after_flip(off, nbr, cand, v, v);
+      cta_mark_after_flip(off, nbr, cand, u, v);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_pos = v;
+        s_epos = ehit + 1;
+      }
     }
     __syncthreads();
     if (s_pos >= n) break;
