@@ -59,12 +59,21 @@ double* aux_buffer(mqo_batch* b) {
   return b->d_aux;
 }
 
+// Copy-in at the API: the host buffer is read completely before the call
+// returns (for pinned memory cudaMemcpyAsync would otherwise still be
+// reading it), so callers may reuse it at once.
 void upload_chain_major(mqo_batch* b, const double* host, double* dst) {
   const mqo_graph* g = b->g;
   const int64_t count = static_cast<int64_t>(g->n) * b->B;
+  if (b->Bp == 1) {  // one chain: vertex-major is chain-major, no staging
+    MQO_CUDA(cudaMemcpyAsync(dst, host, sizeof(double) * count, cudaMemcpyHostToDevice, b->stream));
+    MQO_CUDA(cudaStreamSynchronize(b->stream));
+    return;
+  }
   double* staging = aux_buffer(b);
   MQO_CUDA(cudaMemcpyAsync(staging, host, sizeof(double) * count, cudaMemcpyHostToDevice,
                            b->stream));
+  MQO_CUDA(cudaStreamSynchronize(b->stream));
   if (b->Bp != b->B)
     MQO_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * g->n * static_cast<int64_t>(b->Bp),
                              b->stream));
@@ -77,6 +86,11 @@ void upload_chain_major(mqo_batch* b, const double* host, double* dst) {
 void download_chain_major(mqo_batch* b, const double* src, double* host) {
   const mqo_graph* g = b->g;
   const int64_t count = static_cast<int64_t>(g->n) * b->B;
+  if (b->Bp == 1) {
+    MQO_CUDA(cudaMemcpyAsync(host, src, sizeof(double) * count, cudaMemcpyDeviceToHost, b->stream));
+    MQO_CUDA(cudaStreamSynchronize(b->stream));
+    return;
+  }
   double* staging = aux_buffer(b);
   if (g->n && b->B) {
     dim3 grid((g->n + 31) / 32, (b->B + 31) / 32), block(32, 8);
