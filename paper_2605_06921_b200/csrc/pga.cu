@@ -863,7 +863,17 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
   // Small problems: one cooperative persistent kernel per 256-pass chunk
   // (passes separated by grid.sync, launch-free).  Large problems: one
   // launch per pass + a one-CTA control kernel.
-  const bool persistent = int64_t(g->n) * b->Bp <= persistent_cells();
+  // Persistent kernel: small problems always; up to 32M cells when the graph
+  // is hub-light (its static row split stays balanced) and no chain tiling
+  // applies (scripts/traj_paths.py: 5-15% fewer us per pass on ER(2e4..1e6)
+  // for 4M-32M cells; BA(1e6) x 128 -- 128M cells, hubs -- is 25% slower
+  // persistent).
+  const int64_t cells = int64_t(g->n) * b->Bp;
+  const double avg_deg = g->n ? 2.0 * static_cast<double>(g->m) / g->n : 0.0;
+  const bool persistent =
+      cells <= persistent_cells() ||
+      (g_persistent_cells == (int64_t(1) << 22) && cells <= (int64_t(1) << 25) &&
+       group_quads(b) == b->Q && g->max_degree <= 32.0 * avg_deg + 32.0);
   PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl);
   const size_t smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
   if (!persistent) {  // chain tiling (see group_quads)
