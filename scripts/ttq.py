@@ -30,7 +30,18 @@ CONFIGS = {
                                       reset_fraction=0.6, reset_rounds=60), 256, 8),
     "c4": (("ba", 1000000, 5), dict(objective=4, param=0.001, alpha=0.0025, beta=0.8,
                                     reset_fraction=0.8, reset_rounds=90), 128, 8),
+    # ER(1e7, d=16) from the O(m) generator (the reference's O(n^2) ER would
+    # take ~49 h); isolated vertices stripped; the reference gets the same
+    # edge list through Graph::from_edges
+    "c5": (("erfast", 10_000_000, 16 / 10_000_000), dict(objective=0, param=2.0, alpha=0.8,
+                                                         beta=0.3, reset_fraction=0.6,
+                                                         reset_rounds=60), 64, 8),
 }
+
+
+def c5_graph(P, gen, seed, device):
+    g = P.generate(P.ErFastSpec(gen[1], gen[2]), seed, device=device)
+    return P.strip_isolated(g).core if device >= 0 else g
 
 
 def run(name, budget, seed, which):
@@ -39,6 +50,7 @@ def run(name, budget, seed, which):
     if which == "gpu":
         import paper_2605_06921_b200 as P
         g = (P.generate(P.ErSpec(gen[1], gen[2]), seed) if gen[0] == "er"
+             else c5_graph(P, gen, seed, 0) if gen[0] == "erfast"
              else P.generate(P.BaSpec(gen[1], gen[2]), seed))
         spec = P.MisQubo(pc["param"]) if pc["objective"] == 0 else P.PerturbedBias(pc["param"])
         cfg = P.SolverConfig(objective=spec, optimizer=P.OptimizerConfig(pc["alpha"], pc["beta"]),
@@ -51,7 +63,23 @@ def run(name, budget, seed, which):
                     edge_chain_per_s=r.total_iterations * 2 * g.m() / max(r.elapsed_secs, 1e-9))
     L = oracle.load("ref" if oracle.have_ref() else "oracle")
     os.environ["MQO_THREADS"] = str(os.cpu_count() or 1)
-    g = L.generate_er(gen[1], gen[2], seed) if gen[0] == "er" else L.generate_ba(gen[1], gen[2], seed)
+    if gen[0] == "erfast":  # the GPU side's edge list, stripped, through from_edges
+        import numpy as np
+        import paper_2605_06921_b200 as P
+        hg = P.generate(P.ErFastSpec(gen[1], gen[2]), seed, device=-1)
+        off, nbr = hg.csr()
+        deg = np.diff(off)
+        keep = np.flatnonzero(deg > 0)
+        remap = np.full(hg.n(), -1, np.int64)
+        remap[keep] = np.arange(len(keep))
+        src = np.repeat(np.arange(hg.n()), deg)
+        m = src < nbr
+        edges = np.stack([remap[src[m]], remap[nbr[m]]], 1).astype(np.int32)
+        del hg, off, nbr, src, m
+        g = L.from_edges(len(keep), edges)
+    else:
+        g = (L.generate_er(gen[1], gen[2], seed) if gen[0] == "er"
+             else L.generate_ba(gen[1], gen[2], seed))
     c = oracle.Cfg(time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K, **pc)
     t0 = time.time()
     rep, _ = L.solve_pooled(g, c.to_c())
