@@ -44,7 +44,7 @@ def c5_graph(P, gen, seed, device):
     return P.strip_isolated(g).core if device >= 0 else g
 
 
-def run(name, budget, seed, which):
+def run(name, budget, seed, which, local_search=True):
     import oracle
     gen, pc, B, K = CONFIGS[name]
     if which == "gpu":
@@ -55,7 +55,8 @@ def run(name, budget, seed, which):
         spec = P.MisQubo(pc["param"]) if pc["objective"] == 0 else P.PerturbedBias(pc["param"])
         cfg = P.SolverConfig(objective=spec, optimizer=P.OptimizerConfig(pc["alpha"], pc["beta"]),
                              reset_fraction=pc["reset_fraction"], reset_rounds=pc["reset_rounds"],
-                             time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K)
+                             time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K,
+                             local_search=local_search)
         t0 = time.time()
         r = P.solve_pooled(g, cfg)
         return dict(score=r.best_score, outer_loops=r.outer_loops, trajectories=r.trajectories,
@@ -80,7 +81,8 @@ def run(name, budget, seed, which):
     else:
         g = (L.generate_er(gen[1], gen[2], seed) if gen[0] == "er"
              else L.generate_ba(gen[1], gen[2], seed))
-    c = oracle.Cfg(time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K, **pc)
+    c = oracle.Cfg(time_budget_secs=budget, seed=seed, pool_batch=B, pool_keep=K,
+                   local_search=1 if local_search else 0, **pc)
     t0 = time.time()
     rep, _ = L.solve_pooled(g, c.to_c())
     return dict(score=rep["score"], outer_loops=rep["outer_loops"],
@@ -97,13 +99,17 @@ def main():
     ap.add_argument("--seeds", default="1")
     ap.add_argument("--which", default="gpu,ref")
     ap.add_argument("--out", default="")
+    ap.add_argument("--no-local-search", action="store_true",
+                    help="both sides without local search (the reference's restart-from-0 "
+                         "(1,2)-swap is O(swaps x n): hours at n = 1e7)")
     args = ap.parse_args()
     rows = []
     for name in args.configs.split(","):
         for seed in [int(s) for s in args.seeds.split(",")]:
             for which in args.which.split(","):
-                res = run(name, args.budget, seed, which)
-                row = dict(config=name, seed=seed, impl=which, budget_secs=args.budget, **res)
+                res = run(name, args.budget, seed, which, not args.no_local_search)
+                row = dict(config=name, seed=seed, impl=which, budget_secs=args.budget,
+                           local_search=not args.no_local_search, **res)
                 print(json.dumps(row), flush=True)
                 rows.append(row)
     if args.out:
