@@ -39,6 +39,20 @@ CONFIGS = {
 }
 
 
+def stripped_edges(g):
+    """(n_core, edges u<v) of g without its isolated vertices, relabelled in
+    ascending order (strip_isolated, graph.cpp:180-198)."""
+    import numpy as np
+    off, nbr = g.csr()
+    deg = np.diff(off)
+    keep = np.flatnonzero(deg > 0)
+    remap = np.full(g.n(), -1, np.int64)
+    remap[keep] = np.arange(len(keep))
+    src = np.repeat(np.arange(g.n()), deg)
+    m = src < nbr
+    return len(keep), np.stack([remap[src[m]], remap[nbr[m]]], 1).astype(np.int32)
+
+
 def c5_graph(P, gen, seed, device):
     g = P.generate(P.ErFastSpec(gen[1], gen[2]), seed, device=device)
     return P.strip_isolated(g).core if device >= 0 else g
@@ -68,16 +82,9 @@ def run(name, budget, seed, which, local_search=True):
         import numpy as np
         import paper_2605_06921_b200 as P
         hg = P.generate(P.ErFastSpec(gen[1], gen[2]), seed, device=-1)
-        off, nbr = hg.csr()
-        deg = np.diff(off)
-        keep = np.flatnonzero(deg > 0)
-        remap = np.full(hg.n(), -1, np.int64)
-        remap[keep] = np.arange(len(keep))
-        src = np.repeat(np.arange(hg.n()), deg)
-        m = src < nbr
-        edges = np.stack([remap[src[m]], remap[nbr[m]]], 1).astype(np.int32)
-        del hg, off, nbr, src, m
-        g = L.from_edges(len(keep), edges)
+        n_core, edges = stripped_edges(hg)
+        del hg
+        g = L.from_edges(n_core, edges)
     else:
         g = (L.generate_er(gen[1], gen[2], seed) if gen[0] == "er"
              else L.generate_ba(gen[1], gen[2], seed))

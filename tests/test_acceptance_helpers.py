@@ -38,3 +38,19 @@ def test_dense_grad_matches_oracle(O):
                 want = O.gradient(og, kind, param, x)
                 got = A.dense_grad(spec, D, x[None, :])[0]
                 assert np.array_equal(got, want), (kind, x)
+
+
+def test_ttq_stripped_edges_match_strip_isolated(O):
+    """scripts/ttq.py hands the reference the GPU side's stripped graph."""
+    spec = importlib.util.spec_from_file_location("ttq", os.path.join(ROOT, "scripts", "ttq.py"))
+    ttq = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(ttq)
+    import paper_2605_06921_b200 as P
+    hg = P.generate(P.ErFastSpec(3000, 1.5 / 3000), 4, device=-1)
+    n_core, edges = ttq.stripped_edges(hg)
+    off, nbr = hg.csr()
+    og = O.from_edges(hg.n(), np.stack([np.repeat(np.arange(hg.n()), np.diff(off)), nbr], 1))
+    ref_core = O.strip_isolated(og)[0]
+    mine = O.from_edges(n_core, edges)
+    assert mine.n == ref_core.n < hg.n()
+    assert all((a == b).all() for a, b in zip(mine.csr(), ref_core.csr()))
