@@ -215,3 +215,34 @@ def test_graph_files_roundtrip(tmp_path):
     (tmp_path / "bad.txt").write_text("5 2\n0 1\n")
     with pytest.raises(ParseError, match="line 3: truncated edge list"):  # graph_io.cpp:83
         Graph.load(str(tmp_path / "bad.txt"), device=-1)
+
+
+def test_large_goldens_oracle(O):
+    """tests/golden/large.npz (make_large_golden.py, from the compiled
+    reference): full-size RNG stream, 1e6-vertex resets, C3 steps and local
+    search, reproduced by the oracle."""
+    z = load("large")
+    r = O.rng(O.derive_seed(1, 1))
+    assert sha(np.array([r.next_u64() for _ in range(1_000_000)], np.uint64)) == str(
+        z["stream_1e6_sha"])
+    for rho in (0.5, 0.8):
+        r = O.rng(O.derive_seed(1_000_000, int(rho * 10)))
+        _, chosen = O.global_reset(np.ones(1_000_000), rho, r)
+        assert sha(chosen) == str(z[f"reset_1e6_{rho}_sha"])
+        assert r.next_u64() == int(z[f"reset_1e6_{rho}_next"][0])
+    g = O.generate_er(100_000, 1e-4, 1)
+    assert sha(*g.csr()) == str(z["c3_csr_sha"])
+    x = np.random.default_rng(33).uniform(0.0, 1.0, g.n)
+    v = np.zeros(g.n)
+    for t in range(1, 11):
+        x, v = O.step(g, MIS_QUBO, 2.0, x, v, 0.8, 0.3)
+        if t in (1, 10):
+            assert sha(x) == str(z[f"c3_x{t}_sha"]) and sha(v) == str(z[f"c3_v{t}_sha"])
+    ind, _ = O.greedy_maximalize(g, np.zeros(g.n, np.uint8))
+    assert sha(ind) == str(z["c3_greedy_sha"])
+    ind2, size = O.one_two_swap(g, ind)
+    assert sha(ind2) == str(z["c3_swap_sha"]) and size == int(z["c3_swap_size"][0])
+    gb = O.generate_ba(100_000, 5, 2)
+    side = np.random.default_rng(1).integers(0, 2, gb.n).astype(np.uint8)
+    s3, gain = O.one_two_flip(gb, side)
+    assert sha(s3) == str(z["ba1e5_onetwo_sha"]) and gain == int(z["ba1e5_onetwo_gain"][0])

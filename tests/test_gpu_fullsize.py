@@ -105,3 +105,58 @@ def test_c5_integer_gradients_all_chains(P):
     assert abs(2 * g.m() / g.n() - 16.0) < 0.05
     # MIS QUBO gradient = 1 - gamma (A x) (objectives.cpp:109-113), gamma = 2
     _integer_property(P, g, 16, P.MisQubo(2.0), -2.0, 1.0, 2)
+
+
+def _sha(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _xoshiro_next(s):
+    m = (1 << 64) - 1
+    rotl = lambda x, k: ((x << k) | (x >> (64 - k))) & m  # noqa: E731
+    return (rotl((s[1] * 5) & m, 7) * 9) & m
+
+
+def test_large_goldens_gpu(P):
+    """The GPU path against tests/golden/large.npz (the compiled reference):
+    1e6-vertex resets, C3 (ER(1e5)) CSR / steps / greedy / (1,2)-swap, and
+    one_two_flip on BA(1e5)."""
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "large.npz"))
+    g6 = P.Graph.from_edges(1_000_000, [(0, 1)])
+    for rho in (0.5, 0.8):
+        b = P.ChainBatch(g6, 1)
+        b.seed_streams(1_000_000, int(rho * 10))
+        b.set_x(np.ones((1, 1_000_000)))
+        b.global_reset(rho)
+        x = b.get_x()[0]
+        assert _sha(np.flatnonzero(x == 0).astype(np.int32)) == str(z[f"reset_1e6_{rho}_sha"])
+        s = [int(w) for w in b.get_streams()[0]["s"]]
+        assert _xoshiro_next(s) == int(z[f"reset_1e6_{rho}_next"][0])
+    g = P.generate(P.ErSpec(100_000, 1e-4), 1)
+    assert _sha(*g.csr()) == str(z["c3_csr_sha"])
+    b = P.ChainBatch(g, 1)
+    b.set_x(np.random.default_rng(33).uniform(0.0, 1.0, (1, g.n())))
+    b.zero_v()
+    cfg = P.OptimizerConfig(alpha=0.8, beta=0.3)
+    for t in range(1, 11):
+        b.step(P.MisQubo(2.0), cfg)
+        if t in (1, 10):
+            assert _sha(b.get_x()[0]) == str(z[f"c3_x{t}_sha"])
+            assert _sha(b.get_v()[0]) == str(z[f"c3_v{t}_sha"])
+    b.set_x(np.zeros((1, g.n())))  # harvest of the empty set = greedy_maximalize(g, {})
+    _, valid, packed = b.harvest(P.PROBLEM_MIS)
+    ind = P.unpack_bodies(packed, g.n())[0]
+    assert valid[0] and _sha(ind) == str(z["c3_greedy_sha"])
+    ind2, size = P.one_two_swap(g, ind)
+    assert _sha(np.asarray(ind2, np.uint8)) == str(z["c3_swap_sha"])
+    assert size == int(z["c3_swap_size"][0])
+    gb = P.generate(P.BaSpec(100_000, 5), 2)
+    side = np.random.default_rng(1).integers(0, 2, gb.n()).astype(np.uint8)
+    s3, gain = P.one_two_flip(gb, side)
+    assert _sha(np.asarray(s3, np.uint8)) == str(z["ba1e5_onetwo_sha"])
+    assert gain == int(z["ba1e5_onetwo_gain"][0])
