@@ -1321,6 +1321,24 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       MQO_TRACE("one_flip pass %d: %d rounds", pass, rounds);
     }
   };
+  if (op == 0 && flip_cta) {
+    // one_flip_pass alone on the CTA path: every body starts live and the
+    // pass gains are the result, so nothing returns to the host here (no
+    // round trip; the caller's final copy-out synchronises)
+    MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kFlipCtaSmemMax)));
+    MQO_CUDA(cudaMemsetAsync(d_live, 1, sizeof(int32_t) * count, st));  // nonzero = live
+    k_one_flip_cta<<<count, kFlipCtaThreads, static_cast<size_t>(flip_bytes), st>>>(
+        g->d_off, g->d_nbr, n, side, delta, d_live, d_out, flip_csr ? 1 : 0);
+    MQO_CUDA(cudaGetLastError());
+    cudaFreeAsync(d_live, st);
+    cudaFreeAsync(d_live2, st);
+    cudaFreeAsync(d_und, st);
+    cudaFreeAsync(d_g1, st);
+    cudaFreeAsync(d_g2, st);
+    cudaFreeAsync(d_cand, st);
+    return;
+  }
   if (op == 0) {
     one_flip(live);
     total = g1;
