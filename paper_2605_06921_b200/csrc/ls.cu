@@ -20,6 +20,7 @@
 // finds exactly the vertex the restarted scan would find.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -198,6 +199,13 @@ __host__ __device__ inline int64_t flip_cta_smem_csr(int32_t n, int64_t nnz) {
   return flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
 }
 
+// one CTA per body: when the body state fits SMEM, and the graph is small or
+// there are enough bodies to spread over the SMs (one large body runs faster
+// on the grid-wide rounds)
+inline bool one_flip_cta_fits(int32_t n, int32_t count) {
+  return g_swap_smem && flip_cta_smem(n) <= kFlipCtaSmemMax && (n <= 8192 || count >= 16);
+}
+
 // `csr`: the CSR is staged in shared memory too (it fits next to the body
 // state); every row walk is then ~30-cycle SMEM loads instead of L2 trips.
 __global__ void __launch_bounds__(kFlipCtaThreads, 1)
@@ -210,7 +218,8 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   volatile uint8_t* st = sd + n;
   const int64_t* off = off_g;
   const int32_t* nbr = nbr_g;
-  if (csr && live[blockIdx.x]) {
+  // live == nullptr: every body is live
+  if (csr && (!live || live[blockIdx.x])) {
     int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
     int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
     const int64_t nnz = off_g[n];
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   const int s = blockIdx.x;
   uint8_t* side = side_all + int64_t(s) * n;
   int32_t* delta = delta_all + int64_t(s) * n;
-  if (!live[s]) {
+  if (live && !live[s]) {
     if (threadIdx.x == 0) gains[s] = 0;
     return;
   }
@@ -1264,7 +1273,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   // one CTA per body: when the body state fits SMEM, and the graph is small
   // or there are enough bodies to spread over the SMs (one large body runs
   // faster on the grid-wide rounds below)
-  const bool flip_cta = g_swap_smem && flip_cta_smem(n) <= kFlipCtaSmemMax && (n <= 8192 || count >= 16);
+  const bool flip_cta = one_flip_cta_fits(n, count);
   const bool flip_csr = flip_cta_smem_csr(n, 2 * g->m) <= kFlipCtaSmemMax;
   const int64_t flip_bytes = flip_csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n);
   auto one_flip = [&](const std::vector<int32_t>& who) {
@@ -1321,24 +1330,6 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       MQO_TRACE("one_flip pass %d: %d rounds", pass, rounds);
     }
   };
-  if (op == 0 && flip_cta) {
-    // one_flip_pass alone on the CTA path: every body starts live and the
-    // pass gains are the result, so nothing returns to the host here (no
-    // round trip; the caller's final copy-out synchronises)
-    MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kFlipCtaSmemMax)));
-    MQO_CUDA(cudaMemsetAsync(d_live, 1, sizeof(int32_t) * count, st));  // nonzero = live
-    k_one_flip_cta<<<count, kFlipCtaThreads, static_cast<size_t>(flip_bytes), st>>>(
-        g->d_off, g->d_nbr, n, side, delta, d_live, d_out, flip_csr ? 1 : 0);
-    MQO_CUDA(cudaGetLastError());
-    cudaFreeAsync(d_live, st);
-    cudaFreeAsync(d_live2, st);
-    cudaFreeAsync(d_und, st);
-    cudaFreeAsync(d_g1, st);
-    cudaFreeAsync(d_g2, st);
-    cudaFreeAsync(d_cand, st);
-    return;
-  }
   if (op == 0) {
     one_flip(live);
     total = g1;
@@ -1380,6 +1371,27 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   MQO_TRACE("local search op %d on %d bodies", op, count);
   LsWork w;
   const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
+  if (op == 0 && one_flip_cta_fits(n, count)) {
+    // one_flip_pass alone on the CTA path: the kernel builds its own gain
+    // table, every body starts live and its pass gains are the result, so the
+    // call is unpack -> k_one_flip_cta -> pack with no host round trip (the
+    // caller's copy-out synchronises)
+    const bool csr = flip_cta_smem_csr(n, 2 * g->m) <= kFlipCtaSmemMax;
+    MQO_CUDA(cudaMallocAsync(&w.bytes, cells, st));
+    MQO_CUDA(cudaMallocAsync(&w.ints, sizeof(int32_t) * cells, st));
+    k_unpack<<<ls_grid(cells), 256, 0, st>>>(d_packed, W, n, count, w.bytes);
+    MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kFlipCtaSmemMax)));
+    k_one_flip_cta<<<count, kFlipCtaThreads,
+                     static_cast<size_t>(csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n)), st>>>(
+        g->d_off, g->d_nbr, n, w.bytes, w.ints, nullptr, d_out, csr ? 1 : 0);
+    k_pack_bytes<<<ls_grid(int64_t(count) * W), 256, 0, st>>>(w.bytes, W, n, count, d_packed, nullptr);
+    MQO_CUDA(cudaGetLastError());
+    cudaFreeAsync(w.bytes, st);
+    cudaFreeAsync(w.ints, st);
+    MQO_TRACE("local search op 0 (CTA path) queued");
+    return;
+  }
   MQO_CUDA(cudaMallocAsync(&w.bytes, cells, st));
   MQO_CUDA(cudaMallocAsync(&w.ints, sizeof(int32_t) * cells, st));
   MQO_CUDA(cudaMallocAsync(&w.small, sizeof(int32_t) * count, st));
@@ -1494,25 +1506,29 @@ extern "C" int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_
     MQO_CUDA(cudaSetDevice(b->g->device));
     if (count == 0) return;
     const int64_t W = body_words(b->g->n);
+    const int64_t words = W * count;
+    // one device buffer [bodies | results] so the copy-out is a single D2H
     uint64_t* d_packed = nullptr;
-    int64_t* d_out = nullptr;
     cudaStream_t st = b->stream;
-    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * std::max<int64_t>(1, W * count), st));
-    MQO_CUDA(cudaMallocAsync(&d_out, sizeof(int64_t) * count, st));
-    MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * W * count, cudaMemcpyHostToDevice, st));
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * (words + count), st));
+    int64_t* d_out = reinterpret_cast<int64_t*>(d_packed + words);
+    MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * words, cudaMemcpyHostToDevice, st));
+    MQO_TRACE("mqo_local_search: bodies uploaded");
     try {
       local_search_device(b, op, count, d_packed, d_out, st);
     } catch (...) {
       cudaFreeAsync(d_packed, st);
-      cudaFreeAsync(d_out, st);
       cudaStreamSynchronize(st);
       throw;
     }
-    MQO_CUDA(cudaMemcpyAsync(packed, d_packed, sizeof(uint64_t) * W * count, cudaMemcpyDeviceToHost, st));
-    MQO_CUDA(cudaMemcpyAsync(out, d_out, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+    std::vector<uint64_t> h(words + count);
+    MQO_CUDA(cudaMemcpyAsync(h.data(), d_packed, sizeof(uint64_t) * (words + count),
+                             cudaMemcpyDeviceToHost, st));
     cudaFreeAsync(d_packed, st);
-    cudaFreeAsync(d_out, st);
     MQO_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(packed, h.data(), sizeof(uint64_t) * words);
+    std::memcpy(out, h.data() + words, sizeof(int64_t) * count);
+    MQO_TRACE("mqo_local_search: done");
   });
 }
 
