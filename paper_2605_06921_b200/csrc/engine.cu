@@ -35,7 +35,7 @@ void read_outcomes(mqo_batch* b, int32_t* iterations, int32_t* reasons);
 void launch_project(mqo_batch* b, double* x, int32_t problem);
 void upload_chain_major(mqo_batch* b, const double* host, double* dst);
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
-                         int64_t* d_out, cudaStream_t st);
+                         int64_t* d_out, cudaStream_t st, int32_t* d_bad = nullptr);
 
 // init_state (solver.cpp:30-46) on the host with this process's libm, so the
 // Box-Muller draws are bit-identical to the reference's (glibc log/sin/cos

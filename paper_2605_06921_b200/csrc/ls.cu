@@ -1032,12 +1032,14 @@ __global__ void __launch_bounds__(32 * W)
     k_mis_swap_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
                    int32_t count, uint8_t* sel_all, int32_t* tight_all, uint8_t* dflag_all,
                    int32_t* dlist_all, int32_t* dlist2_all, int32_t* freed_all,
-                   int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out, int32_t smem) {
+                   int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out, int32_t smem,
+                   const int32_t* __restrict__ bad) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int32_t s_best, s_bu, s_bw, s_keep, s_nadd;
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x;
   if (s >= count) return;
+  if (bad && bad[s]) return;  // not a maximal independent set: the host throws
   uint8_t* sel_g = sel_all + static_cast<int64_t>(s) * n;
   const int64_t* off = off_g;
   const int32_t* nbr = nbr_g;
@@ -1362,8 +1364,12 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   cudaFreeAsync(d_cand, st);
 }
 
+// d_bad (one_two_swap only, may be null): when given, the input check of
+// k_tight is left in d_bad[count] (bit 0 not independent, bit 1 not maximal)
+// for the caller to raise after its copy-out, instead of a host round trip
+// here; flagged bodies are left untouched.
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
-                         int64_t* d_out, cudaStream_t st) {
+                         int64_t* d_out, cudaStream_t st, int32_t* d_bad) {
   mqo_graph* g = b->g;
   const int32_t n = g->n;
   const int64_t W = body_words(n);
@@ -1415,6 +1421,24 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
       }
     }
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
+  } else if (d_bad && g_swap_cta) {
+    MQO_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t) * count, st));
+    k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, d_bad);
+    MQO_CUDA(cudaGetLastError());
+    MQO_CUDA(cudaMallocAsync(&w.dflag, int64_t(count) * (n + 4), st));
+    MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
+    MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
+    MQO_CUDA(cudaMallocAsync(&w.dlist2, sizeof(int32_t) * cells, st));
+    MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
+    const int64_t cbytes = swap_cta_smem_bytes(n, 2 * g->m, g->max_degree);
+    const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
+    MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSwapSmemMax - 1024)));
+    k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
+        g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
+        w.small, g->max_degree, d_out, csm ? 1 : 0, d_bad);
+    MQO_CUDA(cudaGetLastError());
+    MQO_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t) * count, st));
   } else {
     k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.small);
     MQO_CUDA(cudaGetLastError());
@@ -1458,7 +1482,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
                                     static_cast<int>(kSwapSmemMax - 1024)));
       k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
           g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
-          w.small, g->max_degree, d_out, csm ? 1 : 0);
+          w.small, g->max_degree, d_out, csm ? 1 : 0, nullptr);
     } else if (smem) {
       MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSwapSmemMax)));
@@ -1507,25 +1531,35 @@ extern "C" int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_
     if (count == 0) return;
     const int64_t W = body_words(b->g->n);
     const int64_t words = W * count;
-    // one device buffer [bodies | results] so the copy-out is a single D2H
+    // one device buffer [bodies | results | input flags] so the copy-out is a
+    // single D2H
+    const int64_t total = words + count + (count + 1) / 2;
     uint64_t* d_packed = nullptr;
     cudaStream_t st = b->stream;
-    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * (words + count), st));
+    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * total, st));
     int64_t* d_out = reinterpret_cast<int64_t*>(d_packed + words);
+    int32_t* d_bad = reinterpret_cast<int32_t*>(d_packed + words + count);
+    MQO_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t) * count, st));
     MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * words, cudaMemcpyHostToDevice, st));
     MQO_TRACE("mqo_local_search: bodies uploaded");
     try {
-      local_search_device(b, op, count, d_packed, d_out, st);
+      local_search_device(b, op, count, d_packed, d_out, st, op == 3 ? d_bad : nullptr);
     } catch (...) {
       cudaFreeAsync(d_packed, st);
       cudaStreamSynchronize(st);
       throw;
     }
-    std::vector<uint64_t> h(words + count);
-    MQO_CUDA(cudaMemcpyAsync(h.data(), d_packed, sizeof(uint64_t) * (words + count),
-                             cudaMemcpyDeviceToHost, st));
+    std::vector<uint64_t> h(total);
+    MQO_CUDA(cudaMemcpyAsync(h.data(), d_packed, sizeof(uint64_t) * total, cudaMemcpyDeviceToHost, st));
     cudaFreeAsync(d_packed, st);
     MQO_CUDA(cudaStreamSynchronize(st));
+    // one_two_swap's input check (localsearch.cpp:88-96), raised before the
+    // caller's buffer is touched
+    const int32_t* bad = reinterpret_cast<const int32_t*>(h.data() + words + count);
+    for (int32_t i = 0; i < count; ++i) {
+      if (bad[i] & 1) throw std::invalid_argument("one_two_swap: input not an independent set");
+      if (bad[i] & 2) throw std::invalid_argument("one_two_swap: input not maximal");
+    }
     std::memcpy(packed, h.data(), sizeof(uint64_t) * words);
     std::memcpy(out, h.data() + words, sizeof(int64_t) * count);
     MQO_TRACE("mqo_local_search: done");

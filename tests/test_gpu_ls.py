@@ -125,3 +125,25 @@ def test_large_vs_oracle(O, P):
     got, size = P.one_two_swap(pg, start)
     ref, rsize = O.one_two_swap(og, start)
     assert size == rsize and (got == ref).all()
+
+
+def test_swap_batch_input_check_leaves_caller_buffer(P):
+    # one_two_swap on several bodies with one invalid: the call raises the
+    # reference's message and the caller's packed bodies are not modified
+    # (the input check is read back with the results, after the kernels)
+    import ctypes as C
+    from paper_2605_06921_b200 import _lib
+    star = G(P, 5, [(0, v) for v in range(1, 5)])
+    b = P.ChainBatch(star, 1)
+    good = [1, 0, 0, 0, 0]
+    for bad, msg in (([1, 1, 0, 0, 0], "not an independent set"), ([0, 1, 1, 0, 0], "not maximal")):
+        pk = P.pack_bodies(np.array([good, bad, good], np.uint8))
+        before = pk.copy()
+        out = np.zeros(3, np.int64)
+        rc = _lib.lib.mqo_local_search(b._h, _lib.LS_ONE_TWO_SWAP, 3,
+                                       pk.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                       out.ctypes.data_as(C.POINTER(C.c_int64)))
+        assert rc != 0 and msg in _lib.lib.mqo_last_error().decode()
+        assert np.array_equal(pk, before)
+    pk, out = P.local_search(b, _lib.LS_ONE_TWO_SWAP, P.pack_bodies(np.array([good, good], np.uint8)))
+    assert out.tolist() == [4, 4]
