@@ -194,7 +194,8 @@ __global__ void k_flip_apply(int32_t n, int32_t count, uint8_t* side_all,
 // state in global memory (one_two_flip's 2-flip sweep reads it).
 constexpr int kFlipCtaThreads = 1024;
 constexpr int64_t kFlipCtaSmemMax = 226 * 1024;  // + static SMEM stays under the 227 KB cap
-__host__ __device__ inline int64_t flip_cta_smem(int32_t n) { return (6 * int64_t(n) + 15) / 16 * 16; }
+// d0 [n] int32, lo [n] int32 (lower-neighbour count per row), side [n], decision [n]
+__host__ __device__ inline int64_t flip_cta_smem(int32_t n) { return (10 * int64_t(n) + 15) / 16 * 16; }
 __host__ __device__ inline int64_t flip_cta_smem_csr(int32_t n, int64_t nnz) {
   return flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
 }
@@ -208,25 +209,28 @@ inline bool one_flip_cta_fits(int32_t n, int32_t count) {
 
 // `csr`: the CSR is staged in shared memory too (it fits next to the body
 // state); every row walk is then ~30-cycle SMEM loads instead of L2 trips.
+// CSR as a template parameter: the row walks then compile to LDS instead of
+// generic loads.
+template <bool CSR>
 __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     k_one_flip_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
                    uint8_t* side_all, int32_t* delta_all, const int32_t* __restrict__ live,
-                   int64_t* __restrict__ gains, int32_t csr) {
+                   int64_t* __restrict__ gains) {
   extern __shared__ __align__(16) unsigned char sm[];
   int32_t* d0 = reinterpret_cast<int32_t*>(sm);
-  uint8_t* sd = sm + 4 * int64_t(n);
+  int32_t* lo_cnt = d0 + n;
+  uint8_t* sd = sm + 8 * int64_t(n);
   volatile uint8_t* st = sd + n;
-  const int64_t* off = off_g;
-  const int32_t* nbr = nbr_g;
+  int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
+  int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+  const int64_t* off = CSR ? o : off_g;
+  const int32_t* nbr = CSR ? nb : nbr_g;
   // live == nullptr: every body is live
-  if (csr && (!live || live[blockIdx.x])) {
-    int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
-    int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+  if (CSR && (!live || live[blockIdx.x])) {
     const int64_t nnz = off_g[n];
     for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
+#pragma unroll 4
     for (int64_t i = threadIdx.x; i < nnz; i += blockDim.x) nb[i] = nbr_g[i];
-    off = o;
-    nbr = nb;
   }
   __shared__ unsigned long long s_gain;
   __shared__ int s_flips;
@@ -237,7 +241,20 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     if (threadIdx.x == 0) gains[s] = 0;
     return;
   }
-  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) sd[v] = side[v];
+  __syncthreads();  // CSR staged
+  // lower neighbours are a row prefix (rows ascend): their count, so the
+  // round and commit walks below are counted loops the compiler can unroll
+  // (independent loads in flight) instead of break-terminated chains
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+    sd[v] = side[v];
+    int64_t a = off[v], b = off[v + 1];
+    const int64_t e0 = a;
+    while (a < b) {  // first entry >= v
+      const int64_t mid = (a + b) >> 1;
+      if (nbr[mid] < v) a = mid + 1; else b = mid;
+    }
+    lo_cnt[v] = static_cast<int32_t>(a - e0);
+  }
   __syncthreads();
   long long total = 0;
   for (;;) {
@@ -245,7 +262,10 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
       const uint8_t sv = sd[v];
       int32_t same = 0;
-      for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) same += sd[nbr[e]] == sv ? 1 : -1;
+      const int64_t e0 = off[v];
+      const int32_t deg = static_cast<int32_t>(off[v + 1] - e0);
+#pragma unroll 4
+      for (int32_t k = 0; k < deg; ++k) same += sd[nbr[e0 + k]] == sv ? 1 : -1;
       d0[v] = same;
       st[v] = 0;
     }
@@ -261,9 +281,11 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
         if (st[v]) continue;
         const uint8_t sv = sd[v];
         int32_t base = d0[v], lo = 0, hi = 0;
-        for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
-          const int32_t u = nbr[e];
-          if (u >= v) break;
+        const int64_t e0 = off[v];
+        const int32_t L = lo_cnt[v];
+#pragma unroll 4
+        for (int32_t k = 0; k < L; ++k) {
+          const int32_t u = nbr[e0 + k];
           const int32_t c = sd[u] == sv ? -2 : 2;
           const uint8_t su = st[u];
           if (su == 2)
@@ -288,9 +310,11 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
       ++flips;
       const uint8_t sv = sd[v];
       int32_t at = d0[v];
-      for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
-        const int32_t u = nbr[e];
-        if (u >= v) break;
+      const int64_t e0 = off[v];
+      const int32_t L = lo_cnt[v];
+#pragma unroll 4
+      for (int32_t k = 0; k < L; ++k) {
+        const int32_t u = nbr[e0 + k];
         if (st[u] == 2) at += sd[u] == sv ? -2 : 2;
       }
       g += at;
@@ -312,6 +336,13 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     delta[v] = d0[v];
   }
   if (threadIdx.x == 0) gains[s] = total;
+}
+
+void set_flip_cta_smem_attr() {
+  MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kFlipCtaSmemMax)));
+  MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kFlipCtaSmemMax)));
 }
 
 // ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
@@ -1280,12 +1311,12 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   const int64_t flip_bytes = flip_csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n);
   auto one_flip = [&](const std::vector<int32_t>& who) {
     if (flip_cta) {  // small graphs: every pass of a body inside one CTA
-      MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kFlipCtaSmemMax)));
+      set_flip_cta_smem_attr();
       MQO_CUDA(cudaMemcpyAsync(d_live, who.data(), sizeof(int32_t) * count,
                                cudaMemcpyHostToDevice, st));
-      k_one_flip_cta<<<count, kFlipCtaThreads, static_cast<size_t>(flip_bytes), st>>>(
-          g->d_off, g->d_nbr, n, side, delta, d_live, d_g1, flip_csr ? 1 : 0);
+      (flip_csr ? k_one_flip_cta<true> : k_one_flip_cta<false>)<<<count, kFlipCtaThreads,
+                                                                  static_cast<size_t>(flip_bytes), st>>>(
+          g->d_off, g->d_nbr, n, side, delta, d_live, d_g1);
       MQO_CUDA(cudaGetLastError());
       MQO_CUDA(cudaMemcpyAsync(g1.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
       MQO_CUDA(cudaStreamSynchronize(st));
@@ -1386,11 +1417,11 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     MQO_CUDA(cudaMallocAsync(&w.bytes, cells, st));
     MQO_CUDA(cudaMallocAsync(&w.ints, sizeof(int32_t) * cells, st));
     k_unpack<<<ls_grid(cells), 256, 0, st>>>(d_packed, W, n, count, w.bytes);
-    MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kFlipCtaSmemMax)));
-    k_one_flip_cta<<<count, kFlipCtaThreads,
-                     static_cast<size_t>(csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n)), st>>>(
-        g->d_off, g->d_nbr, n, w.bytes, w.ints, nullptr, d_out, csr ? 1 : 0);
+    set_flip_cta_smem_attr();
+    (csr ? k_one_flip_cta<true> : k_one_flip_cta<false>)<<<
+        count, kFlipCtaThreads,
+        static_cast<size_t>(csr ? flip_cta_smem_csr(n, 2 * g->m) : flip_cta_smem(n)), st>>>(
+        g->d_off, g->d_nbr, n, w.bytes, w.ints, nullptr, d_out);
     k_pack_bytes<<<ls_grid(int64_t(count) * W), 256, 0, st>>>(w.bytes, W, n, count, d_packed, nullptr);
     MQO_CUDA(cudaGetLastError());
     cudaFreeAsync(w.bytes, st);
