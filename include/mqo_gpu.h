@@ -274,14 +274,16 @@ int mqo_build_tables(mqo_batch* b, int32_t kind, int32_t count, const uint64_t* 
 
 /* ---- K7/K8 local search (localsearch.hpp:28-48) ---------------------------
  * Runs `op` on `count` packed bodies (host, [count][ceil(n/64)], updated in
- * place) on the batch's device, one warp per body, with the reference's
- * exact index-ordered first-improvement commits:
+ * place) on the batch's device (a CTA per body, or grid-wide rounds for one
+ * large body), with the reference's exact index-ordered first-improvement
+ * commits:
  *   MQO_LS_ONE_FLIP     one_flip_pass  (localsearch.cpp:139-157), out = gain
  *   MQO_LS_TWO_FLIP     two_flip_pass  (159-181),                 out = gain
  *   MQO_LS_ONE_TWO_FLIP one_two_flip   (183-190),                 out = gain
  *   MQO_LS_ONE_TWO_SWAP one_two_swap   (88-137),                  out = |I|
  * one_two_swap rejects a non-maximal or dependent input with
- * MQO_ERR_INVALID and the reference's message. */
+ * MQO_ERR_INVALID and the reference's message (the first offending body in
+ * order); `packed` and `out` are then left untouched. */
 enum { MQO_LS_ONE_FLIP = 0, MQO_LS_TWO_FLIP = 1, MQO_LS_ONE_TWO_FLIP = 2, MQO_LS_ONE_TWO_SWAP = 3 };
 int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_t* packed, int64_t* out);
 
