@@ -54,9 +54,9 @@ def main():
     Bb = a.batch
     rows = []
 
-    def emit(case, n, m, cpu_s, g1_s, gb_s, items=True):
+    def emit(case, n, m, cpu_s, g1_s, gb_s, items=True, batch=None):
         row = {"case": case, "n": n, "m": m, "ref_cpu_us": cpu_s * 1e6, "gpu_1_us": g1_s * 1e6,
-               "gpu_b_us_per_vector": gb_s * 1e6, "batch": Bb,
+               "gpu_b_us_per_vector": gb_s * 1e6, "batch": batch or Bb,
                "speedup_1": cpu_s / g1_s, "speedup_b": cpu_s / gb_s}
         if items:
             row.update(ref_items_per_s=m / cpu_s, gpu_b_items_per_s=m / gb_s)
@@ -138,7 +138,7 @@ def main():
         g1 = timeit(lambda: P.local_search(b1, _lib.LS_ONE_FLIP, pk[:1]))
         many = np.repeat(pk, 16, axis=0)
         gb = timeit(lambda: P.local_search(b1, _lib.LS_ONE_FLIP, many)) / len(many)
-        emit("one_flip_pass", n, og.m, cpu, g1, gb, items=False)
+        emit("one_flip_pass", n, og.m, cpu, g1, gb, items=False, batch=len(many))
 
     # BM_one_two_swap (d = 8, seed 5; from greedy_maximalize(g, {}))
     for n in (1 << 10, 1 << 12, 1 << 14):
@@ -150,7 +150,7 @@ def main():
         g1 = timeit(lambda: P.local_search(b1, _lib.LS_ONE_TWO_SWAP, pk))
         many = np.repeat(pk, 16, axis=0)
         gb = timeit(lambda: P.local_search(b1, _lib.LS_ONE_TWO_SWAP, many)) / len(many)
-        emit("one_two_swap", n, og.m, cpu, g1, gb, items=False)
+        emit("one_two_swap", n, og.m, cpu, g1, gb, items=False, batch=len(many))
 
     if a.out:
         with open(a.out, "w") as f:
