@@ -147,3 +147,20 @@ def test_swap_batch_input_check_leaves_caller_buffer(P):
         assert np.array_equal(pk, before)
     pk, out = P.local_search(b, _lib.LS_ONE_TWO_SWAP, P.pack_bodies(np.array([good, good], np.uint8)))
     assert out.tolist() == [4, 4]
+
+
+@pytest.mark.parametrize("n,d,bodies", [(1024, 16, 1), (8000, 16, 1), (16384, 16, 16), (4096, 8, 20)])
+def test_one_flip_cta_variants_vs_oracle(O, P, n, d, bodies):
+    # k_one_flip_cta with the CSR in shared memory (n = 1024, 4096) and read
+    # from global memory (ER(8000, d=16): 512 KB of rows; 16 bodies at 16384),
+    # one body per call and batched, against the oracle's one_flip_pass
+    from paper_2605_06921_b200 import _lib
+    og = O.generate_er(n, d / n, 3)
+    pg = P.generate(P.ErSpec(n, d / n), 3)
+    sides = np.random.default_rng(n + bodies).integers(0, 2, (bodies, n)).astype(np.uint8)
+    b = P.ChainBatch(pg, 1)
+    packed, gains = P.local_search(b, _lib.LS_ONE_FLIP, P.pack_bodies(sides))
+    got = P.unpack_bodies(packed, n)
+    for k in range(bodies):
+        ref_side, ref_gain = O.one_flip_pass(og, sides[k])
+        assert gains[k] == ref_gain and (got[k] == ref_side).all(), k
