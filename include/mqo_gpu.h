@@ -232,8 +232,9 @@ int mqo_batch_set_streams(mqo_batch* b, const mqo_rng_state* in);
 /* ---- K3 init_state (solver.cpp:30-46) ----------------------------------
  * x_b = Pi(d_base + N(0, sigma^2)) drawn from chain b's stream in vertex
  * order (Box-Muller, rng.hpp:49-62), replayed segment-parallel on the
- * device.  sigma == 0 draws nothing.  Box-Muller's log/sin/cos come from
- * CUDA's libm: within 1 ulp of glibc, not bit-identical. */
+ * device.  sigma == 0 draws nothing.  Box-Muller's log / sincos are device
+ * replays of the host glibc 2.39 routines the reference calls (__log_fma,
+ * __sincos_fma; csrc/glibc_math.cuh): bit-identical to init_state. */
 int mqo_init_states(mqo_batch* b, int32_t problem, double sigma);
 /* The init_constant path (solver.cpp:283-287): x = Pi(c 1), no draws. */
 int mqo_init_constant(mqo_batch* b, int32_t problem, double c);
@@ -288,10 +289,10 @@ enum { MQO_LS_ONE_FLIP = 0, MQO_LS_TWO_FLIP = 1, MQO_LS_ONE_TWO_FLIP = 2, MQO_LS
 int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_t* packed, int64_t* out);
 
 /* ---- the solver engine (solver.hpp:11-80, run_engine solver.cpp:192-372) -- */
-/* init_state noise source: EXACT replays Box-Muller on the host with the
- * process's libm (bit-identical to the reference's glibc draws); DEVICE
- * uses CUDA's log/sincos (within 1e-14 absolute, ~5% of values differ in
- * the last bit).  Both consume the streams identically. */
+/* init_state noise source.  Both values select the device kernel K3,
+ * which is bit-identical to the reference (glibc log / sincos replayed on
+ * the device); the field is kept for ABI compatibility with round-1
+ * callers (EXACT used to run Box-Muller on host threads). */
 enum { MQO_INIT_EXACT = 0, MQO_INIT_DEVICE = 1 };
 /* RunReport::warnings (solver.cpp:222,230,362), as bits in emission order. */
 enum { MQO_WARN_EDGELESS = 1, MQO_WARN_RESET_NOOP = 2, MQO_WARN_NO_SOLUTION = 4 };
@@ -317,7 +318,7 @@ typedef struct {
   int64_t stop_at_score;
   int32_t has_max_outer_loops;
   int32_t max_outer_loops;
-  int32_t init_mode; /* MQO_INIT_EXACT (default) | MQO_INIT_DEVICE */
+  int32_t init_mode; /* ignored: init is always the bit-exact device K3 */
 } mqo_solver_config;
 
 /* RunReport (solver.hpp:42-61); the best body goes to a separate buffer. */
@@ -347,6 +348,33 @@ typedef struct {
   int (*broadcast)(void* ctx, void* buf, size_t bytes, int32_t root);
 } mqo_comm;
 
+/* Native communicators, replacing the caller
+ * callbacks above for GPU runs.  NCCL is loaded at first use (dlopen of
+ * libnccl.so.2); its failures and a failed peer rank are MQO_ERR_NCCL with
+ * the message in mqo_last_error() (and, for a failed collective inside a
+ * callback, mqo_comm_last_error()).  Communicators are freed with
+ * mqo_comm_free.
+ *   mqo_nccl_unique_id     rank 0 creates the id; ship it to the other ranks
+ *                          out of band (torch.distributed, MPI, a file)
+ *   mqo_comm_nccl_create   one process per GPU: this process's rank
+ *   mqo_comm_create_devices  one process driving `ndev` distinct GPUs
+ *                          (ncclCommInitAll); out[ndev]
+ *   mqo_comm_create_local  `world` ranks that are host threads of this
+ *                          process, exchanging through host memory (ranks
+ *                          sharing one GPU, where NCCL refuses); out[world]
+ * Replaces: the reference's in-process parallel_for over chains
+ * (solver.cpp:78-106), whose results are thread-count independent
+ * (tests/test_solver.cpp:221-233). */
+#define MQO_NCCL_ID_BYTES 128
+int mqo_nccl_unique_id(uint8_t* id /* [MQO_NCCL_ID_BYTES] */);
+int mqo_comm_nccl_create(int32_t rank, int32_t world, const uint8_t* id, int32_t device,
+                         mqo_comm** out);
+int mqo_comm_create_devices(int32_t ndev, const int32_t* devices, mqo_comm** out);
+int mqo_comm_create_local(int32_t world, mqo_comm** out);
+int mqo_comm_free(mqo_comm* c);
+/* Message of the last failed native collective on this thread ("" if none). */
+const char* mqo_comm_last_error(void);
+
 /* solve_pooled (solver.hpp:80): runs the engine on `g`'s device.
  * best_body (may be NULL) receives the best solution as uint8[n]
  * (MIS indicator / MaxCut side).  With comm != NULL rank r owns chains
@@ -368,8 +396,24 @@ int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm*
 int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
                        mqo_run_report* report, uint8_t* best_body, int64_t* rank_scores);
 
-/* init_state on the host for one stream (the EXACT init path), usable on a
- * host-only graph: x[n] out, *st advanced like Rng. */
+/* One process, several GPUs: solve_pooled (mode MQO_SOLVE_POOLED, "Mode P":
+ * the report equals the single-GPU B-chain run) or the replica solve (mode
+ * MQO_SOLVE_REPLICAS, "Mode R") of `g` over `devices[ndev]`, one host thread
+ * per GPU.  Rank r runs on devices[r] with its own copy of the graph
+ * (uploaded from g's host CSR unless devices[r] is g's device) and chains
+ * [r*ceil(B/ndev), ...).  Distinct devices exchange over NCCL
+ * (ncclCommInitAll); repeated devices fall back to the in-process exchange
+ * (tests on one GPU).  rank_scores (may be NULL, MQO_SOLVE_REPLICAS only)
+ * receives every rank's best score.  A failure on any rank fails the call
+ * on every rank (the first rank's error is returned). */
+enum { MQO_SOLVE_POOLED = 0, MQO_SOLVE_REPLICAS = 1 };
+int mqo_solve_devices(mqo_graph* g, const mqo_solver_config* cfg, const int32_t* devices,
+                      int32_t ndev, int32_t mode, mqo_run_report* report, uint8_t* best_body,
+                      int64_t* rank_scores);
+
+/* init_state on the host for one stream with this process's libm, for
+ * host-only graphs (device < 0): x[n] out, *st advanced like Rng.  Graphs in
+ * HBM use mqo_init_states (the facade's init_state does). */
 int mqo_init_state_host(const mqo_graph* g, int32_t problem, double sigma, mqo_rng_state* st,
                         double* x);
 

@@ -155,6 +155,9 @@ class Lib:
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if hasattr(L, "orc_graph_from_csr"):  # oracle-c only (test helper)
+            L.orc_graph_from_csr.restype = C.c_int
+            L.orc_graph_from_csr.argtypes = [C.c_int32, _I64, _I32, C.POINTER(_P)]
         self.name = L.orc_impl_name().decode()
 
     # ---------------------------------------------------------------- errors
@@ -180,6 +183,12 @@ class Lib:
         u = np.ascontiguousarray(e[:, 0])
         v = np.ascontiguousarray(e[:, 1])
         return self._graph(self.L.orc_graph_from_edges, n, len(u), _ptr(u, _I32), _ptr(v, _I32))
+
+    def from_csr(self, n: int, off, nbr) -> "Graph":
+        """Wrap a canonical CSR (oracle-c test helper; no re-sort)."""
+        off = np.ascontiguousarray(off, np.int64)
+        nbr = np.ascontiguousarray(nbr, np.int32)
+        return self._graph(self.L.orc_graph_from_csr, n, _ptr(off, _I64), _ptr(nbr, _I32))
 
     def generate_er(self, n: int, p: float, seed: int) -> "Graph":
         return self._graph(self.L.orc_generate_er, n, p, seed)

@@ -240,6 +240,42 @@ int orc_graph_from_edges(int32_t n, int64_t ne, const int32_t* eu, const int32_t
   return graph_build(n, ne, keys, (graph_t**)out);
 }
 
+/* Test helper (not a reference function): wraps a CSR that is already in
+ * Graph's canonical form -- e.g. the device's O(m) ER generator output for
+ * C5, where re-sorting 8e7 edge pairs per test would dominate -- after the
+ * same invariant checks as Graph::check_invariants (graph.cpp:44-56) plus
+ * symmetry.  Reference-side equivalent: Graph::from_edges on the edge list. */
+int orc_graph_from_csr(int32_t n, const int64_t* off, const int32_t* nbr, void** out) {
+  if (n < 0) return fail(ORC_INVALID, "graph: negative vertex count");
+  graph_t* g = (graph_t*)xcalloc(1, sizeof *g);
+  g->n = n;
+  g->m = off[n] / 2;
+  g->off = (int64_t*)xmalloc(((size_t)n + 1) * sizeof(int64_t));
+  memcpy(g->off, off, ((size_t)n + 1) * sizeof(int64_t));
+  g->nbr = (int32_t*)xmalloc((size_t)off[n] * sizeof(int32_t) + 1);
+  memcpy(g->nbr, nbr, (size_t)off[n] * sizeof(int32_t));
+  g->max_degree = 0;
+  for (int32_t v = 0; v < n; ++v) {
+    if (deg(g, v) > g->max_degree) g->max_degree = deg(g, v);
+    for (int64_t e = g->off[v]; e < g->off[v + 1]; ++e) {
+      const int32_t u = g->nbr[e];
+      if (u < 0 || u >= n || u == v) return fail(ORC_LOGIC, "graph: bad neighbour");
+      if (e > g->off[v] && g->nbr[e - 1] >= u)
+        return fail(ORC_LOGIC, "graph: neighbor list not strictly ascending");
+      /* symmetry: v must appear in row u */
+      int64_t lo = g->off[u], hi = g->off[u + 1];
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (g->nbr[mid] < v) lo = mid + 1; else hi = mid;
+      }
+      if (lo == g->off[u + 1] || g->nbr[lo] != v) return fail(ORC_LOGIC, "graph: not symmetric");
+    }
+  }
+  if (off[n] % 2) return fail(ORC_LOGIC, "graph: degree sum != 2m");
+  *out = g;
+  return ORC_OK;
+}
+
 /* growable u64 key list for the generators */
 typedef struct {
   uint64_t* k;

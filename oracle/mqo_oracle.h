@@ -90,6 +90,8 @@ uint64_t orc_derive_seed(uint64_t master, uint64_t stream);
 /* --- Graph (graph.hpp) --- */
 int orc_graph_from_edges(int32_t n, int64_t ne, const int32_t* eu, const int32_t* ev,
                          void** out);
+/* oracle-c only (test helper): wrap an already canonical CSR */
+int orc_graph_from_csr(int32_t n, const int64_t* off, const int32_t* nbr, void** out);
 int orc_generate_er(int32_t n, double p, uint64_t seed, void** out);
 int orc_generate_ba(int32_t n, int32_t m_attach, uint64_t seed, void** out);
 int orc_generate_sbm(int32_t n, int32_t k, double p_in, double p_out, uint64_t seed,

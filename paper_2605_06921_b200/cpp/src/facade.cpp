@@ -511,8 +511,17 @@ RelaxedState init_state(Problem problem, const Graph& g, double sigma, Rng& rng)
   s.x.resize(g.n());
   const Rng::State st = rng.state();
   mqo_rng_state r{{st.s[0], st.s[1], st.s[2], st.s[3]}, st.spare, st.has_spare ? 1 : 0, 0};
-  check(mqo_init_state_host(g.handle(), problem == Problem::Mis ? MQO_PROBLEM_MIS : MQO_PROBLEM_MAXCUT,
-                            sigma, &r, s.x.data()));
+  const int32_t pr = problem == Problem::Mis ? MQO_PROBLEM_MIS : MQO_PROBLEM_MAXCUT;
+  if (g.n() == 0 || g.max_degree() < 1) {
+    // the reference's argument errors (solver.cpp:31-33), no draws
+    check(mqo_init_state_host(g.handle(), pr, sigma, &r, s.x.data()));
+  } else {  // K3 on the device: one chain, bit-identical to Rng::normal
+    Batch b(g, 1);
+    check(mqo_batch_set_streams(b.b, &r));
+    check(mqo_init_states(b.b, pr, sigma));
+    check(mqo_batch_get_x(b.b, s.x.data()));
+    check(mqo_batch_get_streams(b.b, &r));
+  }
   rng.set_state({{r.s[0], r.s[1], r.s[2], r.s[3]}, r.spare, r.has_spare != 0});
   return s;
 }

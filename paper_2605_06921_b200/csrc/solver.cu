@@ -19,6 +19,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "glibc_math.cuh"
 #include "jump.cuh"
 #include "rng.cuh"
 
@@ -88,6 +89,7 @@ __device__ __forceinline__ Xoshiro load_state(const ChainRng& r) {
 
 // ------------------------------------------------------------- K3 init
 // Thread (segment t, chain b): Box-Muller pairs [t*128, t*128+128) of the
+// (log / sincos: glibc_math.cuh, identical bits to the reference's libm calls)
 // chain's init section; warps span 32 consecutive chains so the writes of a
 // vertex row are coalesced.
 __global__ void k_init_normals(const int64_t* __restrict__ off, int32_t n, int32_t dmax,
@@ -130,10 +132,10 @@ __global__ void k_init_normals(const int64_t* __restrict__ off, int32_t n, int32
     const double u1 = u01_of(xoshiro_next(x));
     const double u2 = u01_of(xoshiro_next(x));
     if (u1 <= 0.0) rejected = true;  // rng.hpp:56 redraw -> exact replay
-    const double rad = sqrt(ex_mul(-2.0, log(u1)));
+    const double rad = __dsqrt_rn(ex_mul(-2.0, mqo_glibc::glibc_log(u1)));
     const double theta = ex_mul(kTwoPi, u2);
     double sn, cs;
-    sincos(theta, &sn, &cs);
+    mqo_glibc::glibc_sincos(theta, &sn, &cs);
     const int64_t v = s0 + 2 * p;
     const double first = ex_add(0.0, ex_mul(ex_mul(sigma, rad), cs));
     X[v * Bp + b] = clamp_box(ex_add(base_of(v), first), lo);
@@ -184,10 +186,10 @@ __global__ void k_init_sequential(const int64_t* __restrict__ off, int32_t n, in
       double u1 = u01_of(xoshiro_next(x));
       const double u2 = u01_of(xoshiro_next(x));
       while (u1 <= 0.0) u1 = u01_of(xoshiro_next(x));
-      const double rad = sqrt(ex_mul(-2.0, log(u1)));
+      const double rad = __dsqrt_rn(ex_mul(-2.0, mqo_glibc::glibc_log(u1)));
       const double theta = ex_mul(kTwoPi, u2);
       double sn, cs;
-      sincos(theta, &sn, &cs);
+      mqo_glibc::glibc_sincos(theta, &sn, &cs);
       r.spare = ex_mul(rad, sn);
       r.has_spare = 1;
       nv = ex_add(0.0, ex_mul(ex_mul(sigma, rad), cs));
@@ -575,7 +577,8 @@ void free_solver_buffers(mqo_batch* b) {
   cudaFree(b->d_counter);
 }
 
-// K3 on the device (CUDA libm log / sincos for Box-Muller).
+// K3 on the device; Box-Muller's log / sincos are the bit-exact replays of
+// the host glibc routines (glibc_math.cuh), so x matches init_state bit for bit.
 void init_states_device(mqo_batch* b, int32_t problem, double sigma) {
   mqo_graph* g = b->g;
   ensure_solver_buffers(b);

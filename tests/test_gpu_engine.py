@@ -137,19 +137,21 @@ def test_solver_kats(P):  # test_solver.cpp:120-165
     assert not r.found_solution and r.best_score == 0 and r.warnings
 
 
-def test_engine_device_init_mode(P):
-    """INIT_DEVICE runs the whole engine on CUDA libm normals: a valid,
-    reproducible run (bit-parity is the EXACT mode's contract)."""
+def test_engine_init_modes_identical(O, P):
+    """Both init_mode values run the bit-exact device K3 (no host path):
+    identical reports, equal to the oracle's solve_pooled."""
+    og = O.generate_er(1000, 0.01, 1)
     g = P.generate(P.ErSpec(1000, 0.01), 1)
-    cfg = P.SolverConfig(objective=P.MisQubo(2.0), optimizer=P.OptimizerConfig(0.8, 0.3),
-                         reset_fraction=0.7, reset_rounds=5, seed=1, time_budget_secs=60,
-                         max_outer_loops=1, pool_batch=8, pool_keep=4, init_mode=P.INIT_DEVICE)
-    a, b = P.solve_pooled(g, cfg), P.solve_pooled(g, cfg)
-    assert as_dict(a) == as_dict(b) and (a.best_body == b.best_body).all()
-    off, nbr = g.csr()
-    members = np.flatnonzero(a.best_body)
-    for v in members:  # independent
-        assert not a.best_body[nbr[off[v]:off[v + 1]]].any()
+    oc = oracle.Cfg(objective=MIS_QUBO, param=2.0, alpha=0.8, beta=0.3, reset_fraction=0.7,
+                    reset_rounds=5, seed=1, time_budget_secs=600, max_outer_loops=1,
+                    pool_batch=8, pool_keep=4)
+    ref, body = O.solve_pooled(og, oc.to_c())
+    for mode in (P.INIT_EXACT, P.INIT_DEVICE):
+        cfg = to_cfg(P, oc)
+        cfg.init_mode = mode
+        r = P.solve_pooled(g, cfg)
+        assert {k: ref[k] for k in KEYS} == as_dict(r)
+        assert (r.best_body == body).all()
 
 
 def test_engine_two_ranks_match_single(P, tmp_path):
