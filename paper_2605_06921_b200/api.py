@@ -32,7 +32,7 @@ __all__ = [
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
     "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
-    "solve_maxcut", "solve_replicas", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
+    "solve_maxcut", "solve_replicas", "solve_devices", "NativeComm", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
     "InvalidArgument", "LogicError", "MqoError", "ParseError", "DimacsResult", "parse_dimacs_text",
     "read_canonical", "write_canonical", "load_graph_file", "write_graph_file",
 ]
@@ -662,12 +662,81 @@ def _make_comm(comm) -> _Comm:
     return c
 
 
+class NativeComm:
+    """A communicator implemented inside libmqo_b200 (include/mqo_gpu.h):
+    NCCL over NVLink (one process per GPU: `NativeComm.nccl`), or the
+    in-process exchange for ranks that are threads of this process
+    (`NativeComm.local_group`).  Pass it as `comm=` to solve_pooled /
+    solve_replicas: the engine's collectives then run without Python."""
+
+    def __init__(self, ptr):
+        self._p = C.cast(ptr, C.POINTER(_Comm))
+        self.rank, self.world = self._p.contents.rank, self._p.contents.world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib.mqo_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, unique_id: bytes, device: int) -> "NativeComm":
+        out = C.c_void_p()
+        idb = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(lib.mqo_comm_nccl_create(rank, world, idb, device, C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def local_group(cls, world: int) -> list:
+        out = (C.c_void_p * world)()
+        check(lib.mqo_comm_create_local(world, out))
+        return [cls(out[i]) for i in range(world)]
+
+    def close(self):
+        if getattr(self, "_p", None) is not None:
+            lib.mqo_comm_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+lib.mqo_nccl_unique_id.argtypes = [C.c_void_p]
+lib.mqo_nccl_unique_id.restype = C.c_int
+lib.mqo_comm_nccl_create.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                     C.POINTER(C.c_void_p)]
+lib.mqo_comm_nccl_create.restype = C.c_int
+lib.mqo_comm_create_local.argtypes = [C.c_int32, C.c_void_p]
+lib.mqo_comm_create_local.restype = C.c_int
+lib.mqo_comm_create_devices.argtypes = [C.c_int32, _I32, C.c_void_p]
+lib.mqo_comm_create_devices.restype = C.c_int
+lib.mqo_comm_free.argtypes = [C.c_void_p]
+lib.mqo_comm_free.restype = C.c_int
+lib.mqo_comm_last_error.restype = C.c_char_p
+
+
+def _comm_arg(comm):
+    """(ctypes argument, keep-alive) for a NativeComm, a Python comm or None."""
+    if comm is None:
+        return None, None
+    if isinstance(comm, NativeComm):
+        return comm._p, comm
+    c = _make_comm(comm)
+    return C.byref(c), c
+
+
 lib.mqo_solve_pooled.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), C.POINTER(_Comm),
                                  C.POINTER(_RunReport), _U8]
 lib.mqo_solve_pooled.restype = C.c_int
 lib.mqo_solve_replicas.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), C.POINTER(_Comm),
                                    C.POINTER(_RunReport), _U8, _I64]
 lib.mqo_solve_replicas.restype = C.c_int
+lib.mqo_solve_devices.argtypes = [C.c_void_p, C.POINTER(_SolverCfg), _I32, C.c_int32, C.c_int32,
+                                  C.POINTER(_RunReport), _U8, _I64]
+lib.mqo_solve_devices.restype = C.c_int
 lib.mqo_init_state_host.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_void_p, _D]
 lib.mqo_init_state_host.restype = C.c_int
 
@@ -739,9 +808,9 @@ def solve_pooled(g: Graph, cfg: SolverConfig, comm=None) -> RunReport:
     adapter; chains are then sharded over the ranks."""
     rep = _RunReport()
     body = np.zeros(max(g.n(), 1), np.uint8)
-    c = _make_comm(comm) if comm is not None else None  # kept alive for the call
-    check(lib.mqo_solve_pooled(g._h, C.byref(cfg.to_c()), C.byref(c) if c else None,
-                               C.byref(rep), _ptr(body, _U8)))
+    arg, keep = _comm_arg(comm)  # kept alive for the call
+    check(lib.mqo_solve_pooled(g._h, C.byref(cfg.to_c()), arg, C.byref(rep), _ptr(body, _U8)))
+    del keep
     return _report(rep, body, g)
 
 
@@ -752,12 +821,29 @@ def solve_replicas(g: Graph, cfg: SolverConfig, comm=None):
     best scores)."""
     rep = _RunReport()
     body = np.zeros(max(g.n(), 1), np.uint8)
-    c = _make_comm(comm) if comm is not None else None
+    arg, keep = _comm_arg(comm)
     world = comm.world if comm is not None else 1
     scores = np.zeros(world, np.int64)
-    check(lib.mqo_solve_replicas(g._h, C.byref(cfg.to_c()), C.byref(c) if c else None,
-                                 C.byref(rep), _ptr(body, _U8), _ptr(scores, _I64)))
+    check(lib.mqo_solve_replicas(g._h, C.byref(cfg.to_c()), arg, C.byref(rep), _ptr(body, _U8),
+                                 _ptr(scores, _I64)))
+    del keep
     return _report(rep, body, g), scores
+
+
+def solve_devices(g: Graph, cfg: SolverConfig, devices, mode: str = "pooled"):
+    """One process, several GPUs (include/mqo_gpu.h mqo_solve_devices): rank
+    r runs chains [r*ceil(B/N), ...) on devices[r] in its own host thread;
+    "pooled" (Mode P) equals the single-GPU run, "replicas" (Mode R) ends
+    with one argmax all-reduce.  Distinct devices exchange over NCCL.
+    Returns (RunReport, per-rank best scores or None)."""
+    devs = np.ascontiguousarray(devices, np.int32)
+    m = {"pooled": 0, "replicas": 1}[mode]
+    rep = _RunReport()
+    body = np.zeros(max(g.n(), 1), np.uint8)
+    scores = np.zeros(len(devs), np.int64)
+    check(lib.mqo_solve_devices(g._h, C.byref(cfg.to_c()), _ptr(devs, _I32), len(devs), m,
+                                C.byref(rep), _ptr(body, _U8), _ptr(scores, _I64)))
+    return _report(rep, body, g), (scores if m == 1 else None)
 
 
 def _report(rep, body, g) -> "RunReport":

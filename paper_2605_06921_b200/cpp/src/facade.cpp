@@ -76,6 +76,24 @@ struct Batch {
   Batch& operator=(const Batch&) = delete;
 };
 
+// MQO_DEVICES: comma-separated device ids for the multi-GPU engine (empty
+// or one id: the single-GPU path on the graph's device).
+std::vector<int32_t> devices_from_env() {
+  std::vector<int32_t> out;
+  const char* e = std::getenv("MQO_DEVICES");
+  if (!e) return out;
+  std::string s(e), tok;
+  for (size_t i = 0; i <= s.size(); ++i) {
+    if (i == s.size() || s[i] == ',') {
+      if (!tok.empty()) out.push_back(static_cast<int32_t>(std::stoi(tok)));
+      tok.clear();
+    } else if (s[i] != ' ') {
+      tok += s[i];
+    }
+  }
+  return out;
+}
+
 int64_t words(Vertex n) { return (static_cast<int64_t>(n) + 63) / 64; }
 
 std::vector<uint64_t> pack(const std::vector<uint8_t>& bytes) {
@@ -581,7 +599,16 @@ RunReport run_engine(const Graph& g, const SolverConfig& cfg) {
   if (g.n() == 0) throw std::invalid_argument("solver: empty graph");
   mqo_run_report r{};
   std::vector<uint8_t> body(g.n());
-  check(mqo_solve_pooled(g.handle(), &c, nullptr, &r, body.data()));
+  // MQO_DEVICES="0,1,...,7": shard the B chains over those GPUs of this
+  // process (mqo_solve_devices, NCCL over NVLink); the report is the same
+  // as the single-GPU run (Mode P).
+  std::vector<int32_t> devs = devices_from_env();
+  if (static_cast<int>(devs.size()) > c.pool_batch) devs.resize(c.pool_batch);  // >= 1 chain per rank
+  if (devs.size() > 1)
+    check(mqo_solve_devices(g.handle(), &c, devs.data(), static_cast<int32_t>(devs.size()),
+                            MQO_SOLVE_POOLED, &r, body.data(), nullptr));
+  else
+    check(mqo_solve_pooled(g.handle(), &c, nullptr, &r, body.data()));
   RunReport rep;
   rep.config = cfg;
   rep.found_solution = r.found_solution != 0;

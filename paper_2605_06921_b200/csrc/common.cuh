@@ -48,6 +48,17 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// A failed collective (NCCL or a caller's mqo_comm callback) or a peer rank
+// that failed: MQO_ERR_NCCL at the ABI.
+struct CommError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// Raised on the healthy ranks when a peer rank failed (the failed rank
+// rethrows its own error).
+struct PeerFailed : CommError {
+  using CommError::CommError;
+};
+
 #define MQO_CUDA(expr)                                                           \
   do {                                                                           \
     cudaError_t _e = (expr);                                                     \
@@ -74,6 +85,9 @@ int guard(F&& f) {
   } catch (const CudaError& e) {
     set_error(e.what());
     return MQO_ERR_CUDA;
+  } catch (const CommError& e) {
+    set_error(e.what());
+    return MQO_ERR_NCCL;
   } catch (const std::exception& e) {
     set_error(e.what());
     return MQO_ERR_OTHER;

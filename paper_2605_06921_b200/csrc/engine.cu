@@ -17,6 +17,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
+#include <exception>
 #include <thread>
 
 #include "common.cuh"
@@ -37,9 +39,9 @@ void upload_chain_major(mqo_batch* b, const double* host, double* dst);
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
                          int64_t* d_out, cudaStream_t st, int32_t* d_bad = nullptr);
 
-// init_state (solver.cpp:30-46) on the host with this process's libm, so the
-// Box-Muller draws are bit-identical to the reference's (glibc log/sin/cos
-// are not reproducible on the device).  Consumes `st` exactly like Rng.
+// init_state (solver.cpp:30-46) on the host with this process's libm, for
+// host-only graphs (mqo_init_state_host).  The engine and device graphs use
+// K3 (init_states_device).  Consumes `st` exactly like Rng.
 void host_init_state(const int64_t* off, int32_t n, int32_t dmax, int32_t problem, double sigma,
                      mqo_rng_state& st, double* x) {
   Xoshiro r{{st.s[0], st.s[1], st.s[2], st.s[3]}};
@@ -142,6 +144,13 @@ void validate(const mqo_solver_config& c) {  // solver.cpp:14-28
     throw std::invalid_argument("solver: max_outer_loops must be >= 1");
 }
 
+// Message of the last failed collective on this thread (set by the native
+// communicators in comm.cu; empty for caller-supplied callbacks).
+std::string comm_error_text() {
+  const char* m = mqo_comm_last_error();
+  return m && *m ? std::string(m) : std::string("callback returned an error");
+}
+
 // Communicator wrapper (single process when comm == nullptr).
 struct Comm {
   const mqo_comm* c;
@@ -153,13 +162,13 @@ struct Comm {
       return;
     }
     if (c->allgather(c->ctx, send, recv, bytes) != 0)
-      throw std::runtime_error("mqo_comm.allgather failed");
+      throw CommError("mqo_comm.allgather failed: " + comm_error_text());
   }
   void allreduce_max(uint64_t* data, size_t count) const {
     if (world() == 1) return;
     if (c->allreduce_max_u64) {
       if (c->allreduce_max_u64(c->ctx, data, count) != 0)
-        throw std::runtime_error("mqo_comm.allreduce_max_u64 failed");
+        throw CommError("mqo_comm.allreduce_max_u64 failed: " + comm_error_text());
       return;
     }
     std::vector<uint64_t> all(count * world());
@@ -171,7 +180,7 @@ struct Comm {
     if (world() == 1) return;
     if (c->broadcast) {
       if (c->broadcast(c->ctx, buf, bytes, root) != 0)
-        throw std::runtime_error("mqo_comm.broadcast failed");
+        throw CommError("mqo_comm.broadcast failed: " + comm_error_text());
       return;
     }
     std::vector<uint8_t> all(bytes * world());
@@ -189,6 +198,7 @@ struct Engine {
   int64_t W;
   int B_global, B_local, first_chain;
   int chain_offset = 0;  // single-process engines: first global chain (Mode R shards)
+  int rank_id = -1;      // Mode R: the outer rank of this shard engine
   uint64_t* stage = nullptr;  // pinned staging for local-search bodies
   size_t stage_words = 0;
   ~Engine() {
@@ -206,51 +216,63 @@ struct Engine {
   std::vector<int64_t> g_scores;
   std::vector<int32_t> g_valid, g_iters, g_stops;
 
+  // Failure handling across ranks.  Local device work of a rank runs
+  // through local(): an exception is parked in `pending` instead of leaving
+  // the engine, the rank skips further local work but still joins the next
+  // collective with an error flag, and every rank then throws at the same
+  // point -- a failure on one rank can never leave its peers blocked in a
+  // collective.  Single-process engines rethrow immediately.
+  std::exception_ptr pending;
+  const int fault_rank = [] {
+    const char* e = std::getenv("MQO_FAULT_RANK");
+    return e && *e ? std::atoi(e) : -1;
+  }();
+  template <typename F>
+  void local(F&& f) {
+    if (pending) return;
+    try {
+      f();
+    } catch (...) {
+      if (comm.world() == 1) throw;
+      pending = std::current_exception();
+    }
+  }
+  void raise_if(bool any_failed) {
+    if (!any_failed) return;
+    if (pending) std::rethrow_exception(pending);
+    throw PeerFailed("mqo: a peer rank failed; the collective solve was aborted on every rank");
+  }
+
   // Deadline decisions are collective: any rank past the deadline stops
   // every rank at the same point, so the ranks' merge sequences never
-  // diverge (each decision is one tiny all-gather).
-  bool past_deadline() const {
-    const uint8_t mine = mono_now() >= deadline ? 1 : 0;
+  // diverge (each decision is one tiny all-gather, which also carries the
+  // error flag).
+  bool past_deadline() {
+    const uint8_t mine = (mono_now() >= deadline ? 1 : 0) | (pending ? 2 : 0);
     if (comm.world() == 1) return mine != 0;
     std::vector<uint8_t> all(comm.world());
     comm.allgather(&mine, all.data(), 1);
-    for (uint8_t a : all)
-      if (a) return true;
-    return false;
+    bool past = false, failed = false;
+    for (uint8_t a : all) {
+      past |= (a & 1) != 0;
+      failed |= (a & 2) != 0;
+    }
+    raise_if(failed);
+    return past;
   }
   bool target_hit() const {
     return have_best && cfg.has_stop_at_score && best.score >= cfg.stop_at_score;
   }
 
+  // Phase-1 init (solver.cpp:283-289): init_constant or init_state, both
+  // on the device; the Box-Muller noise replays the reference's glibc
+  // log / sincos bit for bit (glibc_math.cuh), so there is no host path.
   void init_phase() {
     if (cfg.has_init_constant) {
       init_states_constant(batch, problem, cfg.init_constant);
       return;
     }
-    if (cfg.init_mode == MQO_INIT_DEVICE || !(cfg.init_noise > 0.0)) {
-      init_states_device(batch, problem, cfg.init_noise);
-      return;
-    }
-    // exact replay: host Box-Muller with the reference's libm
-    std::vector<mqo_rng_state> st(B_local);
-    if (mqo_batch_get_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
-    MQO_TRACE("init: streams read");
-    std::vector<double> x(static_cast<size_t>(B_local) * n);
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int threads = static_cast<int>(std::min<unsigned>(hw, static_cast<unsigned>(B_local)));
-    std::vector<std::thread> pool_t;
-    for (int t = 0; t < threads; ++t)
-      pool_t.emplace_back([&, t] {
-        for (int c = t; c < B_local; c += threads)
-          host_init_state(g->h_off.data(), n, g->max_degree, problem, cfg.init_noise, st[c],
-                          x.data() + static_cast<size_t>(c) * n);
-      });
-    for (auto& th : pool_t) th.join();
-    MQO_TRACE("init: host normals done (%d threads)", threads);
-    upload_chain_major(batch, x.data(), batch->d_x[batch->cur]);
-    MQO_TRACE("init: uploaded");
-    if (mqo_batch_set_streams(batch, st.data()) != MQO_OK) throw CudaError(mqo_last_error());
-    MQO_TRACE("init: streams written");
+    init_states_device(batch, problem, cfg.init_noise);
   }
 
   void trajectories() {
@@ -264,26 +286,34 @@ struct Engine {
   // bodies of the candidates that can touch the pool, then merges
   // (solver.cpp:252-275).
   void harvest_and_merge(bool count_resets) {
-    harvest_device(batch, problem);
     std::vector<int32_t> iters(B_local), stops(B_local), dep(B_local);
     std::vector<int64_t> scores(B_local);
-    read_outcomes(batch, iters.data(), stops.data());
-    MQO_CUDA(cudaMemcpyAsync(scores.data(), batch->d_scores, sizeof(int64_t) * B_local,
-                             cudaMemcpyDeviceToHost, batch->stream));
-    MQO_CUDA(cudaMemcpyAsync(dep.data(), batch->d_valid, sizeof(int32_t) * B_local,
-                             cudaMemcpyDeviceToHost, batch->stream));
-    MQO_CUDA(cudaStreamSynchronize(batch->stream));
-    // record = {score, valid, iters, stop} for every local chain, padded
+    local([&] {
+      harvest_device(batch, problem);
+      read_outcomes(batch, iters.data(), stops.data());
+      MQO_CUDA(cudaMemcpyAsync(scores.data(), batch->d_scores, sizeof(int64_t) * B_local,
+                               cudaMemcpyDeviceToHost, batch->stream));
+      MQO_CUDA(cudaMemcpyAsync(dep.data(), batch->d_valid, sizeof(int32_t) * B_local,
+                               cudaMemcpyDeviceToHost, batch->stream));
+      MQO_CUDA(cudaStreamSynchronize(batch->stream));
+    });
+    // record = {score, valid, iters, stop} for every local chain, padded,
+    // after one header word carrying this rank's error flag
     const int world = comm.world();
     const int per = (B_global + world - 1) / world;
-    std::vector<int64_t> rec(static_cast<size_t>(per) * 4, 0), all(rec.size() * world);
-    for (int i = 0; i < B_local; ++i) {
-      rec[4 * i] = scores[i];
-      rec[4 * i + 1] = problem == MQO_PROBLEM_MIS ? (dep[i] ? 0 : 1) : 1;
-      rec[4 * i + 2] = iters[i];
-      rec[4 * i + 3] = stops[i];
+    const size_t stride = static_cast<size_t>(per) * 4 + 1;
+    std::vector<int64_t> rec(stride, 0), all(rec.size() * world);
+    rec[0] = pending ? 1 : 0;
+    for (int i = 0; i < B_local && !pending; ++i) {
+      rec[1 + 4 * i] = scores[i];
+      rec[1 + 4 * i + 1] = problem == MQO_PROBLEM_MIS ? (dep[i] ? 0 : 1) : 1;
+      rec[1 + 4 * i + 2] = iters[i];
+      rec[1 + 4 * i + 3] = stops[i];
     }
     comm.allgather(rec.data(), all.data(), rec.size() * sizeof(int64_t));
+    bool failed = false;
+    for (int r = 0; r < world; ++r) failed |= all[r * stride] != 0;
+    raise_if(failed);
     g_scores.assign(B_global, 0);
     g_valid.assign(B_global, 0);
     g_iters.assign(B_global, 0);
@@ -292,7 +322,7 @@ struct Engine {
       for (int i = 0; i < per; ++i) {
         const int b = r * per + i;
         if (b >= B_global) break;
-        const int64_t* q = all.data() + (static_cast<size_t>(r) * per + i) * 4;
+        const int64_t* q = all.data() + static_cast<size_t>(r) * stride + 1 + static_cast<size_t>(i) * 4;
         g_scores[b] = q[0];
         g_valid[b] = static_cast<int32_t>(q[1]);
         g_iters[b] = static_cast<int32_t>(q[2]);
@@ -418,18 +448,23 @@ struct Engine {
     const int count = static_cast<int>(members.size());
     std::vector<Entry> mine;
     for (int i = rank; i < count; i += world) mine.push_back(members[i]);
-    polish(mine);
+    local([&] { polish(mine); });
     const int per = (count + world - 1) / world;
     const size_t rec = 1 + static_cast<size_t>(W);  // score + body words
-    std::vector<uint64_t> send(per * rec, 0), recv(send.size() * world);
-    for (size_t k = 0; k < mine.size(); ++k) {
-      send[k * rec] = static_cast<uint64_t>(mine[k].score);
-      std::copy(mine[k].body.begin(), mine[k].body.end(), send.begin() + k * rec + 1);
+    const size_t stride = 1 + static_cast<size_t>(per) * rec;  // error flag + records
+    std::vector<uint64_t> send(stride, 0), recv(send.size() * world);
+    send[0] = pending ? 1 : 0;
+    for (size_t k = 0; k < mine.size() && !pending; ++k) {
+      send[1 + k * rec] = static_cast<uint64_t>(mine[k].score);
+      std::copy(mine[k].body.begin(), mine[k].body.end(), send.begin() + 1 + k * rec + 1);
     }
     comm.allgather(send.data(), recv.data(), send.size() * sizeof(uint64_t));
+    bool failed = false;
+    for (int r = 0; r < world; ++r) failed |= recv[r * stride] != 0;
+    raise_if(failed);
     for (int i = 0; i < count; ++i) {
       const int r = i % world, k = i / world;
-      const uint64_t* src = recv.data() + (static_cast<size_t>(r) * per + k) * rec;
+      const uint64_t* src = recv.data() + static_cast<size_t>(r) * stride + 1 + static_cast<size_t>(k) * rec;
       members[i].score = static_cast<int64_t>(src[0]);
       members[i].body.assign(src + 1, src + rec);
     }
@@ -467,14 +502,16 @@ struct Engine {
     first_chain = std::min(B_global, rank * per);
     B_local = std::max(0, std::min(B_global, first_chain + per) - first_chain);
     if (B_local < 1) throw std::invalid_argument("solver: more ranks than chains");
-    if (mqo_batch_create(g, B_local, &batch) != MQO_OK) throw CudaError(mqo_last_error());
     try {
-      if (mqo_batch_seed_streams(batch, cfg.seed,
-                                 1 + static_cast<uint64_t>(first_chain + chain_offset)) != MQO_OK)
-        throw CudaError(mqo_last_error());
+      local([&] {
+        if (mqo_batch_create(g, B_local, &batch) != MQO_OK) throw CudaError(mqo_last_error());
+        if (mqo_batch_seed_streams(batch, cfg.seed,
+                                   1 + static_cast<uint64_t>(first_chain + chain_offset)) != MQO_OK)
+          throw CudaError(mqo_last_error());
+      });
       loop();
     } catch (...) {
-      mqo_batch_free(batch);
+      if (batch) mqo_batch_free(batch);
       batch = nullptr;
       throw;
     }
@@ -490,19 +527,25 @@ struct Engine {
       if (cfg.has_max_outer_loops && rep.outer_loops >= cfg.max_outer_loops) break;
       // Phase 1 (solver.cpp:280-296)
       MQO_TRACE("outer %d: init", rep.outer_loops);
-      init_phase();
-      MQO_TRACE("outer %d: trajectories", rep.outer_loops);
-      trajectories();
+      local([&] {
+        init_phase();
+        MQO_TRACE("outer %d: trajectories", rep.outer_loops);
+        trajectories();
+      });
       MQO_TRACE("outer %d: harvest", rep.outer_loops);
       harvest_and_merge(false);
       // Phase 2 (298-312)
       for (int round = 0; round < cfg.reset_rounds; ++round) {
         if (past_deadline() || target_hit() || pool.e.empty()) break;
         MQO_TRACE("round %d: reset", round);
-        upload_pool();
-        reset_from_pool(batch, problem, cfg.reset_fraction);
-        MQO_TRACE("round %d: trajectories", round);
-        trajectories();
+        local([&] {
+          if (fault_rank == (rank_id >= 0 ? rank_id : comm.rank()))  // MQO_FAULT_RANK (tests)
+            throw std::runtime_error("injected fault on rank " + std::to_string(fault_rank));
+          upload_pool();
+          reset_from_pool(batch, problem, cfg.reset_fraction);
+          MQO_TRACE("round %d: trajectories", round);
+          trajectories();
+        });
         MQO_TRACE("round %d: harvest", round);
         harvest_and_merge(true);
       }
@@ -552,9 +595,10 @@ struct Engine {
 
 }  // namespace
 
-extern "C" int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
-                                mqo_run_report* report, uint8_t* best_body) {
-  return guard([&] {
+namespace {
+
+void solve_pooled_impl(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                       mqo_run_report* report, uint8_t* best_body) {
     if (!g || !cfg || !report) throw std::invalid_argument("mqo_solve_pooled: null argument");
     if (g->device >= 0) MQO_CUDA(cudaSetDevice(g->device));
     Engine e;
@@ -567,13 +611,10 @@ extern "C" int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, cons
       for (int32_t v = 0; v < g->n; ++v)
         best_body[v] = e.best.body.empty() ? 0 : (e.best.body[v >> 6] >> (63 - (v & 63))) & 1;
     }
-  });
 }
 
-extern "C" int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
-                                  mqo_run_report* report, uint8_t* best_body,
-                                  int64_t* rank_scores) {
-  return guard([&] {
+void solve_replicas_impl(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                         mqo_run_report* report, uint8_t* best_body, int64_t* rank_scores) {
     if (!g || !cfg || !report) throw std::invalid_argument("mqo_solve_replicas: null argument");
     if (g->device >= 0) MQO_CUDA(cudaSetDevice(g->device));
     const Comm cm{comm};
@@ -589,12 +630,26 @@ extern "C" int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, co
     e.cfg.pool_batch = local;
     e.comm = Comm{nullptr};
     e.chain_offset = first;
-    e.run();
+    e.rank_id = rank;
+    // a local failure still joins the all-reduce (error word), so no peer
+    // is left waiting; then every rank throws
+    std::exception_ptr failure;
+    try {
+      e.run();
+    } catch (...) {
+      if (world == 1) throw;
+      failure = std::current_exception();
+    }
     // the one exchange: argmax over ranks (a single tiny all-reduce)
-    const int64_t sc = e.rep.found_solution ? e.best.score : -1;
-    uint64_t key = (static_cast<uint64_t>(sc + 1) << 16) | static_cast<uint64_t>(0xFFFF - rank);
-    cm.allreduce_max(&key, 1);
-    const int winner = 0xFFFF - static_cast<int>(key & 0xFFFF);
+    const int64_t sc = !failure && e.rep.found_solution ? e.best.score : -1;
+    uint64_t key[2] = {(static_cast<uint64_t>(sc + 1) << 16) | static_cast<uint64_t>(0xFFFF - rank),
+                       failure ? 1ull : 0ull};
+    cm.allreduce_max(key, 2);
+    if (key[1]) {
+      if (failure) std::rethrow_exception(failure);
+      throw PeerFailed("mqo: a peer rank failed; the replica solve was aborted on every rank");
+    }
+    const int winner = 0xFFFF - static_cast<int>(key[0] & 0xFFFF);
     // counters: the winner's report, sums / maxima over ranks
     mqo_run_report mine = e.rep;
     std::vector<mqo_run_report> all(world);
@@ -625,6 +680,101 @@ extern "C" int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, co
     *report = r;
     if (best_body)
       for (int32_t v = 0; v < g->n; ++v) best_body[v] = (body[v >> 6] >> (63 - (v & 63))) & 1;
+}
+
+}  // namespace
+
+extern "C" int mqo_solve_pooled(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                                mqo_run_report* report, uint8_t* best_body) {
+  return guard([&] { solve_pooled_impl(g, cfg, comm, report, best_body); });
+}
+
+extern "C" int mqo_solve_replicas(mqo_graph* g, const mqo_solver_config* cfg, const mqo_comm* comm,
+                                  mqo_run_report* report, uint8_t* best_body,
+                                  int64_t* rank_scores) {
+  return guard([&] { solve_replicas_impl(g, cfg, comm, report, best_body, rank_scores); });
+}
+
+extern "C" int mqo_solve_devices(mqo_graph* g, const mqo_solver_config* cfg, const int32_t* devices,
+                                 int32_t ndev, int32_t mode, mqo_run_report* report,
+                                 uint8_t* best_body, int64_t* rank_scores) {
+  return guard([&] {
+    if (!g || !cfg || !report || !devices || ndev < 1)
+      throw std::invalid_argument("mqo_solve_devices: bad argument");
+    if (mode != MQO_SOLVE_POOLED && mode != MQO_SOLVE_REPLICAS)
+      throw std::invalid_argument("mqo_solve_devices: unknown mode");
+    validate(*cfg);
+    if (ndev > cfg->pool_batch) throw std::invalid_argument("solver: more ranks than chains");
+    if (ndev == 1 && devices[0] == g->device) {
+      if (mode == MQO_SOLVE_POOLED) return solve_pooled_impl(g, cfg, nullptr, report, best_body);
+      return solve_replicas_impl(g, cfg, nullptr, report, best_body, rank_scores);
+    }
+    bool distinct = true;
+    for (int i = 0; i < ndev; ++i)
+      for (int j = 0; j < i; ++j) distinct &= devices[i] != devices[j];
+    // per-rank graphs: g itself on its own device, else a copy of its CSR
+    std::vector<mqo_graph*> graphs(ndev, nullptr), owned;
+    std::vector<mqo_comm*> comms(ndev, nullptr);
+    auto cleanup = [&] {
+      for (mqo_comm* c : comms)
+        if (c) mqo_comm_free(c);
+      for (mqo_graph* q : owned) mqo_graph_free(q);
+    };
+    try {
+      for (int r = 0; r < ndev; ++r) {
+        if (devices[r] == g->device) {
+          graphs[r] = g;
+          continue;
+        }
+        for (int q = 0; q < r && !graphs[r]; ++q)
+          if (devices[q] == devices[r]) graphs[r] = graphs[q];
+        if (graphs[r]) continue;
+        mqo_graph* copy = nullptr;
+        if (mqo_graph_upload(g->n, g->h_off.data(), g->h_nbr.data(), devices[r], &copy) != MQO_OK)
+          throw CudaError(mqo_last_error());
+        owned.push_back(copy);
+        graphs[r] = copy;
+      }
+      const int rc = distinct ? mqo_comm_create_devices(ndev, devices, comms.data())
+                              : mqo_comm_create_local(ndev, comms.data());
+      if (rc != MQO_OK) throw CommError(mqo_last_error());
+      std::vector<std::exception_ptr> errors(ndev);
+      std::vector<mqo_run_report> reports(ndev);
+      std::vector<std::thread> threads;
+      for (int r = 0; r < ndev; ++r)
+        threads.emplace_back([&, r] {
+          try {
+            MQO_CUDA(cudaSetDevice(devices[r]));
+            if (mode == MQO_SOLVE_POOLED)
+              solve_pooled_impl(graphs[r], cfg, comms[r], &reports[r], r == 0 ? best_body : nullptr);
+            else
+              solve_replicas_impl(graphs[r], cfg, comms[r], &reports[r],
+                                  r == 0 ? best_body : nullptr, r == 0 ? rank_scores : nullptr);
+          } catch (...) {
+            errors[r] = std::current_exception();
+          }
+        });
+      for (auto& t : threads) t.join();
+      // the failing rank's own error, not a peer's "a peer rank failed"
+      std::exception_ptr first;
+      for (auto& e : errors) {
+        if (!e) continue;
+        try {
+          std::rethrow_exception(e);
+        } catch (const PeerFailed&) {
+          if (!first) first = e;
+        } catch (...) {
+          std::rethrow_exception(e);
+        }
+      }
+      if (first) std::rethrow_exception(first);
+      *report = reports[0];
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+    if (g->device >= 0) MQO_CUDA(cudaSetDevice(g->device));
   });
 }
 

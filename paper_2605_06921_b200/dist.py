@@ -63,6 +63,23 @@ class TorchComm:
         return t.cpu().numpy().tobytes()
 
 
+def nccl_comm(device: int | None = None, group=None):
+    """The library's native NCCL communicator (include/mqo_gpu.h
+    mqo_comm_nccl_create) for this torch.distributed rank: rank 0 creates
+    the unique id, torch.distributed ships it to the others; afterwards the
+    engine's collectives run inside libmqo_b200 without Python."""
+    import torch
+    import torch.distributed as dist
+    from .api import NativeComm
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [NativeComm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    if device is None:
+        device = torch.cuda.current_device()
+    return NativeComm.nccl(rank, world, box[0], device)
+
+
 def shard(b_global: int, world: int, rank: int) -> range:
     """Chains owned by `rank` (contiguous blocks of ceil(B/world)), the same
     split the engine uses."""
