@@ -208,6 +208,7 @@ extern "C" int mqo_batch_stream(const mqo_batch* b, void** stream) {
 extern "C" int mqo_batch_sync(mqo_batch* b) {
   return guard([&] {
     if (!b) throw std::invalid_argument("mqo_batch_sync: null batch");
+    MQO_CUDA(cudaSetDevice(b->g->device));
     MQO_CUDA(cudaStreamSynchronize(b->stream));
   });
 }
@@ -247,6 +248,7 @@ extern "C" int mqo_batch_get_v(mqo_batch* b, double* v) {
 extern "C" int mqo_batch_zero_v(mqo_batch* b) {
   return guard([&] {
     if (!b) throw std::invalid_argument("mqo_batch_zero_v: null batch");
+    MQO_CUDA(cudaSetDevice(b->g->device));
     MQO_CUDA(cudaMemsetAsync(b->d_v, 0, sizeof(double) * int64_t(b->g->n) * b->Bp, b->stream));
   });
 }

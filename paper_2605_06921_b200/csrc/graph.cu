@@ -67,6 +67,27 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
       }
       max_degree = std::max<int32_t>(max_degree, static_cast<int32_t>(e - b));
     }
+    // Symmetry (u in N(v) <=> v in N(u)), which from_edges guarantees and
+    // the local-search kernels rely on, in O(m): rows are sorted, so the
+    // lower entries of row u are exactly the v < u whose rows hold u, met in
+    // ascending v when the rows are walked in order.
+    {
+      std::vector<int64_t> low(static_cast<size_t>(n), 0);  // lower entries of row u matched so far
+      for (int32_t v = 0; v < n; ++v)
+        for (int64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
+          const int32_t u = neighbors[i];
+          if (u < v) continue;
+          const int64_t at = offsets[u] + low[u];
+          if (at >= offsets[u + 1] || neighbors[at] != v)
+            throw std::logic_error("graph: adjacency not symmetric");
+          ++low[u];
+        }
+      for (int32_t u = 0; u < n; ++u) {
+        const int64_t b = offsets[u], e = offsets[u + 1];
+        if (low[u] != (std::lower_bound(neighbors + b, neighbors + e, u) - (neighbors + b)))
+          throw std::logic_error("graph: adjacency not symmetric");
+      }
+    }
     auto* g = new mqo_graph;
     g->device = device;
     g->n = n;

@@ -338,11 +338,20 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   if (threadIdx.x == 0) gains[s] = total;
 }
 
+// Once per device (the attribute is per device and context; setting it to
+// the cap on every call cost two driver calls per one_flip_pass).
 void set_flip_cta_smem_attr() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  MQO_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && done[dev]) return;
   MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kFlipCtaSmemMax)));
   MQO_CUDA(cudaFuncSetAttribute(k_one_flip_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kFlipCtaSmemMax)));
+  if (dev < 64) done[dev] = true;
 }
 
 // ---- host-driven 2-flip sweeps (localsearch.cpp:159-181) --------------
@@ -1395,8 +1404,46 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   cudaFreeAsync(d_cand, st);
 }
 
-// d_bad (one_two_swap only, may be null): when given, the input check of
-// k_tight is left in d_bad[count] (bit 0 not independent, bit 1 not maximal)
+// Scratch of the (1,2)-swap kernels: dirty flags, the dirty list(s) and the
+// freed-neighbour buffer per body.
+void alloc_swap_lists(const mqo_graph* g, int32_t count, LsWork& w, cudaStream_t st,
+                      bool second_list = false) {
+  const int64_t n = g->n, cells = std::max<int64_t>(1, int64_t(count) * n);
+  MQO_CUDA(cudaMallocAsync(&w.dflag, int64_t(count) * (n + 4), st));
+  MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
+  MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
+  if (second_list) MQO_CUDA(cudaMallocAsync(&w.dlist2, sizeof(int32_t) * cells, st));
+  MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
+}
+
+// k_mis_swap_cta (a CTA of 16 warps per body, CSR + state staged in SMEM
+// when they fit) on bodies whose tightness is in w.ints; d_bad (may be
+// null) marks bodies the input check rejected, which are skipped.
+void launch_swap_cta(const mqo_graph* g, int32_t count, LsWork& w, int64_t* d_out,
+                     cudaStream_t st, int32_t* d_bad) {
+  alloc_swap_lists(g, count, w, st, true);
+  const int64_t cbytes = swap_cta_smem_bytes(g->n, 2 * g->m, g->max_degree);
+  const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
+  {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    int dev = 0;
+    MQO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 64 || !done[dev]) {
+      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSwapSmemMax - 1024)));
+      if (dev < 64) done[dev] = true;
+    }
+  }
+  k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
+      g->d_off, g->d_nbr, g->n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
+      w.small, g->max_degree, d_out, csm ? 1 : 0, d_bad);
+  MQO_CUDA(cudaGetLastError());
+}
+
+// d_bad (one_two_swap only, may be null, zeroed by the caller): when given,
+// the input check of k_tight is left in d_bad[count] (bit 0 not independent, bit 1 not maximal)
 // for the caller to raise after its copy-out, instead of a host round trip
 // here; flagged bodies are left untouched.
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
@@ -1453,22 +1500,11 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     }
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
   } else if (d_bad && g_swap_cta) {
-    MQO_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t) * count, st));
+    // the input check stays on the device: k_tight flags bad bodies in
+    // d_bad (zeroed by the caller), which the swap kernel then leaves untouched
     k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, d_bad);
     MQO_CUDA(cudaGetLastError());
-    MQO_CUDA(cudaMallocAsync(&w.dflag, int64_t(count) * (n + 4), st));
-    MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
-    MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
-    MQO_CUDA(cudaMallocAsync(&w.dlist2, sizeof(int32_t) * cells, st));
-    MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
-    const int64_t cbytes = swap_cta_smem_bytes(n, 2 * g->m, g->max_degree);
-    const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
-    MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSwapSmemMax - 1024)));
-    k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
-        g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
-        w.small, g->max_degree, d_out, csm ? 1 : 0, d_bad);
-    MQO_CUDA(cudaGetLastError());
+    launch_swap_cta(g, count, w, d_out, st, d_bad);
     MQO_CUDA(cudaMemsetAsync(d_out, 0, sizeof(int64_t) * count, st));
   } else {
     k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.small);
@@ -1493,10 +1529,6 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
       }
     }
     MQO_CUDA(cudaMemsetAsync(w.small, 0, sizeof(int32_t) * count, st));
-    MQO_CUDA(cudaMallocAsync(&w.dflag, int64_t(count) * (n + 4), st));
-    MQO_CUDA(cudaMemsetAsync(w.dflag, 0, int64_t(count) * (n + 4), st));
-    MQO_CUDA(cudaMallocAsync(&w.dlist, sizeof(int32_t) * cells, st));
-    MQO_CUDA(cudaMallocAsync(&w.freed, sizeof(int32_t) * int64_t(count) * (g->max_degree + 1), st));
     cudaEvent_t ev[2] = {nullptr, nullptr};
     if (trace_on()) {
       cudaEventCreate(&ev[0]);
@@ -1505,22 +1537,17 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
     }
     const int64_t sbytes = swap_smem_bytes(n, 2 * g->m, g->max_degree);
     const bool smem = sbytes <= kSwapSmemMax && g_swap_smem;
-    const int64_t cbytes = swap_cta_smem_bytes(n, 2 * g->m, g->max_degree);
     if (g_swap_cta) {  // a CTA of 16 warps per body
-      const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
-      MQO_CUDA(cudaMallocAsync(&w.dlist2, sizeof(int32_t) * cells, st));
-      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kSwapSmemMax - 1024)));
-      k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
-          g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
-          w.small, g->max_degree, d_out, csm ? 1 : 0, nullptr);
+      launch_swap_cta(g, count, w, d_out, st, nullptr);
     } else if (smem) {
+      alloc_swap_lists(g, count, w, st);
       MQO_CUDA(cudaFuncSetAttribute(k_mis_swap, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSwapSmemMax)));
       k_mis_swap<<<count, 256, static_cast<size_t>(sbytes), st>>>(
           g->d_off, g->d_nbr, n, count, w.bytes, w.ints, w.dflag, w.dlist, w.freed, w.small,
           g->max_degree, d_out, 1);
     } else {
+      alloc_swap_lists(g, count, w, st);
       k_mis_swap<<<blocks, 32 * kLsWarps, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints,
                                                    w.dflag, w.dlist, w.freed, w.small,
                                                    g->max_degree, d_out, 0);
