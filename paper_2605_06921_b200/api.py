@@ -32,7 +32,7 @@ __all__ = [
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
     "pack_bodies", "unpack_bodies", "local_search", "one_flip_pass", "two_flip_pass",
     "one_two_flip", "one_two_swap", "SolverConfig", "RunReport", "solve_pooled", "solve_mis",
-    "solve_maxcut", "solve_replicas", "solve_devices", "NativeComm", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
+    "solve_maxcut", "solve_replicas", "solve_devices", "NativeComm", "tune", "init_state_host", "INIT_EXACT", "INIT_DEVICE", "PROBLEM_MIS", "PROBLEM_MAXCUT",
     "InvalidArgument", "LogicError", "MqoError", "ParseError", "DimacsResult", "parse_dimacs_text",
     "read_canonical", "write_canonical", "load_graph_file", "write_graph_file",
 ]
@@ -799,6 +799,12 @@ class RunReport:  # solver.hpp:48-61
     last_trajectory_stop: int
     elapsed_secs: float
     warnings: list
+
+
+def tune(key: str, value: float) -> None:
+    """Measurement knobs of the kernels (include/mqo_gpu.h mqo_tune): e.g.
+    "heavy_deg", "persistent_cells", "cta_traj", "group_quads"."""
+    check(lib.mqo_tune(key.encode(), float(value)))
 
 
 def solve_pooled(g: Graph, cfg: SolverConfig, comm=None) -> RunReport:

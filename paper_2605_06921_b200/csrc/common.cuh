@@ -162,6 +162,7 @@ struct mqo_graph {
   std::vector<int32_t> h_cta_rows, h_cta_base;  // per-slice rows / ELL base (host copy)
   std::vector<int64_t> h_off;
   std::vector<int32_t> h_nbr;
+  std::vector<int32_t> h_deg_ge;  // [max_degree + 2]: rows of degree >= d (heavy-row planning)
   std::mutex lazy_mu;  // guards the lazily built fields (d_cta, d_hmax): a graph may be
                        // shared by solves running on several host threads
 };

@@ -110,6 +110,9 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
       for (int32_t v = 0; v < n; ++v)
         order[count[max_degree - (offsets[v + 1] - offsets[v])]++] = v;
     }
+    g->h_deg_ge.assign(static_cast<size_t>(max_degree) + 2, 0);
+    for (int32_t v = 0; v < n; ++v) ++g->h_deg_ge[static_cast<size_t>(offsets[v + 1] - offsets[v])];
+    for (int64_t d = max_degree; d >= 0; --d) g->h_deg_ge[d] += g->h_deg_ge[d + 1];
     if (device < 0) {  // host-only graph: CSR kept for host-side users, no HBM copy
       *out = g;
       return;

@@ -75,9 +75,15 @@ struct PassArgs {
   int32_t is_mis;
   int32_t hot_rows;          // gathers of rows < hot_rows are kept in L2 (evict_last)
   int32_t q0, Qg;            // this launch's chain group: quads [q0, q0 + Qg) of Q
-  int32_t gblocks;           // > 0: groups fused in one launch, gblocks CTAs each
   uint8_t* qmask;            // [Q] active-chain mask per quad (per-launch path)
   int32_t cpl;
+  // Heavy rows (see heavy_row): order[0, heavy) are staged through SMEM by
+  // whole CTAs -- the first hblocks CTAs of every chain group -- and the
+  // per-lane path walks rows [heavy, n) with the lblocks CTAs after them.
+  int32_t heavy;             // rows of degree >= the heavy threshold (a prefix of order)
+  int32_t hblocks, lblocks;  // CTAs per chain group for heavy / light rows (lblocks 0: rest)
+  int32_t stage_doubles;     // SMEM staging capacity (doubles) of a heavy CTA
+  int32_t stage_off;         // byte offset of the staging buffer in dynamic SMEM
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -283,18 +289,36 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
 
 // Walks this thread's (row, quad) units for one pass.  Thread -> quad is
 // fixed for the whole launch so per-chain accumulators live in registers.
+// CTA roles of a launch.  Fused chain groups: CTAs [g*S, (g+1)*S) sweep
+// group g, S = hblocks + lblocks.  The block scheduler dispatches CTAs in
+// index order, so the groups still run one after another (one L2-sized X
+// slice live at a time, two at the seams) without a launch boundary -- and
+// its tail -- between them; within a group the heavy-row CTAs (longest
+// work) are dispatched first.
+struct Role {
+  bool heavy;
+  int index, count;  // this CTA's index among the group's heavy / light CTAs, and their count
+  int32_t qbase;     // first quad of the group
+};
+__device__ __forceinline__ Role cta_role(const PassArgs& a) {
+  const int S = a.lblocks > 0 ? a.hblocks + a.lblocks : static_cast<int>(gridDim.x);
+  const int grp = blockIdx.x / S, local = blockIdx.x % S;
+  Role r;
+  r.qbase = a.q0 + grp * a.Qg;
+  r.heavy = local < a.hblocks;
+  r.index = r.heavy ? local : local - a.hblocks;
+  r.count = r.heavy ? a.hblocks : S - a.hblocks;
+  return r;
+}
+
 template <int KIND, int CPL, int MODE, bool CHECK, class TU>
 __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, double* Xo,
                                           const uint8_t* qmask, bool write, Acc<CPL>& acc,
-                                          int32_t& my_q) {
+                                          int32_t& my_q, const Role& role) {
   const int lane = threadIdx.x & 31;
-  // Fused chain groups: CTAs [g*gblocks, (g+1)*gblocks) sweep group g.  The
-  // block scheduler dispatches CTAs in index order, so the groups still run
-  // one after another (one L2-sized X slice live at a time, two at the
-  // seams) without a launch boundary -- and its tail -- between them.
-  const int vblock = a.gblocks > 0 ? blockIdx.x % a.gblocks : blockIdx.x;
-  const int vgrid = a.gblocks > 0 ? a.gblocks : gridDim.x;
-  const int32_t qbase = a.q0 + (a.gblocks > 0 ? (blockIdx.x / a.gblocks) * a.Qg : 0);
+  const int vblock = role.index;
+  const int vgrid = role.count;
+  const int32_t qbase = role.qbase;
   const int gwarp = (vblock * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (vgrid * blockDim.x) >> 5;
   int32_t q, r0, rstep;
@@ -320,8 +344,155 @@ __device__ __forceinline__ void pass_rows(const PassArgs& a, const double* X, do
     amask = real >= CPL ? (1u << CPL) - 1u : (real > 0 ? (1u << real) - 1u : 0u);
   }
   if (!amask) return;
-  for (int32_t r = r0; r < a.n; r += rstep)
+  for (int32_t r = a.heavy + r0; r < a.n; r += rstep)
     row_unit<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, __ldg(a.order + r), col, amask, write, acc);
+}
+
+// ---------------------------------------------------------- heavy rows
+// A lane-per-(row, quad) gather walks a row as one chain of dependent
+// round trips (index load, then U neighbour loads): deg/U of them, ~1 us
+// each -- 0.8 ms for the 3350-neighbour hub of BA(1e6,5), a floor under
+// every pass however few chains run (measured: 0.82 ms/step at 4 chains,
+// profiles/r11_smallb_c4.jsonl).  Rows of degree >= the heavy threshold
+// are instead staged by a whole CTA: every thread issues cp.async copies
+// of the row's neighbour values (coalesced per neighbour) into one SMEM
+// half while one thread per chain sums the other half in CSR order -- the
+// same fp64 additions in the same order, so results stay bit-identical --
+// and the epilogue is the per-lane path's, one chain per thread.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kHeavyCols = 4;  // chains per thread in a heavy row (ncol <= 4 * kThreads)
+
+// Stage neighbours [e, e + cnt) of the row: cnt x ncol doubles at dst.
+__device__ __forceinline__ void heavy_issue(const PassArgs& a, const double* X, int64_t e,
+                                            int cnt, int32_t col0, int ncol, bool pairs,
+                                            double* dst) {
+  if (pairs) {
+    const int half = ncol >> 1, total = cnt * half;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int j = t / half, c2 = t - j * half;
+      const int32_t u = __ldg(a.nbr + e + j);
+      cp_async16(dst + j * ncol + 2 * c2, X + static_cast<int64_t>(u) * a.Bp + col0 + 2 * c2);
+    }
+  } else {
+    const int total = cnt * ncol;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int j = t / ncol, c = t - j * ncol;
+      const int32_t u = __ldg(a.nbr + e + j);
+      cp_async8(dst + j * ncol + c, X + static_cast<int64_t>(u) * a.Bp + col0 + c);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int KIND, int CPL, int MODE, bool CHECK, class TU>
+__device__ void heavy_row(const PassArgs& a, const double* X, double* Xo, int32_t v, int32_t col0,
+                          int ncol, const uint8_t* qmask, bool write, uint32_t* viol_sink,
+                          double* stage) {
+  const int64_t e0 = __ldg(a.off + v), e1 = __ldg(a.off + v + 1);
+  const int nb = max(1, (a.stage_doubles >> 1) / ncol);  // neighbours per SMEM half
+  double* const half1 = stage + nb * ncol;
+  const bool pairs = (ncol & 1) == 0 && (a.Bp & 1) == 0;
+  const int64_t rowbase = static_cast<int64_t>(v) * a.Bp + col0;
+  double s[kHeavyCols], xv[kHeavyCols];
+  unsigned nbsel = 0;
+#pragma unroll
+  for (int k = 0; k < kHeavyCols; ++k) {
+    s[k] = 0.0;
+    const int c = threadIdx.x + k * blockDim.x;
+    xv[k] = c < ncol ? __ldcg(X + rowbase + c) : 0.0;
+  }
+  if (e1 > e0) heavy_issue(a, X, e0, static_cast<int>(e1 - e0 < nb ? e1 - e0 : nb), col0, ncol, pairs,
+                           stage);
+  int k = 0;
+  for (int64_t e = e0; e < e1; e += nb, ++k) {
+    const int cnt = static_cast<int>(e1 - e < nb ? e1 - e : nb);
+    if (e + nb < e1) {  // next chunk into the other half while this one is summed
+      heavy_issue(a, X, e + nb, static_cast<int>(e1 - e - nb < nb ? e1 - e - nb : nb), col0, ncol, pairs,
+                  (k & 1) ? stage : half1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* h = (k & 1) ? half1 : stage;
+#pragma unroll
+    for (int q = 0; q < kHeavyCols; ++q) {
+      const int c = threadIdx.x + q * blockDim.x;
+      if (c >= ncol) break;
+      double acc = s[q];
+      for (int j = 0; j < cnt; ++j) {
+        const double val = h[j * ncol + c];
+        if constexpr (KIND == MQO_LAPLACIAN)
+          acc = ex_add(acc, ex_sub(xv[q], val));  // graph.cpp:85
+        else
+          acc = ex_add(acc, val);                 // graph.cpp:68
+        if constexpr (CHECK) nbsel |= (val > 0.5 ? 1u : 0u) << q;
+      }
+      s[q] = acc;
+    }
+    __syncthreads();  // this half may be refilled by the next issue
+  }
+  const double deg = static_cast<double>(e1 - e0);
+#pragma unroll
+  for (int q = 0; q < kHeavyCols; ++q) {
+    const int c = threadIdx.x + q * blockDim.x;
+    if (c >= ncol) break;
+    const int32_t b = col0 + c;
+    const bool active = qmask ? ((qmask[b / CPL] >> (b % CPL)) & 1u) != 0 : b < a.B;
+    if (!active) continue;
+    if constexpr (CHECK) {  // pga.cpp:125-133 on binarize(x)
+      const bool sel = xv[q] > 0.5;
+      const bool any = (nbsel >> q) & 1u;
+      if (sel ? any : !any) {
+        if constexpr (MODE == kCheck)
+          atomicOr(viol_sink + b, 1u);
+        else
+          viol_sink[b] = 1u;
+      }
+      if constexpr (MODE == kCheck)
+        if (xv[q] != 0.0 && xv[q] != 1.0) atomicOr(reinterpret_cast<unsigned*>(a.flag + 1), 1u);
+    }
+    if constexpr (MODE == kCheck) continue;
+    const double g = grad_epi<KIND>(s[q], xv[q], deg, a.param);
+    if constexpr (MODE == kGrad) {
+      __stcg(a.gout + rowbase + c, g);
+      continue;
+    }
+    if (!write) continue;
+    // pga.cpp:82-85: v = beta v + g ; next = clamp(x + alpha v)
+    const double vv = ex_add(ex_mul(a.beta, __ldcg(a.v + rowbase + c)), g);
+    const double xn = clamp_box(ex_add(xv[q], ex_mul(a.alpha, vv)), a.lo);
+    if constexpr (MODE == kTraj && !CHECK)  // pga.cpp:86, 99-102
+      if (fabs(ex_sub(xn, xv[q])) > a.conv_tol) viol_sink[b] = 1u;
+    __stcg(a.v + rowbase + c, vv);
+    __stcg(Xo + rowbase + c, xn);
+  }
+}
+
+// The heavy-row CTAs of a group: rows role.index, role.index + count, ...
+template <int KIND, int CPL, int MODE, bool CHECK, class TU>
+__device__ __forceinline__ void heavy_rows(const PassArgs& a, const double* X, double* Xo,
+                                           const uint8_t* qmask, bool write, uint32_t* viol_sink,
+                                           const Role& role) {
+  extern __shared__ __align__(16) unsigned char heavy_smem[];
+  double* stage = reinterpret_cast<double*>(heavy_smem + a.stage_off);
+  const int32_t col0 = role.qbase * CPL;
+  const int ncol = min(a.Qg * CPL, a.B - col0);
+  if (ncol <= 0) return;
+  for (int32_t r = role.index; r < a.heavy; r += role.count)
+    heavy_row<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, __ldg(a.order + r), col0, ncol, qmask, write,
+                                          viol_sink, stage);
 }
 
 // Folds thread accumulators into shared per-chain slots.
@@ -345,7 +516,12 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_pass(PassArgs a) {
   // kStep must not read rows another unit already updated, so it writes the
   // other buffer; the host flips `cur` afterwards.
   if constexpr (MODE == kStep) Xo = a.x[a.base ^ 1];
-  pass_rows<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, nullptr, true, acc, q);
+  const Role role = cta_role(a);
+  if (role.heavy) {
+    heavy_rows<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, nullptr, true, a.viol, role);
+    return;
+  }
+  pass_rows<KIND, CPL, MODE, CHECK, TU>(a, X, Xo, nullptr, true, acc, q, role);
   if constexpr (CHECK) {
     if (acc.viol) {
 #pragma unroll
@@ -395,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
     const bool write = !MIS || p <= a.T;  // pass T+1 is check-only (MIS)
     Acc<CPL> acc;
     int32_t q = 0;
-    pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q);
+    pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, s_qmask, write, acc, q, cta_role(a));
     fold_to_smem<CPL>(acc, q, s_viol);
     __syncthreads();
     for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
@@ -469,8 +645,13 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   const bool write = !MIS || p <= a.T;
   Acc<CPL> acc;
   int32_t q = 0;
-  pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, a.qmask, write, acc, q);
-  fold_to_smem<CPL>(acc, q, s_viol);
+  const Role role = cta_role(a);
+  if (role.heavy) {
+    heavy_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, a.qmask, write, s_viol, role);
+  } else {
+    pass_rows<KIND, CPL, kTraj, MIS, TU>(a, X, Xo, a.qmask, write, acc, q, role);
+    fold_to_smem<CPL>(acc, q, s_viol);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < a.Bp; b += blockDim.x) {
     if (!s_viol[b]) continue;
@@ -781,23 +962,68 @@ PassArgs make_args(mqo_batch* b, const mqo_objective& obj) {
   return a;
 }
 
-// One pass over every chain group: a single launch of Q/Qg x `blocks` CTAs
-// (MQO_FUSE_GROUPS=0: one launch per group, the earlier form).
+// Heavy rows (heavy_row): the degree threshold of the SMEM-staged path.
+// 0 = automatic: rows whose per-lane critical path -- deg/U dependent
+// round trips of ~1 us -- would exceed half the pass's bandwidth time at
+// the measured HBM rate, and at least 64; < 0 = off.  At 128 chains on
+// BA(1e6,5) the threshold exceeds every degree (the bench kernel is
+// unchanged); at 16 chains rows of degree >= ~570 are staged.
+int g_heavy_deg = [] {
+  const char* e = std::getenv("MQO_HEAVY_DEG");
+  return e ? std::atoi(e) : 0;
+}();
+constexpr int kStageDoubles = 4096;  // 32 KB of SMEM staging per heavy CTA
+
+struct HeavyPlan {
+  int32_t heavy = 0, hblocks = 0;
+  size_t smem = 0;  // dynamic SMEM bytes to add
+};
+HeavyPlan heavy_plan(const mqo_batch* b, int Qg, size_t base_smem) {
+  HeavyPlan h;
+  const mqo_graph* g = b->g;
+  const int64_t ncol = std::min<int64_t>(int64_t(Qg) * b->cpl, b->B);
+  if (g_heavy_deg < 0 || ncol > int64_t(kHeavyCols) * kThreads || g->h_deg_ge.empty()) return h;
+  int64_t thr = g_heavy_deg;
+  if (thr == 0) {
+    const double nnz = 2.0 * static_cast<double>(g->m);
+    const double bytes = 8.0 * (g->n + 1) + 4.0 * nnz + ncol * (8.0 * nnz + 32.0 * g->n);
+    const double pass_us = bytes / 6.5e6;  // ~6.5 TB/s
+    const int U = b->cpl == 4 ? 4 : 16;
+    thr = std::max<int64_t>(64, static_cast<int64_t>(U * pass_us / 2.0));
+  }
+  if (thr > g->max_degree) return h;
+  h.heavy = g->h_deg_ge[static_cast<size_t>(thr)];
+  if (h.heavy <= 0) return h;
+  h.hblocks = std::min<int32_t>(h.heavy, 2 * sm_count(g->device));
+  h.smem = ((base_smem + 15) / 16) * 16 - base_smem + sizeof(double) * kStageDoubles;
+  return h;
+}
+
+// One pass over every chain group: a single launch of Q/Qg groups x
+// (hblocks heavy-row + `blocks` light-row) CTAs (MQO_FUSE_GROUPS=0: one
+// launch per group, the earlier form).
 bool g_fuse_groups = [] {
   const char* e = std::getenv("MQO_FUSE_GROUPS");
   return !(e && *e == '0');
 }();
 template <class F>
 void launch_groups(const mqo_batch* b, PassArgs& a, int blocks, size_t smem, F fn) {
+  const HeavyPlan hp = heavy_plan(b, a.Qg, smem);
+  a.heavy = hp.heavy;
+  a.hblocks = hp.hblocks;
+  a.lblocks = blocks;
+  a.stage_doubles = kStageDoubles;
+  a.stage_off = static_cast<int32_t>((smem + 15) / 16 * 16);
+  const size_t total_smem = smem + hp.smem;
+  const int per_group = hp.hblocks + blocks;
   if (g_fuse_groups && a.Qg < b->Q) {
     a.q0 = 0;
-    a.gblocks = blocks;
-    fn<<<blocks * (b->Q / a.Qg), kThreads, smem, b->stream>>>(a);
-    a.gblocks = 0;
-    return;
+    fn<<<per_group * (b->Q / a.Qg), kThreads, total_smem, b->stream>>>(a);
+  } else {
+    for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<per_group, kThreads, total_smem, b->stream>>>(a);
+    a.q0 = 0;
   }
-  for (a.q0 = 0; a.q0 < b->Q; a.q0 += a.Qg) fn<<<blocks, kThreads, smem, b->stream>>>(a);
-  a.q0 = 0;
+  a.heavy = a.hblocks = a.lblocks = 0;
 }
 
 // Problems up to this many (vertex, chain) cells run the persistent kernel.
@@ -961,7 +1187,8 @@ void read_outcomes(mqo_batch* b, int32_t* iterations, int32_t* reasons) {
 
 // Tuning knobs of the fused kernels (measurement scripts only):
 //   "k1_variant"  K1 Tune<> instantiation (0 = default), "hot_frac"
-//   fraction of L2 reserved (evict_last) for hot-row gathers.
+//   fraction of L2 reserved (evict_last) for hot-row gathers, "heavy_deg"
+//   degree threshold of the SMEM-staged heavy rows (0 auto, < 0 off).
 extern "C" int mqo_tune(const char* key, double value) {
   return guard([&] {
     const std::string k = key ? key : "";
@@ -981,6 +1208,8 @@ extern "C" int mqo_tune(const char* key, double value) {
       g_group_quads = static_cast<int>(value);
     else if (k == "grid_per_sm")
       g_grid_per_sm = std::max(0, static_cast<int>(value));
+    else if (k == "heavy_deg")
+      g_heavy_deg = static_cast<int>(value);
     else
       throw std::invalid_argument("mqo_tune: unknown key");
   });
