@@ -47,6 +47,14 @@ const int g_scan_cta = [] {
   return e ? std::atoi(e) : 16;
 }();
 
+// MQO_SCAN_MULTI=0: the 2-flip sweep commits one move per step
+// (k_two_scan_cta) instead of every independent move of a window
+// (k_two_scan_multi)
+const bool g_scan_multi = [] {
+  const char* e = std::getenv("MQO_SCAN_MULTI");
+  return !(e && *e == '0');
+}();
+
 __device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 1; }
 
 // ---------------------------------------------------------------- MaxCut
@@ -681,6 +689,319 @@ __global__ void __launch_bounds__(32 * kScanWarps)
   }
 }
 
+// ---- 2-flip sweep with many commits per step ---------------------------
+// The reference scan (localsearch.cpp:159-181) visits v ascending and, for
+// each u in N(v), u > v, on the other side with delta_v + delta_u + 2 > 0,
+// flips both at once and carries on along v's row with the new state.  What
+// the decision at vertex w reads is R(w) = {w} U {u in N(w): u > w} (side
+// and delta of each); a joint flip of v with partners F changes sides in
+// {v} U F and deltas in C = {v} U F U N(v) U N(F), so it can change the
+// decision at w only if R(w) meets C, i.e. w in C or w a lower neighbour of
+// some y in C.  Let m(v) be the smallest such w above v.
+//
+// A CTA per body takes K marked vertices at a time and every warp
+// simulates whole rows of its candidates against the current state --
+// including the row's later hits after v has flipped (delta of a later u
+// shifts by +-2 for every flip of v and of each partner adjacent to u) --
+// and computes m(v) for rows with a hit.  The sequential scan would then
+// reach candidate k in exactly the state the snapshot shows as long as
+// c_k < M = min m over the hits committed before it; so every hit below M
+// is committed in one step (their flipped sets are pairwise non-adjacent,
+// the shared neighbours' delta updates commute), and the next step starts
+// at M (or after the window).  Commits, their order and the gain are the
+// reference's; what changes is that a step commits every independent hit of
+// the window instead of one.
+constexpr int kMultiMaxFlips = 8;  // partners simulated per row and step
+
+// first index in the sorted row [b, e) holding a value > x
+__device__ __forceinline__ int64_t row_upper(const int32_t* __restrict__ nbr, int64_t b,
+                                             int64_t e, int32_t x) {
+  while (b < e) {
+    const int64_t mid = (b + e) >> 1;
+    if (nbr[mid] <= x) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+__device__ __forceinline__ bool row_has(const int32_t* __restrict__ nbr, int64_t b, int64_t e,
+                                        int32_t x) {
+  const int64_t i = row_upper(nbr, b, e, x - 1);
+  return i < e && nbr[i] == x;
+}
+
+// min over y in {t} U N(t), y > v, of y and of the smallest lower neighbour
+// w of y with v < w < y (this lane's share; the caller reduces).  A smaller
+// value is always safe (the step just stops earlier), so rows longer than
+// kMultiScanRow -- hubs, whose 2-hop walk would stall the whole step --
+// answer v + 1.
+constexpr int64_t kMultiScanRow = 256;
+__device__ __forceinline__ int32_t affected_min(const int64_t* __restrict__ off,
+                                                const int32_t* __restrict__ nbr, int32_t t,
+                                                int32_t v, int lane) {
+  int32_t m = INT_MAX;
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  if (e1 - e0 > kMultiScanRow) return v + 1;
+  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+    const int32_t y = a < e0 ? t : nbr[a];
+    if (y <= v) continue;
+    m = min(m, y);
+    const int64_t yb = off[y], ye = off[y + 1];
+    const int64_t i = row_upper(nbr, yb, ye, v);
+    if (i < ye && nbr[i] < y) m = min(m, nbr[i]);
+  }
+  return m;
+}
+
+template <int NW, int C>
+__global__ void __launch_bounds__(32 * NW)
+    k_two_scan_multi(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                     const int32_t* __restrict__ hmax, int32_t n, int32_t count,
+                     uint8_t* side_all, int32_t* delta_all, uint8_t* cand_all, int32_t* live,
+                     int64_t* gains) {
+  constexpr int K = NW * C;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = blockIdx.x;
+  if (s >= count || !live[s]) return;
+  uint8_t* side = side_all + static_cast<int64_t>(s) * n;
+  int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
+  uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
+  __shared__ int32_t c_v[K];
+  __shared__ int64_t c_e[K];                 // row start (resumed rows: after the last flip)
+  __shared__ int32_t r_m[K], r_gain[K], r_nf[K];
+  __shared__ int64_t r_resume[K];            // >= 0: row not finished (too many flips)
+  __shared__ int32_t r_part[K][kMultiMaxFlips];
+  __shared__ uint8_t r_commit[K];
+  __shared__ int32_t s_k, s_pos, s_span;
+  __shared__ int64_t s_epos;
+  __shared__ long long s_total;
+  // per-warp simulation scratch: partner rows [pb, pe) and sides after flip
+  __shared__ int64_t w_pb[NW][kMultiMaxFlips], w_pe[NW][kMultiMaxFlips];
+  __shared__ uint8_t w_pside[NW][kMultiMaxFlips];
+  if (threadIdx.x == 0) {
+    s_pos = 0;
+    s_epos = -1;
+    s_total = 0;
+  }
+  __syncthreads();
+  for (;;) {
+    // A. the next K marked vertices from s_pos (warp 0); s_span = last
+    // position examined
+    if (warp == 0) {
+      int k = 0;
+      int32_t from = s_pos;
+      if (s_epos >= 0) {  // resume the current vertex's row
+        if (lane == 0) {
+          c_v[0] = s_pos;
+          c_e[0] = s_epos;
+        }
+        k = 1;
+        from = s_pos + 1;
+      }
+      int32_t span = n - 1;
+      for (int32_t cb = from; cb < n && k < K; cb += 32) {
+        if (((cb - from) & 511) == 0) {  // empty 512-mark stretches cost one round trip
+          bool any16 = false;
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int32_t q = cb + 16 * lane + t;
+            any16 |= q < n && *reinterpret_cast<const volatile uint8_t*>(cand + q) != 0;
+          }
+          if (!__any_sync(0xffffffffu, any16)) {
+            cb += 512 - 32;
+            continue;
+          }
+        }
+        const bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
+        unsigned mask = __ballot_sync(0xffffffffu, f);
+        while (mask && k < K) {
+          const int i = warp_first(mask);
+          if (lane == 0) {
+            c_v[k] = cb + i;
+            c_e[k] = -1;
+          }
+          ++k;
+          mask &= mask - 1;
+          if (k == K) span = cb + i;
+        }
+      }
+      if (lane == 0) {
+        s_k = k;
+        s_span = span;
+      }
+    }
+    __syncthreads();
+    const int Kc = s_k;
+    if (Kc == 0) break;
+    // B. simulate each candidate's row against the current state (read only)
+    for (int k = warp; k < Kc; k += NW) {
+      const int32_t v = c_v[k];
+      const int64_t e1 = off[v + 1];
+      const bool resumed = c_e[k] >= 0;
+      int64_t e = resumed ? c_e[k] : off[v];
+      int32_t dv = delta[v];
+      uint8_t sv = side[v];
+      int nf = 0, flips_v = 0;
+      int32_t gain = 0;
+      int32_t* part = r_part[k];  // partners (SMEM: indexed at run time)
+      int64_t resume = -1;
+      if (!resumed && dv + hmax[v] + 2 <= 0) e = e1;  // delta_u <= hmax[v]: no hit in the row
+      while (e < e1) {
+        const int64_t my = e + lane;
+        bool ok = false;
+        int32_t u = -1, du = 0;
+        if (my < e1) {
+          u = nbr[my];
+          if (u > v) {
+            const uint8_t su = side[u];
+            if (su != sv) {
+              du = delta[u];
+              // v flipped an odd number of times: the net +-2 of its flips
+              if (flips_v & 1) du += su == sv ? 2 : -2;
+              for (int f = 0; f < nf; ++f)
+                if (row_has(nbr, w_pb[warp][f], w_pe[warp][f], u))
+                  du += su == w_pside[warp][f] ? 2 : -2;
+              ok = dv + du + 2 > 0;
+            }
+          }
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, ok);
+        if (!hit) {
+          e += 32;
+          continue;
+        }
+        const int j = warp_first(hit);
+        const int32_t uh = __shfl_sync(0xffffffffu, u, j);
+        const int32_t dh = __shfl_sync(0xffffffffu, du, j);
+        if (nf == kMultiMaxFlips) {  // partner list full: finish the row next step
+          resume = e + j;
+          break;
+        }
+        gain += dv + dh + 2;
+        // apply_flip(v), then apply_flip(uh) as seen from v (localsearch.cpp:28-33)
+        sv ^= 1;
+        dv = -dv;
+        ++flips_v;
+        const uint8_t su_new = side[uh] ^ 1;
+        dv += sv == su_new ? 2 : -2;
+        if (lane == 0) {
+          part[nf] = uh;
+          w_pside[warp][nf] = su_new;
+          w_pb[warp][nf] = off[uh];
+          w_pe[warp][nf] = off[uh + 1];
+        }
+        __syncwarp();
+        ++nf;
+        e = e + j + 1;
+      }
+      // m(v): smallest position above v whose decision the flips can change
+      int32_t m = INT_MAX;
+      if (nf > 0) {
+        m = affected_min(off, nbr, v, v, lane);
+        for (int f = 0; f < nf; ++f) m = min(m, affected_min(off, nbr, part[f], v, lane));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+      }
+      if (lane == 0) {
+        r_m[k] = m;
+        r_gain[k] = gain;
+        r_nf[k] = nf;
+        r_resume[k] = resume;
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // C. commit every hit below M (warp 0, 32 candidates per round)
+    if (warp == 0) {
+      int32_t M = INT_MAX;
+      int32_t next = -1;
+      int64_t next_e = -1;
+      long long add = 0;
+      for (int base = 0; base < Kc; base += 32) {
+        const int k = base + lane;
+        const bool in = k < Kc;
+        const int32_t v = in ? c_v[k] : INT_MAX;
+        const bool hit = in && r_nf[k] > 0;
+        const int32_t mk = hit ? r_m[k] : INT_MAX;
+        // exclusive prefix min of m over earlier hits of this round
+        int32_t pre = mk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t t = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre = min(pre, t);
+        }
+        int32_t excl = __shfl_up_sync(0xffffffffu, pre, 1);
+        if (lane == 0) excl = INT_MAX;
+        const int32_t Mk = min(M, excl);  // M seen by candidate k
+        // stop at the first candidate at/after M, or right after a row that
+        // could not be finished (its resume point is the next start)
+        const bool stop_before = in && v >= Mk;
+        const bool stop_after = in && !stop_before && hit && r_resume[k] >= 0;
+        const unsigned sb = __ballot_sync(0xffffffffu, stop_before);
+        const unsigned sa = __ballot_sync(0xffffffffu, stop_after);
+        const int first_sb = sb ? warp_first(sb) : 32;
+        const int first_sa = sa ? warp_first(sa) : 32;
+        const int cut = min(first_sb, first_sa + 1);  // lanes [0, cut) are decided
+        const bool commit = in && lane < cut && hit;
+        if (in) r_commit[k] = commit ? 1 : 0;
+        long long gsum = commit ? r_gain[k] : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+        add += gsum;
+        const int32_t last_m = __shfl_sync(0xffffffffu, pre, 31);
+        if (cut < 32) {
+          if (first_sb <= first_sa) {
+            next = __shfl_sync(0xffffffffu, Mk, first_sb);  // rescan from the affected position
+          } else {
+            next = __shfl_sync(0xffffffffu, v, first_sa);
+            next_e = __shfl_sync(0xffffffffu, in ? r_resume[k] : -1, first_sa);
+          }
+          for (int kk = base + cut + lane; kk < Kc; kk += 32) r_commit[kk] = 0;
+          break;
+        }
+        M = min(M, last_m);
+      }
+      if (next < 0) next = min(M, s_span + 1);
+      if (lane == 0) {
+        s_total += add;
+        s_pos = next;
+        s_epos = next_e;
+      }
+    }
+    __syncthreads();
+    // D. apply the committed rows (warp per row): flips in the scan's
+    // order v, u1, v, u2, ... then the re-marks of the changed set
+    for (int k = warp; k < Kc; k += NW) {
+      if (!r_commit[k]) continue;
+      const int32_t v = c_v[k];
+      const int nf = r_nf[k];
+      for (int f = 0; f < nf; ++f) {
+        for (int step = 0; step < 2; ++step) {
+          const int32_t t = step == 0 ? v : r_part[k][f];
+          if (lane == 0) {
+            side[t] ^= 1;
+            delta[t] = -delta[t];
+          }
+          __syncwarp();
+          const uint8_t st = side[t];
+          for (int64_t e = off[t] + lane, e1 = off[t + 1]; e < e1; e += 32) {
+            const int32_t y = nbr[e];
+            atomicAdd(delta + y, side[y] == st ? 2 : -2);
+          }
+          __syncwarp();
+        }
+      }
+      warp_mark_after_flip(off, nbr, cand, v, v, lane);
+      for (int f = 0; f < nf; ++f) warp_mark_after_flip(off, nbr, cand, r_part[k][f], v, lane);
+    }
+    __syncthreads();
+    if (s_pos >= n) break;
+  }
+  if (threadIdx.x == 0) {
+    gains[s] += s_total;
+    live[s] = s_total > 0 ? 1 : 0;  // improved: sweep again
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -1287,7 +1608,10 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
     for (int sweep = 0;; ++sweep) {
       k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
                                                  delta, d_live2, d_cand);
-      if (g_scan_cta == 16)
+      if (g_scan_multi)
+        k_two_scan_multi<32, 4><<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
+                                                           side, delta, d_cand, d_live2, d_g2);
+      else if (g_scan_cta == 16)
         k_two_scan_cta<16><<<count, 32 * 16, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
                                                       side, delta, d_cand, d_live2, d_g2);
       else if (g_scan_cta == 32)

@@ -1096,12 +1096,16 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
   // persistent).
   const int64_t cells = int64_t(g->n) * b->Bp;
   const double avg_deg = g->n ? 2.0 * static_cast<double>(g->m) / g->n : 0.0;
+  // (the persistent kernel's static row split has no heavy-row CTAs: graphs
+  // with rows the per-pass launches would stage take the per-pass path)
+  const size_t base_smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
   const bool persistent =
-      cells <= persistent_cells() ||
-      (g_persistent_cells == (int64_t(1) << 22) && cells <= (int64_t(1) << 25) &&
-       group_quads(b) == b->Q && g->max_degree <= 32.0 * avg_deg + 32.0);
+      heavy_plan(b, group_quads(b), base_smem).heavy == 0 &&
+      (cells <= persistent_cells() ||
+       (g_persistent_cells == (int64_t(1) << 22) && cells <= (int64_t(1) << 25) &&
+        group_quads(b) == b->Q && g->max_degree <= 32.0 * avg_deg + 32.0));
   PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl);
-  const size_t smem = sizeof(unsigned long long) * b->Bp + sizeof(uint32_t) * b->Bp + b->Bp + b->Q;
+  const size_t smem = base_smem;
   if (!persistent) {  // chain tiling (see group_quads)
     a.Qg = group_quads(b);
     a.hot_rows = hot_rows(b, a.Qg);
