@@ -104,7 +104,10 @@ int mqo_graph_from_edges(int32_t n, int64_t num_edges, const int32_t* eu, const 
  * sequence from the reference's O(n^2) ER (graph.cpp:107-116, infeasible at
  * n = 1e7); used for the large configs, with the edge list then fed to both
  * sides. */
-enum { MQO_GEN_ER = 0, MQO_GEN_BA = 1, MQO_GEN_SBM = 2, MQO_GEN_ER_FAST = 3 };
+/* MQO_GEN_SBM_FAST: O(m) stochastic block model (geometric skipping over
+ * the p_in and p_out pair runs of each row; the reference's distribution,
+ * not its O(n^2) draw sequence, graph.cpp:148-165). */
+enum { MQO_GEN_ER = 0, MQO_GEN_BA = 1, MQO_GEN_SBM = 2, MQO_GEN_ER_FAST = 3, MQO_GEN_SBM_FAST = 4 };
 typedef struct {
   int32_t kind;
   int32_t n;

@@ -26,7 +26,7 @@ from ._lib import (ADJACENCY, CHECKER_ACCEPTED, CONVERGED, ITER_CAP, LAPLACIAN, 
                    lib)
 
 __all__ = [
-    "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "generate", "StripResult",
+    "Graph", "ErSpec", "ErFastSpec", "BaSpec", "SbmSpec", "SbmFastSpec", "generate", "StripResult",
     "strip_isolated", "connected_components", "MisQubo", "Laplacian",
     "PerturbedLaplacian", "Adjacency", "PerturbedBias", "OptimizerConfig", "ChainBatch",
     "StopReason", "problem_of", "step", "gradient", "run_trajectory", "mis_fixed_point_check",
@@ -138,6 +138,16 @@ class BaSpec:  # graph.hpp:72-75
 
 @dataclass(frozen=True)
 class SbmSpec:  # graph.hpp:77-82
+    n: int
+    k: int = 2
+    p_in: float = 0.0
+    p_out: float = 0.0
+
+
+@dataclass(frozen=True)
+class SbmFastSpec:
+    """O(m) stochastic block model (geometric skipping over the p_in / p_out
+    pair runs); the reference's distribution, not its draw sequence."""
     n: int
     k: int = 2
     p_in: float = 0.0
@@ -349,6 +359,8 @@ def generate(spec, seed: int, device: int = 0) -> Graph:
         s.kind, s.n, s.m_attach = 1, spec.n, spec.m_attach
     elif isinstance(spec, SbmSpec):
         s.kind, s.n, s.k, s.p_in, s.p_out = 2, spec.n, spec.k, spec.p_in, spec.p_out
+    elif isinstance(spec, SbmFastSpec):
+        s.kind, s.n, s.k, s.p_in, s.p_out = 4, spec.n, spec.k, spec.p_in, spec.p_out
     else:
         raise InvalidArgument(1, "generate: unknown spec")
     h = C.c_void_p()

@@ -61,7 +61,8 @@ def preset_for(problem: str, n: int, mean_degree: float):
 
 
 def parse_gen_spec(text: str):
-    """cli_common.cpp:44-75 (+ er-fast:<n>:<d>, the O(m) generator)."""
+    """cli_common.cpp:44-75 (+ er-fast:<n>:<d> and sbm-fast:<n>:<k>:<pin>:<pout>,
+    the O(m) generators)."""
     parts = text.split(":")
     try:
         if parts[0] in ("er", "er-fast") and len(parts) == 3:
@@ -70,11 +71,12 @@ def parse_gen_spec(text: str):
             return (P.ErSpec if parts[0] == "er" else P.ErFastSpec)(n, p)
         if parts[0] == "ba" and len(parts) == 3:
             return P.BaSpec(int(parts[1]), int(parts[2]))
-        if parts[0] == "sbm" and len(parts) == 5:
-            return P.SbmSpec(int(parts[1]), int(parts[2]), float(parts[3]), float(parts[4]))
+        if parts[0] in ("sbm", "sbm-fast") and len(parts) == 5:
+            return (P.SbmSpec if parts[0] == "sbm" else P.SbmFastSpec)(
+                int(parts[1]), int(parts[2]), float(parts[3]), float(parts[4]))
     except ValueError as e:
         raise UsageError(f"cannot parse generator spec '{text}': {e}")
-    raise UsageError(f"unknown generator spec '{text}' (er, er-fast, ba, sbm)")
+    raise UsageError(f"unknown generator spec '{text}' (er, er-fast, ba, sbm, sbm-fast)")
 
 
 def encode_bits(bits: np.ndarray) -> dict:

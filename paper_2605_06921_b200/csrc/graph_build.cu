@@ -166,6 +166,61 @@ void generate_sbm(int32_t n, int32_t k, double p_in, double p_out, uint64_t seed
   csr_from_keys(n, keys, off, nbr);
 }
 
+// O(m) stochastic block model: the reference's pair loop (graph.cpp:148-165)
+// draws one Bernoulli per pair, O(n^2).  Blocks are contiguous (vertex v in
+// block v*k/n), so row u's pairs (u, v > u) split into one p_in run -- the
+// rest of u's block -- and one p_out run -- every later block.  Geometric
+// skipping (Batagelj & Brandes 2005) over the concatenation of all p_in runs,
+// and separately over all p_out runs, makes every pair an independent
+// Bernoulli(p_in or p_out) draw, the reference's distribution, in O(n + m)
+// expected work.  Not the reference's draw sequence; streams
+// Rng(derive_seed(seed, 0x5B31)) (p_in) and (seed, 0x5B30) (p_out).
+struct SkipRun {  // geometric skipping over a sequence of pair runs
+  Xoshiro r;
+  double lq;
+  bool all, none;
+  int64_t left = -1;  // pairs to skip before the next edge (-1: draw)
+  explicit SkipRun(uint64_t seed, double p)
+      : r(xoshiro_seed(seed)), lq(p < 1.0 ? std::log1p(-p) : 0.0), all(p >= 1.0), none(p <= 0.0) {}
+  // calls emit(v) for every edge among the `len` pairs (u, first + i)
+  template <class F>
+  void run(int64_t first, int64_t len, F emit) {
+    if (none || len <= 0) return;
+    int64_t i = 0;
+    for (;;) {
+      if (left < 0) {
+        left = all ? 0 : static_cast<int64_t>(std::floor(std::log1p(-u01_of(xoshiro_next(r))) / lq));
+      }
+      if (i + left >= len) {  // the skip runs past this run: carry the rest over
+        left -= len - i;
+        return;
+      }
+      i += left;
+      emit(first + i);
+      ++i;
+      left = -1;
+    }
+  }
+};
+
+void generate_sbm_fast(int32_t n, int32_t k, double p_in, double p_out, uint64_t seed,
+                       std::vector<int64_t>& off, std::vector<int32_t>& nbr) {
+  if (k < 1) throw std::invalid_argument("sbm: k must be >= 1");
+  if (p_in < 0.0 || p_in > 1.0 || p_out < 0.0 || p_out > 1.0)
+    throw std::invalid_argument("sbm: probabilities outside [0,1]");
+  if (p_in <= p_out) throw std::invalid_argument("sbm: requires p_in > p_out");
+  std::vector<uint64_t> keys;
+  SkipRun in(derive_seed(seed, 0x5B31ULL), p_in), out(derive_seed(seed, 0x5B30ULL), p_out);
+  for (int32_t u = 0; u + 1 < n; ++u) {
+    const int64_t bu = (static_cast<int64_t>(u) * k) / n;
+    // first vertex of the next block: smallest v with v*k/n > bu
+    const int64_t hi = std::min<int64_t>(n, ((bu + 1) * n + k - 1) / k);
+    in.run(u + 1, hi - (u + 1), [&](int64_t v) { keys.push_back(key_of(u, static_cast<int32_t>(v))); });
+    out.run(hi, n - hi, [&](int64_t v) { keys.push_back(key_of(u, static_cast<int32_t>(v))); });
+  }
+  csr_from_keys(n, keys, off, nbr);
+}
+
 }  // namespace
 
 extern "C" int mqo_graph_from_edges(int32_t n, int64_t num_edges, const int32_t* eu,
@@ -194,6 +249,9 @@ extern "C" int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph*
       case MQO_GEN_ER_FAST: generate_er_fast(spec->n, spec->p, spec->seed, off, nbr); break;
       case MQO_GEN_SBM:
         generate_sbm(spec->n, spec->k, spec->p_in, spec->p_out, spec->seed, off, nbr);
+        break;
+      case MQO_GEN_SBM_FAST:
+        generate_sbm_fast(spec->n, spec->k, spec->p_in, spec->p_out, spec->seed, off, nbr);
         break;
       default: throw std::invalid_argument("mqo_generate: unknown generator kind");
     }
