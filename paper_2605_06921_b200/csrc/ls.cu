@@ -392,17 +392,62 @@ __device__ __forceinline__ bool two_cand(const int64_t* __restrict__ off,
   return false;
 }
 
+// Rows longer than this are tested by a whole warp (k_two_cand_heavy): a
+// thread walking a hub's 3350 upper neighbours one dependent load at a time
+// took milliseconds and set the sweep's critical path.
+constexpr int64_t kCandWarpDeg = 64;
+
 __global__ void k_two_cand(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
                            const int32_t* __restrict__ hmax, int32_t n, int32_t count,
                            const uint8_t* __restrict__ side_all, const int32_t* __restrict__ delta_all,
-                           const int32_t* __restrict__ live, uint8_t* __restrict__ cand_all) {
+                           const int32_t* __restrict__ live, uint8_t* __restrict__ cand_all,
+                           const uint8_t* __restrict__ mask_all) {
   const int64_t total = static_cast<int64_t>(count) * n;
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = q / n;
     const int32_t v = static_cast<int32_t>(q - s * n);
     if (!live[s]) continue;
-    cand_all[q] = two_cand(off, nbr, hmax, side_all + s * n, delta_all + s * n, v) ? 1 : 0;
+    if (off[v + 1] - off[v] > kCandWarpDeg) continue;  // k_two_cand_heavy
+    // mask (may be null): only vertices the last sweep's commits touched can
+    // have become candidates; the rest keep their "no move"
+    cand_all[q] = (!mask_all || mask_all[q]) &&
+                  two_cand(off, nbr, hmax, side_all + s * n, delta_all + s * n, v) ? 1 : 0;
+  }
+}
+
+// The long rows (a prefix of the degree-descending order): a warp per
+// (body, row), lanes over the upper neighbours.
+__global__ void k_two_cand_heavy(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                 const int32_t* __restrict__ hmax,
+                                 const int32_t* __restrict__ order, int32_t heavy, int32_t n,
+                                 int32_t count, const uint8_t* __restrict__ side_all,
+                                 const int32_t* __restrict__ delta_all,
+                                 const int32_t* __restrict__ live, uint8_t* __restrict__ cand_all,
+                                 const uint8_t* __restrict__ mask_all) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = static_cast<int64_t>(count) * heavy;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < total;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t s = w / heavy;
+    if (!live[s]) continue;
+    const int32_t v = order[w - s * heavy];
+    const uint8_t* side = side_all + s * n;
+    const int32_t* delta = delta_all + s * n;
+    const int32_t dv = delta[v];
+    bool found = false;
+    if ((!mask_all || mask_all[s * n + v]) && dv + hmax[v] + 2 > 0) {  // uniform per warp
+      const uint8_t sv = side[v];
+      const int64_t e0 = off[v], e1 = off[v + 1];
+      for (int64_t top = e1 - 1; top >= e0; top -= 32) {  // u > v lie at the row's end
+        const int64_t e = top - lane;
+        const int32_t u = e >= e0 ? nbr[e] : -1;
+        const bool ok = u > v && side[u] != sv && dv + delta[u] + 2 > 0;
+        found = __any_sync(0xffffffffu, ok);
+        if (found || __all_sync(0xffffffffu, u <= v)) break;
+      }
+    }
+    if (lane == 0) cand_all[s * n + v] = found ? 1 : 0;
   }
 }
 
@@ -752,12 +797,32 @@ __device__ __forceinline__ int32_t affected_min(const int64_t* __restrict__ off,
   return m;
 }
 
+// warp_mark_after_flip that also records every affected position -- above
+// and below v -- in `next`: the next sweep's candidates (a vertex whose read
+// set no commit touched after its turn keeps the "no move" it had)
+__device__ void warp_mark_after_flip2(const int64_t* off, const int32_t* nbr, uint8_t* cand,
+                                      uint8_t* next, int32_t t, int32_t v, int lane) {
+  const int64_t e0 = off[t], e1 = off[t + 1];
+  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+    const int32_t y = a < e0 ? t : nbr[a];
+    if (y > v) cand[y] = 1;
+    next[y] = 1;
+    for (int64_t c = off[y]; c < off[y + 1]; ++c) {
+      const int32_t w = nbr[c];
+      if (w >= y) break;  // rows ascending: only w < y
+      if (w > v) cand[w] = 1;
+      next[w] = 1;
+    }
+  }
+  __syncwarp();
+}
+
 template <int NW, int C>
 __global__ void __launch_bounds__(32 * NW)
     k_two_scan_multi(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
                      const int32_t* __restrict__ hmax, int32_t n, int32_t count,
-                     uint8_t* side_all, int32_t* delta_all, uint8_t* cand_all, int32_t* live,
-                     int64_t* gains) {
+                     uint8_t* side_all, int32_t* delta_all, uint8_t* cand_all,
+                     uint8_t* next_all, int32_t* live, int64_t* gains, int64_t* stats) {
   constexpr int K = NW * C;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int s = blockIdx.x;
@@ -765,6 +830,7 @@ __global__ void __launch_bounds__(32 * NW)
   uint8_t* side = side_all + static_cast<int64_t>(s) * n;
   int32_t* delta = delta_all + static_cast<int64_t>(s) * n;
   uint8_t* cand = cand_all + static_cast<int64_t>(s) * n;
+  uint8_t* next_marks = next_all + static_cast<int64_t>(s) * n;
   __shared__ int32_t c_v[K];
   __shared__ int64_t c_e[K];                 // row start (resumed rows: after the last flip)
   __shared__ int32_t r_m[K], r_gain[K], r_nf[K];
@@ -774,6 +840,9 @@ __global__ void __launch_bounds__(32 * NW)
   __shared__ int32_t s_k, s_pos, s_span;
   __shared__ int64_t s_epos;
   __shared__ long long s_total;
+  __shared__ int32_t w_cnt[NW], w_tot;
+  __shared__ int32_t s_steps, s_commits;
+  __shared__ long long s_cyc[4];  // MQO_TRACE: cycles in phases A-D
   // per-warp simulation scratch: partner rows [pb, pe) and sides after flip
   __shared__ int64_t w_pb[NW][kMultiMaxFlips], w_pe[NW][kMultiMaxFlips];
   __shared__ uint8_t w_pside[NW][kMultiMaxFlips];
@@ -781,57 +850,84 @@ __global__ void __launch_bounds__(32 * NW)
     s_pos = 0;
     s_epos = -1;
     s_total = 0;
+    s_steps = 0;
+    s_commits = 0;
+    s_cyc[0] = s_cyc[1] = s_cyc[2] = s_cyc[3] = 0;
   }
   __syncthreads();
   for (;;) {
-    // A. the next K marked vertices from s_pos (warp 0); s_span = last
+    long long t_a = clock64();
+    // A. the next K marked vertices from s_pos, collected by the whole CTA:
+    // warp w scans 1024 positions (32 per lane), per-lane masks, warp and
+    // CTA prefix counts, positions written in order; s_span = last
     // position examined
-    if (warp == 0) {
-      int k = 0;
-      int32_t from = s_pos;
-      if (s_epos >= 0) {  // resume the current vertex's row
-        if (lane == 0) {
-          c_v[0] = s_pos;
-          c_e[0] = s_epos;
-        }
-        k = 1;
-        from = s_pos + 1;
+    if (threadIdx.x == 0) {
+      s_k = 0;
+      s_span = n - 1;
+      if (s_epos >= 0) {  // resume the current vertex's row first
+        c_v[0] = s_pos;
+        c_e[0] = s_epos;
+        s_k = 1;
       }
-      int32_t span = n - 1;
-      for (int32_t cb = from; cb < n && k < K; cb += 32) {
-        if (((cb - from) & 511) == 0) {  // empty 512-mark stretches cost one round trip
-          bool any16 = false;
+    }
+    __syncthreads();
+    const int32_t start = s_epos >= 0 ? s_pos + 1 : s_pos;
+    // 16-byte aligned windows (the body's marks need not be aligned)
+    const int32_t skew = static_cast<int32_t>(reinterpret_cast<uintptr_t>(cand + start) & 15);
+    for (int32_t from = start - skew; from < n; from += NW * 1024) {
+      const int32_t base = from + warp * 1024 + lane * 32;
+      unsigned bits = 0;
+      if (base < n) {
+        const uint4 w0 = __ldcg(reinterpret_cast<const uint4*>(cand + base));
+        const uint4 w1 = __ldcg(reinterpret_cast<const uint4*>(cand + base) + 1);
+        const uint32_t wd[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const int32_t q = cb + 16 * lane + t;
-            any16 |= q < n && *reinterpret_cast<const volatile uint8_t*>(cand + q) != 0;
-          }
-          if (!__any_sync(0xffffffffu, any16)) {
-            cb += 512 - 32;
-            continue;
-          }
-        }
-        const bool f = cb + lane < n && *reinterpret_cast<volatile uint8_t*>(cand + cb + lane);
-        unsigned mask = __ballot_sync(0xffffffffu, f);
-        while (mask && k < K) {
-          const int i = warp_first(mask);
-          if (lane == 0) {
-            c_v[k] = cb + i;
-            c_e[k] = -1;
-          }
-          ++k;
-          mask &= mask - 1;
-          if (k == K) span = cb + i;
-        }
+        for (int t = 0; t < 32; ++t)
+          if ((wd[t >> 2] >> (8 * (t & 3))) & 0xffu) bits |= 1u << t;
+        // positions outside [start, n)
+        if (base < start) bits &= start - base >= 32 ? 0u : ~0u << (start - base);
+        if (base + 32 > n) bits &= n - base >= 32 ? ~0u : (1u << (n - base)) - 1u;
       }
-      if (lane == 0) {
-        s_k = k;
-        s_span = span;
+      const int cnt = __popc(bits);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
+      if (lane == 31) w_cnt[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {  // exclusive prefix over the warps
+        int c = lane < NW ? w_cnt[lane] : 0, pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre += t;
+        }
+        if (lane < NW) w_cnt[lane] = pre - c;
+        if (lane == 31) w_tot = pre;
+      }
+      __syncthreads();
+      const int k0 = s_k;
+      int k = k0 + w_cnt[warp] + incl - cnt;
+      while (bits && k < K) {
+        const int t = __ffs(bits) - 1;
+        bits &= bits - 1;
+        c_v[k] = base + t;
+        c_e[k] = -1;
+        if (k == K - 1) s_span = base + t;
+        ++k;
+      }
+      __syncthreads();
+      const int total = w_tot;
+      if (threadIdx.x == 0) s_k = min(K, k0 + total);
+      __syncthreads();
+      if (s_k >= K) break;
     }
     __syncthreads();
     const int Kc = s_k;
     if (Kc == 0) break;
+    long long t_b = clock64();
     // B. simulate each candidate's row against the current state (read only)
     for (int k = warp; k < Kc; k += NW) {
       const int32_t v = c_v[k];
@@ -910,64 +1006,92 @@ __global__ void __launch_bounds__(32 * NW)
       __syncwarp();
     }
     __syncthreads();
-    // C. commit every hit below M (warp 0, 32 candidates per round)
+    long long t_c = clock64();
+    // C. commit every hit below M (warp 0; lane l owns candidates
+    // [l*L, l*L + L)): a scan of the lanes' minima of m gives each lane the M
+    // its first candidate sees, the lane walks its L candidates, and the
+    // first stop over the warp ends the step
     if (warp == 0) {
-      int32_t M = INT_MAX;
-      int32_t next = -1;
-      int64_t next_e = -1;
-      long long add = 0;
-      for (int base = 0; base < Kc; base += 32) {
-        const int k = base + lane;
-        const bool in = k < Kc;
-        const int32_t v = in ? c_v[k] : INT_MAX;
-        const bool hit = in && r_nf[k] > 0;
-        const int32_t mk = hit ? r_m[k] : INT_MAX;
-        // exclusive prefix min of m over earlier hits of this round
-        int32_t pre = mk;
+      constexpr int L = K / 32;
+      int32_t loc = INT_MAX;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t t = __shfl_up_sync(0xffffffffu, pre, o);
-          if (lane >= o) pre = min(pre, t);
-        }
-        int32_t excl = __shfl_up_sync(0xffffffffu, pre, 1);
-        if (lane == 0) excl = INT_MAX;
-        const int32_t Mk = min(M, excl);  // M seen by candidate k
-        // stop at the first candidate at/after M, or right after a row that
-        // could not be finished (its resume point is the next start)
-        const bool stop_before = in && v >= Mk;
-        const bool stop_after = in && !stop_before && hit && r_resume[k] >= 0;
-        const unsigned sb = __ballot_sync(0xffffffffu, stop_before);
-        const unsigned sa = __ballot_sync(0xffffffffu, stop_after);
-        const int first_sb = sb ? warp_first(sb) : 32;
-        const int first_sa = sa ? warp_first(sa) : 32;
-        const int cut = min(first_sb, first_sa + 1);  // lanes [0, cut) are decided
-        const bool commit = in && lane < cut && hit;
-        if (in) r_commit[k] = commit ? 1 : 0;
-        long long gsum = commit ? r_gain[k] : 0;
+      for (int i = 0; i < L; ++i) {
+        const int k = lane * L + i;
+        if (k < Kc && r_nf[k] > 0) loc = min(loc, r_m[k]);
+      }
+      int32_t pre = loc;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
-        add += gsum;
-        const int32_t last_m = __shfl_sync(0xffffffffu, pre, 31);
-        if (cut < 32) {
-          if (first_sb <= first_sa) {
-            next = __shfl_sync(0xffffffffu, Mk, first_sb);  // rescan from the affected position
-          } else {
-            next = __shfl_sync(0xffffffffu, v, first_sa);
-            next_e = __shfl_sync(0xffffffffu, in ? r_resume[k] : -1, first_sa);
-          }
-          for (int kk = base + cut + lane; kk < Kc; kk += 32) r_commit[kk] = 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre = min(pre, t);
+      }
+      int32_t running = __shfl_up_sync(0xffffffffu, pre, 1);
+      if (lane == 0) running = INT_MAX;
+      const int32_t all_min = __shfl_sync(0xffffffffu, pre, 31);
+      // key 2k: stop before candidate k; 2k + 1: stop right after k
+      int32_t key = INT_MAX, stop_next = -1;
+      int64_t stop_e = -1;
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const int k = lane * L + i;
+        if (k >= Kc || key != INT_MAX) break;
+        const int32_t v = c_v[k];
+        if (v >= running) {  // a committed hit before k touched k's decision
+          key = 2 * k;
+          stop_next = running;
           break;
         }
-        M = min(M, last_m);
+        if (r_nf[k] > 0) {
+          if (r_resume[k] >= 0) {  // row not finished: resume it next step
+            key = 2 * k + 1;
+            stop_next = v;
+            stop_e = r_resume[k];
+            break;
+          }
+          running = min(running, r_m[k]);
+        }
       }
-      if (next < 0) next = min(M, s_span + 1);
+      int32_t gkey = key;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gkey = min(gkey, __shfl_xor_sync(0xffffffffu, gkey, o));
+      long long add = 0;
+      int commits = 0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const int k = lane * L + i;
+        if (k >= Kc) break;
+        const bool commit = r_nf[k] > 0 && 2 * k < gkey;
+        r_commit[k] = commit ? 1 : 0;
+        if (commit) {
+          add += r_gain[k];
+          ++commits;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        add += __shfl_xor_sync(0xffffffffu, add, o);
+        commits += __shfl_xor_sync(0xffffffffu, commits, o);
+      }
+      const unsigned owner = __ballot_sync(0xffffffffu, key == gkey && key != INT_MAX);
+      int32_t next;
+      int64_t next_e = -1;
+      if (owner) {
+        const int src = warp_first(owner);
+        next = __shfl_sync(0xffffffffu, stop_next, src);
+        next_e = __shfl_sync(0xffffffffu, stop_e, src);
+      } else {
+        next = min(all_min, s_span + 1);
+      }
       if (lane == 0) {
+        ++s_steps;
+        s_commits += commits;
         s_total += add;
         s_pos = next;
         s_epos = next_e;
       }
     }
     __syncthreads();
+    long long t_d = clock64();
     // D. apply the committed rows (warp per row): flips in the scan's
     // order v, u1, v, u2, ... then the re-marks of the changed set
     for (int k = warp; k < Kc; k += NW) {
@@ -990,15 +1114,31 @@ __global__ void __launch_bounds__(32 * NW)
           __syncwarp();
         }
       }
-      warp_mark_after_flip(off, nbr, cand, v, v, lane);
-      for (int f = 0; f < nf; ++f) warp_mark_after_flip(off, nbr, cand, r_part[k][f], v, lane);
+      warp_mark_after_flip2(off, nbr, cand, next_marks, v, v, lane);
+      for (int f = 0; f < nf; ++f)
+        warp_mark_after_flip2(off, nbr, cand, next_marks, r_part[k][f], v, lane);
     }
     __syncthreads();
+    if (stats && threadIdx.x == 0) {
+      const long long t_e = clock64();
+      s_cyc[0] += t_b - t_a;
+      s_cyc[1] += t_c - t_b;
+      s_cyc[2] += t_d - t_c;
+      s_cyc[3] += t_e - t_d;
+    }
     if (s_pos >= n) break;
   }
   if (threadIdx.x == 0) {
     gains[s] += s_total;
     live[s] = s_total > 0 ? 1 : 0;  // improved: sweep again
+    if (stats) {  // MQO_TRACE: steps and commits of this sweep
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats), static_cast<unsigned long long>(s_steps));
+      atomicAdd(reinterpret_cast<unsigned long long*>(stats + 1),
+                static_cast<unsigned long long>(s_commits));
+      for (int q = 0; q < 4; ++q)
+        atomicAdd(reinterpret_cast<unsigned long long*>(stats + 2 + q),
+                  static_cast<unsigned long long>(s_cyc[q]));
+    }
   }
 }
 
@@ -1599,18 +1739,43 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   MQO_CUDA(cudaMallocAsync(&d_und, sizeof(int32_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_g1, sizeof(int64_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_g2, sizeof(int64_t) * count, st));
-  MQO_CUDA(cudaMallocAsync(&d_cand, cells, st));
+  // marks of this sweep / of the next one (+64: the scan reads 16-byte
+  // aligned windows past a body's end)
+  MQO_CUDA(cudaMallocAsync(&d_cand, cells + 64, st));
+  uint8_t* d_next = nullptr;
+  if (g_scan_multi) MQO_CUDA(cudaMallocAsync(&d_next, cells + 64, st));
+  int64_t* d_stats = nullptr;  // MQO_TRACE: 2-flip steps / commits per sweep
+  if (trace_on()) {
+    MQO_CUDA(cudaMallocAsync(&d_stats, 6 * sizeof(int64_t), st));
+    MQO_CUDA(cudaMemsetAsync(d_stats, 0, 6 * sizeof(int64_t), st));
+  }
   std::vector<int32_t> live(count, 1), live2(count);
   std::vector<int64_t> total(count, 0), g1(count, 0), g2(count, 0);
   auto two_flip = [&](const std::vector<int32_t>& who) {
     MQO_CUDA(cudaMemcpyAsync(d_live2, who.data(), sizeof(int32_t) * count, cudaMemcpyHostToDevice, st));
     MQO_CUDA(cudaMemsetAsync(d_g2, 0, sizeof(int64_t) * count, st));
     for (int sweep = 0;; ++sweep) {
+      // the exact candidate test: every vertex in the first sweep, then only
+      // those the last sweep's commits touched (its `next` marks)
+      uint8_t* mask = nullptr;
+      if (sweep > 0 && g_scan_multi) {
+        std::swap(d_cand, d_next);
+        mask = d_cand;  // tested in place: each cell reads only its own mark
+      }
       k_two_cand<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side,
-                                                 delta, d_live2, d_cand);
-      if (g_scan_multi)
+                                                 delta, d_live2, d_cand, mask);
+      const int32_t heavy = g->h_deg_ge.size() > size_t(kCandWarpDeg) + 1
+                                ? g->h_deg_ge[kCandWarpDeg + 1] : 0;
+      if (heavy > 0)
+        k_two_cand_heavy<<<ls_grid(int64_t(count) * heavy * 32), 256, 0, st>>>(
+            g->d_off, g->d_nbr, g->d_hmax, g->d_order, heavy, n, count, side, delta, d_live2,
+            d_cand, mask);
+      if (g_scan_multi) {
+        MQO_CUDA(cudaMemsetAsync(d_next, 0, cells, st));
         k_two_scan_multi<32, 4><<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
-                                                           side, delta, d_cand, d_live2, d_g2);
+                                                           side, delta, d_cand, d_next, d_live2,
+                                                           d_g2, d_stats);
+      }
       else if (g_scan_cta == 16)
         k_two_scan_cta<16><<<count, 32 * 16, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
                                                       side, delta, d_cand, d_live2, d_g2);
@@ -1628,7 +1793,17 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       MQO_CUDA(cudaStreamSynchronize(st));
       bool any = false;
       for (int i = 0; i < count; ++i) any |= live2[i] != 0;
-      MQO_TRACE("two_flip sweep %d", sweep);
+      if (d_stats) {
+        int64_t sc[6] = {0, 0, 0, 0, 0, 0};
+        MQO_CUDA(cudaMemcpy(sc, d_stats, sizeof(sc), cudaMemcpyDeviceToHost));
+        MQO_CUDA(cudaMemset(d_stats, 0, sizeof(sc)));
+        MQO_TRACE("two_flip sweep %d: %lld steps, %lld row commits (all bodies); Mcycles A %.2f "
+                  "B %.2f C %.2f D %.2f", sweep, static_cast<long long>(sc[0]),
+                  static_cast<long long>(sc[1]), sc[2] * 1e-6, sc[3] * 1e-6, sc[4] * 1e-6,
+                  sc[5] * 1e-6);
+      } else {
+        MQO_TRACE("two_flip sweep %d", sweep);
+      }
       if (!any) break;
     }
     MQO_CUDA(cudaMemcpyAsync(g2.data(), d_g2, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
@@ -1726,6 +1901,8 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   cudaFreeAsync(d_g1, st);
   cudaFreeAsync(d_g2, st);
   cudaFreeAsync(d_cand, st);
+  if (d_next) cudaFreeAsync(d_next, st);
+  if (d_stats) cudaFreeAsync(d_stats, st);
 }
 
 // Scratch of the (1,2)-swap kernels: dirty flags, the dirty list(s) and the
