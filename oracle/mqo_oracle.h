@@ -150,6 +150,8 @@ int orc_one_two_flip(void* g, uint8_t* side, int64_t* gain);
 /* --- Engine (solver.cpp run_engine) --- */
 int orc_solve_pooled(void* g, const orc_solver_cfg* cfg, orc_report* report,
                      uint8_t* best_body);
+/* reference only: the CLI solve / sweep commands (see ref_shim.cpp) */
+int orc_cli_run(const char* args);
 int orc_preset_for(int32_t problem, int32_t n, double mean_degree, double* alpha,
                    double* momentum, double* rho, int32_t* reset_rounds);
 

@@ -447,3 +447,67 @@ extern "C" int ref_parse_graph(const char* text, int64_t len, int32_t fmt, int32
     return 3;
   }
 }
+
+// ---- the reference CLI (tools/src/cli_common.cpp, cmd_basic.cpp,
+// cmd_sweep.cpp), for RunRecord parity of paper_2605_06921_b200/cli.py.
+// `args`: '\n'-separated key=value lines naming SolveOptions fields
+// (cli_common.hpp:33-48; "cmd" = solve | sweep, plus param / values / seeds
+// / jobs / jsonl for sweep).  The command writes its record to `out`
+// (SolveOptions::out_file / the sweep's jsonl path) exactly as the
+// reference binary would print it.  Returns the command's exit code, or -1
+// with the message in orc_last_error() when it throws.
+#include "cli_common.hpp"
+
+extern "C" int orc_cli_run(const char* args) {
+  using namespace mqo::cli;
+  try {
+    SolveOptions opt;
+    std::string cmd = "solve", param, values, seeds = "", jsonl;
+    int jobs = 1;
+    std::istringstream in(args ? args : "");
+    std::string line;
+    while (std::getline(in, line)) {
+      const auto eq = line.find('=');
+      if (eq == std::string::npos) continue;
+      const std::string k = line.substr(0, eq), v = line.substr(eq + 1);
+      if (k == "cmd") cmd = v;
+      else if (k == "problem") opt.problem = v;
+      else if (k == "graph") opt.graph_file = v;
+      else if (k == "gen") opt.gen_spec = v;
+      else if (k == "objective") opt.objective = v;
+      else if (k == "preset") opt.preset = v;
+      else if (k == "report") opt.report = v;
+      else if (k == "out") opt.out_file = v;
+      else if (k == "budget_secs") opt.budget_secs = std::stod(v);
+      else if (k == "seed") opt.seed = std::stoull(v);
+      else if (k == "alpha") opt.alpha = std::stod(v);
+      else if (k == "momentum") opt.momentum = std::stod(v);
+      else if (k == "rho") opt.rho = std::stod(v);
+      else if (k == "lambda") opt.lambda = std::stod(v);
+      else if (k == "gamma") opt.gamma = std::stod(v);
+      else if (k == "sigma") opt.sigma = std::stod(v);
+      else if (k == "conv_tol") opt.conv_tol = std::stod(v);
+      else if (k == "tgs") opt.tgs = std::stoi(v);
+      else if (k == "max_iters") opt.max_iters = std::stoi(v);
+      else if (k == "check_every") opt.check_every = std::stoi(v);
+      else if (k == "pool_b") opt.pool_b = std::stoi(v);
+      else if (k == "pool_k") opt.pool_k = std::stoi(v);
+      else if (k == "max_outer") opt.max_outer = std::stoi(v);
+      else if (k == "init_constant") opt.init_constant = std::stod(v);
+      else if (k == "stop_at_score") opt.stop_at_score = std::stoll(v);
+      else if (k == "no_local_search") opt.no_local_search = v == "1";
+      else if (k == "param") param = v;
+      else if (k == "values") values = v;
+      else if (k == "seeds") seeds = v;
+      else if (k == "jobs") jobs = std::stoi(v);
+      else if (k == "jsonl") jsonl = v;
+      else throw std::invalid_argument("orc_cli_run: unknown key " + k);
+    }
+    if (cmd == "solve") return cmd_solve(opt);
+    if (cmd == "sweep") return cmd_sweep(opt, param, values, seeds, jobs, jsonl);
+    throw std::invalid_argument("orc_cli_run: unknown cmd " + cmd);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}

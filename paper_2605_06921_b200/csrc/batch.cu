@@ -55,7 +55,7 @@ __global__ void k_project(double* __restrict__ x, int64_t count, double lo) {
 namespace mqo_b200 {
 double* aux_buffer(mqo_batch* b) {
   if (!b->d_aux)
-    MQO_CUDA(cudaMalloc(&b->d_aux, sizeof(double) * std::max<int64_t>(1, int64_t(b->g->n) * b->Bp)));
+    dalloc(b, &b->d_aux, sizeof(double) * std::max<int64_t>(1, int64_t(b->g->n) * b->Bp));
   return b->d_aux;
 }
 
@@ -146,18 +146,22 @@ extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
       MQO_CUDA(cudaSetDevice(g->device));
       keep_pool_memory(g->device);
       MQO_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+      // stream-ordered allocations from the device's pool, which keeps its
+      // memory (keep_pool_memory): a solve's batch and scratch come back
+      // without a driver mapping the next time (the engine creates a batch
+      // per solve)
       const size_t state = sizeof(double) * std::max<int64_t>(1, int64_t(g->n) * b->Bp);
-      MQO_CUDA(cudaMalloc(&b->d_x[0], state));
-      MQO_CUDA(cudaMalloc(&b->d_x[1], state));
-      MQO_CUDA(cudaMalloc(&b->d_v, state));
+      dalloc(b, &b->d_x[0], state);
+      dalloc(b, &b->d_x[1], state);
+      dalloc(b, &b->d_v, state);
       MQO_CUDA(cudaMemsetAsync(b->d_x[0], 0, state, b->stream));
       MQO_CUDA(cudaMemsetAsync(b->d_x[1], 0, state, b->stream));
       MQO_CUDA(cudaMemsetAsync(b->d_v, 0, state, b->stream));
-      MQO_CUDA(cudaMalloc(&b->d_ctl, sizeof(ChainCtl) * b->Bp));
-      MQO_CUDA(cudaMalloc(&b->d_viol, sizeof(uint32_t) * 3 * b->Bp));
-      MQO_CUDA(cudaMalloc(&b->d_chg, sizeof(unsigned long long) * 3 * b->Bp));
-      MQO_CUDA(cudaMalloc(&b->d_flag, sizeof(int32_t) * 4));
-      MQO_CUDA(cudaMalloc(&b->d_qmask, std::max(1, b->Q)));
+      dalloc(b, &b->d_ctl, sizeof(ChainCtl) * b->Bp);
+      dalloc(b, &b->d_viol, sizeof(uint32_t) * 3 * b->Bp);
+      dalloc(b, &b->d_chg, sizeof(unsigned long long) * 3 * b->Bp);
+      dalloc(b, &b->d_flag, sizeof(int32_t) * 4);
+      dalloc(b, &b->d_qmask, std::max(1, b->Q));
       MQO_CUDA(cudaHostAlloc(&b->h_flag, sizeof(int32_t) * 4, cudaHostAllocMapped));
       b->h_flag[2] = 0;
       MQO_CUDA(cudaStreamSynchronize(b->stream));
@@ -173,17 +177,19 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
   return guard([&] {
     if (!b) return;
     cudaSetDevice(b->g->device);
-    if (b->stream) cudaStreamSynchronize(b->stream);
-    cudaFree(b->d_x[0]);
-    cudaFree(b->d_x[1]);
-    cudaFree(b->d_v);
-    cudaFree(b->d_aux);
-    cudaFree(b->d_ctl);
-    cudaFree(b->d_viol);
-    cudaFree(b->d_chg);
-    cudaFree(b->d_flag);
-    cudaFree(b->d_qmask);
-    free_solver_buffers(b);
+    if (b->stream) {
+      dfree(b, b->d_x[0]);
+      dfree(b, b->d_x[1]);
+      dfree(b, b->d_v);
+      dfree(b, b->d_aux);
+      dfree(b, b->d_ctl);
+      dfree(b, b->d_viol);
+      dfree(b, b->d_chg);
+      dfree(b, b->d_flag);
+      dfree(b, b->d_qmask);
+      free_solver_buffers(b);
+      cudaStreamSynchronize(b->stream);
+    }
     if (b->h_flag) cudaFreeHost(b->h_flag);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;

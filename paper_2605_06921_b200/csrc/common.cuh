@@ -148,6 +148,14 @@ inline int64_t body_words(int32_t n) { return (static_cast<int64_t>(n) + 63) / 6
 }  // namespace mqo_b200
 
 // ------------------------------------------------------------- handles
+struct mqo_batch;
+namespace mqo_b200 {
+// Stream-ordered allocation of a batch buffer from the device's memory pool
+// (freed with dfree on the batch stream).
+template <typename T>
+void dalloc(mqo_batch* b, T** p, size_t bytes);
+void dfree(mqo_batch* b, void* p);
+}  // namespace mqo_b200
 struct mqo_graph {
   int device = 0;
   int32_t n = 0;
@@ -199,3 +207,15 @@ struct mqo_batch {
   int32_t* d_jdraw = nullptr;           // [Bp][n] reset draws j_i
   int32_t* d_counter = nullptr;         // [4] device counters
 };
+
+namespace mqo_b200 {
+template <typename T>
+void dalloc(mqo_batch* b, T** p, size_t bytes) {
+  void* q = nullptr;
+  MQO_CUDA(cudaMallocAsync(&q, std::max<size_t>(bytes, 1), b->stream));
+  *p = static_cast<T*>(q);
+}
+inline void dfree(mqo_batch* b, void* p) {
+  if (p) cudaFreeAsync(p, b->stream);
+}
+}  // namespace mqo_b200

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <ctime>
+#include <thread>
 
 #include "common.cuh"
 
@@ -39,6 +40,30 @@ bool trace_on() {
 
 using namespace mqo_b200;
 
+namespace {
+// Symmetry of an uploaded CSR (rows already checked sorted and in range):
+// entry e = (v, u) needs v in row u.  One thread per entry; the row of e by
+// binary search over the offsets; *bad = the smallest failing entry.
+__global__ void k_check_symmetric(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                  int32_t n, int64_t nnz, unsigned long long* bad) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < nnz;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int32_t lo = 0, hi = n - 1;  // row v: off[v] <= e < off[v + 1]
+    while (lo < hi) {
+      const int32_t mid = lo + (hi - lo + 1) / 2;
+      if (off[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    const int32_t v = lo, u = nbr[e];
+    int64_t a = off[u], b = off[u + 1];
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (nbr[mid] < v) a = mid + 1; else b = mid;
+    }
+    if (a == off[u + 1] || nbr[a] != v) atomicMin(bad, static_cast<unsigned long long>(e));
+  }
+}
+}  // namespace
+
 extern "C" const char* mqo_last_error(void) { return g_last_error.c_str(); }
 extern "C" int32_t mqo_last_error_line(void) { return g_last_error_line; }
 extern "C" const char* mqo_version(void) { return "mqo_b200 0.1 sm_100a"; }
@@ -53,41 +78,73 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
     const int64_t nnz = offsets[n];
     if (nnz < 0 || (nnz & 1)) throw std::logic_error("graph: degree sum != 2m");
     if (nnz > 0 && !neighbors) throw std::invalid_argument("mqo_graph_upload: null neighbors");
-    // Graph::check_invariants (graph.cpp:44-56) + range checks.
-    int32_t max_degree = 0;
-    for (int32_t v = 0; v < n; ++v) {
-      const int64_t b = offsets[v], e = offsets[v + 1];
-      if (e < b) throw std::logic_error("graph: offsets not monotone");
-      for (int64_t i = b; i < e; ++i) {
-        const int32_t u = neighbors[i];
-        if (u < 0 || u >= n) throw std::invalid_argument("graph: vertex index out of range");
-        if (u == v) throw std::logic_error("graph: self-loop");
-        if (i > b && neighbors[i - 1] >= u)
-          throw std::logic_error("graph: neighbor list not strictly ascending");
-      }
-      max_degree = std::max<int32_t>(max_degree, static_cast<int32_t>(e - b));
+    // Graph::check_invariants (graph.cpp:44-56) + range checks, then
+    // symmetry (u in N(v) <=> v in N(u)), which from_edges guarantees and the
+    // local-search kernels rely on.  Rows are checked in parallel chunks on
+    // host threads; the first violation in (row, entry) order is reported,
+    // invariant violations before symmetry ones, as a sequential scan would.
+    struct Bad {
+      int64_t at = INT64_MAX;  // global entry index (or row for "not monotone")
+      int kind = 0;            // 1 not monotone, 2 range, 3 self-loop, 4 not ascending
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int T = nnz > (int64_t(1) << 18) ? static_cast<int>(hw) : 1;
+    std::vector<int32_t> cut(T + 1, n);
+    cut[0] = 0;
+    for (int t = 1; t < T; ++t) {  // chunk boundaries by entries
+      const int64_t target = nnz / T * t;
+      cut[t] = static_cast<int32_t>(std::upper_bound(offsets, offsets + n + 1, target) - offsets) - 1;
+      cut[t] = std::max(cut[t], cut[t - 1]);
     }
-    // Symmetry (u in N(v) <=> v in N(u)), which from_edges guarantees and
-    // the local-search kernels rely on, in O(m): rows are sorted, so the
-    // lower entries of row u are exactly the v < u whose rows hold u, met in
-    // ascending v when the rows are walked in order.
-    {
-      std::vector<int64_t> low(static_cast<size_t>(n), 0);  // lower entries of row u matched so far
-      for (int32_t v = 0; v < n; ++v)
-        for (int64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
-          const int32_t u = neighbors[i];
-          if (u < v) continue;
-          const int64_t at = offsets[u] + low[u];
-          if (at >= offsets[u + 1] || neighbors[at] != v)
-            throw std::logic_error("graph: adjacency not symmetric");
-          ++low[u];
+    std::vector<Bad> inv(T), sym(T);
+    std::vector<int32_t> dmax(T, 0);
+    auto run = [&](auto&& body) {
+      std::vector<std::thread> th;
+      for (int t = 1; t < T; ++t) th.emplace_back(body, t);
+      body(0);
+      for (auto& x : th) x.join();
+    };
+    run([&](int t) {
+      for (int32_t v = cut[t]; v < cut[t + 1]; ++v) {
+        const int64_t b = offsets[v], e = offsets[v + 1];
+        if (e < b) {
+          inv[t] = {b, 1};
+          return;
         }
-      for (int32_t u = 0; u < n; ++u) {
-        const int64_t b = offsets[u], e = offsets[u + 1];
-        if (low[u] != (std::lower_bound(neighbors + b, neighbors + e, u) - (neighbors + b)))
-          throw std::logic_error("graph: adjacency not symmetric");
+        for (int64_t i = b; i < e; ++i) {
+          const int32_t u = neighbors[i];
+          const int kind = (u < 0 || u >= n) ? 2 : u == v ? 3 : (i > b && neighbors[i - 1] >= u) ? 4 : 0;
+          if (kind) {
+            inv[t] = {i, kind};
+            return;
+          }
+        }
+        dmax[t] = std::max<int32_t>(dmax[t], static_cast<int32_t>(e - b));
       }
+    });
+    for (const Bad& x : inv) {
+      if (x.kind == 1) throw std::logic_error("graph: offsets not monotone");
+      if (x.kind == 2) throw std::invalid_argument("graph: vertex index out of range");
+      if (x.kind == 3) throw std::logic_error("graph: self-loop");
+      if (x.kind == 4) throw std::logic_error("graph: neighbor list not strictly ascending");
     }
+    const int32_t max_degree = *std::max_element(dmax.begin(), dmax.end());
+    MQO_TRACE("graph upload: invariants checked (%d threads)", T);
+    if (device < 0) {  // host-only graph: symmetry on the host threads
+      run([&](int t) {
+        for (int32_t v = cut[t]; v < cut[t + 1]; ++v)
+          for (int64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
+            const int32_t u = neighbors[i];
+            if (!std::binary_search(neighbors + offsets[u], neighbors + offsets[u + 1], v)) {
+              sym[t] = {i, 5};
+              return;
+            }
+          }
+      });
+      for (const Bad& x : sym)
+        if (x.kind) throw std::logic_error("graph: adjacency not symmetric");
+      MQO_TRACE("graph upload: symmetry checked");
+    }  // device graphs: k_check_symmetric after the upload below
     auto* g = new mqo_graph;
     g->device = device;
     g->n = n;
@@ -110,6 +167,7 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
       for (int32_t v = 0; v < n; ++v)
         order[count[max_degree - (offsets[v + 1] - offsets[v])]++] = v;
     }
+    MQO_TRACE("graph upload: host copies + row order");
     g->h_deg_ge.assign(static_cast<size_t>(max_degree) + 2, 0);
     for (int32_t v = 0; v < n; ++v) ++g->h_deg_ge[static_cast<size_t>(offsets[v + 1] - offsets[v])];
     for (int64_t d = max_degree; d >= 0; --d) g->h_deg_ge[d] += g->h_deg_ge[d + 1];
@@ -128,6 +186,22 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
       if (n)
         MQO_CUDA(cudaMemcpy(g->d_order, order.data(), sizeof(int32_t) * n,
                             cudaMemcpyHostToDevice));
+      if (nnz) {  // symmetry, one thread per entry on the device
+        unsigned long long* d_bad = nullptr;
+        MQO_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+        const unsigned long long none = ~0ull;
+        MQO_CUDA(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
+        k_check_symmetric<<<static_cast<int>(std::min<int64_t>((nnz + 255) / 256, 148 * 64)), 256>>>(
+            g->d_off, g->d_nbr, n, nnz, d_bad);
+        unsigned long long bad = 0;
+        const cudaError_t e1 = cudaGetLastError();
+        const cudaError_t e2 = cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
+        cudaFree(d_bad);
+        MQO_CUDA(e1);
+        MQO_CUDA(e2);
+        if (bad != ~0ull) throw std::logic_error("graph: adjacency not symmetric");
+        MQO_TRACE("graph upload: symmetry checked on the device");
+      }
     } catch (...) {
       mqo_graph_free(g);
       throw;

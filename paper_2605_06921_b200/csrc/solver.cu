@@ -522,7 +522,7 @@ void launch_cut(mqo_batch* b, const double* X) {
   const mqo_graph* g = b->g;
   const int32_t words = ((b->B + 31) / 32 + 3) / 4 * 4;
   if (!b->d_sides)
-    MQO_CUDA(cudaMalloc(&b->d_sides, sizeof(uint32_t) * std::max<int64_t>(1, int64_t(g->n) * words)));
+    dalloc(b, &b->d_sides, sizeof(uint32_t) * std::max<int64_t>(1, int64_t(g->n) * words));
   k_side_bits<<<grid_for(int64_t(g->n) * words * 32), 256, 0, b->stream>>>(X, g->n, b->B, b->Bp,
                                                                           words, b->d_sides);
   MQO_CUDA(cudaGetLastError());
@@ -535,27 +535,27 @@ void ensure_solver_buffers(mqo_batch* b) {
   const mqo_graph* g = b->g;
   const int64_t W = body_words(g->n);
   if (!b->d_rng) {
-    MQO_CUDA(cudaMalloc(&b->d_rng, sizeof(ChainRng) * b->Bp * 2));  // [0]: live, [Bp]: saved
+    dalloc(b, &b->d_rng, sizeof(ChainRng) * b->Bp * 2);  // [0]: live, [Bp]: saved
     // on the batch stream: a legacy-stream memset is not ordered with the
     // (non-blocking) batch stream and could land after the seeding copy
     MQO_CUDA(cudaMemsetAsync(b->d_rng, 0, sizeof(ChainRng) * b->Bp * 2, b->stream));
   }
   if (!b->d_bodies) {
-    MQO_CUDA(cudaMalloc(&b->d_bodies, sizeof(uint64_t) * std::max<int64_t>(1, W * b->Bp)));
-    MQO_CUDA(cudaMalloc(&b->d_scores, sizeof(int64_t) * b->Bp));
-    MQO_CUDA(cudaMalloc(&b->d_valid, sizeof(int32_t) * b->Bp));
-    MQO_CUDA(cudaMalloc(&b->d_pick, sizeof(int32_t) * b->Bp));
-    MQO_CUDA(cudaMalloc(&b->d_counter, sizeof(int32_t) * 4));
+    dalloc(b, &b->d_bodies, sizeof(uint64_t) * std::max<int64_t>(1, W * b->Bp));
+    dalloc(b, &b->d_scores, sizeof(int64_t) * b->Bp);
+    dalloc(b, &b->d_valid, sizeof(int32_t) * b->Bp);
+    dalloc(b, &b->d_pick, sizeof(int32_t) * b->Bp);
+    dalloc(b, &b->d_counter, sizeof(int32_t) * 4);
   }
   if (!b->d_state8)
-    MQO_CUDA(cudaMalloc(&b->d_state8, std::max<int64_t>(1, int64_t(g->n) * b->Bp)));
+    dalloc(b, &b->d_state8, std::max<int64_t>(1, int64_t(g->n) * b->Bp));
 }
 
 void ensure_reset_buffers(mqo_batch* b) {
   const int64_t cells = std::max<int64_t>(1, int64_t(b->g->n) * b->B);
   if (!b->d_lastw) {
-    MQO_CUDA(cudaMalloc(&b->d_lastw, sizeof(int32_t) * cells));
-    MQO_CUDA(cudaMalloc(&b->d_jdraw, sizeof(int32_t) * cells));
+    dalloc(b, &b->d_lastw, sizeof(int32_t) * cells);
+    dalloc(b, &b->d_jdraw, sizeof(int32_t) * cells);
   }
 }
 
@@ -564,17 +564,17 @@ void ensure_reset_buffers(mqo_batch* b) {
 namespace mqo_b200 {
 
 void free_solver_buffers(mqo_batch* b) {
-  cudaFree(b->d_rng);
-  cudaFree(b->d_pool);
-  cudaFree(b->d_bodies);
-  cudaFree(b->d_scores);
-  cudaFree(b->d_valid);
-  cudaFree(b->d_pick);
-  cudaFree(b->d_state8);
-  cudaFree(b->d_sides);
-  cudaFree(b->d_lastw);
-  cudaFree(b->d_jdraw);
-  cudaFree(b->d_counter);
+  dfree(b, b->d_rng);
+  dfree(b, b->d_pool);
+  dfree(b, b->d_bodies);
+  dfree(b, b->d_scores);
+  dfree(b, b->d_valid);
+  dfree(b, b->d_pick);
+  dfree(b, b->d_state8);
+  dfree(b, b->d_sides);
+  dfree(b, b->d_lastw);
+  dfree(b, b->d_jdraw);
+  dfree(b, b->d_counter);
 }
 
 // K3 on the device; Box-Muller's log / sincos are the bit-exact replays of
@@ -785,9 +785,9 @@ extern "C" int mqo_set_pool(mqo_batch* b, int32_t count, const uint64_t* packed)
     MQO_CUDA(cudaSetDevice(b->g->device));
     const int64_t W = body_words(b->g->n);
     if (count > b->pool_cap) {
-      cudaFree(b->d_pool);
+      dfree(b, b->d_pool);
       b->d_pool = nullptr;
-      MQO_CUDA(cudaMalloc(&b->d_pool, sizeof(uint64_t) * std::max<int64_t>(1, W * count)));
+      dalloc(b, &b->d_pool, sizeof(uint64_t) * std::max<int64_t>(1, W * count));
       b->pool_cap = count;
     }
     if (count)

@@ -57,3 +57,14 @@ def test_init_state_host_golden():
     st[0]["s"] = words
     x, _ = P.init_state_host(pg, 0, 0.15, st[0])
     assert np.array_equal(x.view(np.uint64), z["init_mis_0.15"].view(np.uint64))
+
+
+def test_upload_rejects_asymmetric_csr():
+    """A one-sided CSR (u in N(v) but v not in N(u)) is rejected at upload
+    (ADVICE r1): the local-search kernels rely on symmetry, and the
+    reference's Graph can only come from from_edges."""
+    import paper_2605_06921_b200 as P
+    with pytest.raises(P.LogicError, match="adjacency not symmetric"):
+        P.Graph.from_csr([0, 1, 2, 3, 4], [1, 2, 3, 0], device=-1)
+    g = P.Graph.from_csr([0, 1, 2], [1, 0], device=-1)  # the symmetric edge is fine
+    assert g.m() == 1
