@@ -212,7 +212,7 @@ def run_solve(a) -> dict:
                          "iterations": rep.total_iterations},
             "stop": P.StopReason.names[rep.last_trajectory_stop],
             "timing": {"solve_secs": rep.elapsed_secs, "graph_load_secs": load_secs},
-            "warnings": warnings, "backend": "b200"}
+            "warnings": warnings}
 
 
 def rescore(g, problem: str, bits: np.ndarray) -> int:

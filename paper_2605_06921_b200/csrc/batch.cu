@@ -162,7 +162,7 @@ extern "C" int mqo_batch_create(mqo_graph* g, int32_t chains, mqo_batch** out) {
       dalloc(b, &b->d_chg, sizeof(unsigned long long) * 3 * b->Bp);
       dalloc(b, &b->d_flag, sizeof(int32_t) * 4);
       dalloc(b, &b->d_qmask, std::max(1, b->Q));
-      MQO_CUDA(cudaHostAlloc(&b->h_flag, sizeof(int32_t) * 4, cudaHostAllocMapped));
+      b->h_flag = static_cast<int32_t*>(pinned_get(sizeof(int32_t) * 4));
       b->h_flag[2] = 0;
       MQO_CUDA(cudaStreamSynchronize(b->stream));
     } catch (...) {
@@ -190,7 +190,7 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
       free_solver_buffers(b);
       cudaStreamSynchronize(b->stream);
     }
-    if (b->h_flag) cudaFreeHost(b->h_flag);
+    pinned_put(b->h_flag, sizeof(int32_t) * 4);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;
   });

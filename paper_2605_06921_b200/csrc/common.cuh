@@ -150,6 +150,12 @@ inline int64_t body_words(int32_t n) { return (static_cast<int64_t>(n) + 63) / 6
 // ------------------------------------------------------------- handles
 struct mqo_batch;
 namespace mqo_b200 {
+// mem.cu: pinned host blocks from a process-wide cache (mapped, portable),
+// and the per-device stream graph arrays are allocated / freed on
+void* pinned_get(size_t bytes);
+void pinned_put(void* p, size_t bytes);
+cudaStream_t mem_stream(int device);
+void keep_pool_memory(int device);
 // Stream-ordered allocation of a batch buffer from the device's memory pool
 // (freed with dfree on the batch stream).
 template <typename T>

@@ -201,9 +201,7 @@ struct Engine {
   int rank_id = -1;      // Mode R: the outer rank of this shard engine
   uint64_t* stage = nullptr;  // pinned staging for local-search bodies
   size_t stage_words = 0;
-  ~Engine() {
-    if (stage) cudaFreeHost(stage);
-  }
+  ~Engine() { pinned_put(stage, sizeof(uint64_t) * stage_words); }
   mqo_batch* batch = nullptr;
   TopKPool pool;
   Entry best;
@@ -417,9 +415,8 @@ struct Engine {
     // one pinned staging buffer: [count][W] bodies + [count] outputs
     const size_t words = static_cast<size_t>(count) * W;
     if (stage_words < words + count) {
-      if (stage) cudaFreeHost(stage);
-      stage = nullptr;
-      MQO_CUDA(cudaMallocHost(&stage, sizeof(uint64_t) * (words + count)));
+      pinned_put(stage, sizeof(uint64_t) * stage_words);
+      stage = static_cast<uint64_t*>(pinned_get(sizeof(uint64_t) * (words + count)));
       stage_words = words + count;
     }
     for (int i = 0; i < count; ++i) std::copy(members[i].body.begin(), members[i].body.end(), stage + i * W);

@@ -177,31 +177,39 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
     }
     try {
       MQO_CUDA(cudaSetDevice(device));
-      MQO_CUDA(cudaMalloc(&g->d_off, sizeof(int64_t) * (n + 1)));
-      MQO_CUDA(cudaMalloc(&g->d_nbr, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
-      MQO_CUDA(cudaMalloc(&g->d_order, sizeof(int32_t) * std::max<int32_t>(n, 1)));
-      MQO_CUDA(cudaMemcpy(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+      // stream-ordered pool allocations on the device's memory stream
+      // (mem.cu): no page mapping per upload, no device-wide sync per free
+      const cudaStream_t ms = mem_stream(device);
+      void* p = nullptr;
+      MQO_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), ms));
+      g->d_off = static_cast<int64_t*>(p);
+      MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), ms));
+      g->d_nbr = static_cast<int32_t*>(p);
+      MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int32_t>(n, 1) + 16, ms));
+      g->d_order = static_cast<int32_t*>(p);
+      MQO_CUDA(cudaMemcpyAsync(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ms));
       if (nnz)
-        MQO_CUDA(cudaMemcpy(g->d_nbr, neighbors, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+        MQO_CUDA(cudaMemcpyAsync(g->d_nbr, neighbors, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, ms));
       if (n)
-        MQO_CUDA(cudaMemcpy(g->d_order, order.data(), sizeof(int32_t) * n,
-                            cudaMemcpyHostToDevice));
-      if (nnz) {  // symmetry, one thread per entry on the device
-        unsigned long long* d_bad = nullptr;
-        MQO_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
-        const unsigned long long none = ~0ull;
-        MQO_CUDA(cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice));
-        k_check_symmetric<<<static_cast<int>(std::min<int64_t>((nnz + 255) / 256, 148 * 64)), 256>>>(
+        MQO_CUDA(cudaMemcpyAsync(g->d_order, order.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ms));
+      // symmetry, one thread per entry on the device; the flag word rides
+      // behind the order array
+      unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(
+          reinterpret_cast<char*>(g->d_order) + (sizeof(int32_t) * std::max<int32_t>(n, 1) + 7) / 8 * 8);
+      MQO_CUDA(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), ms));
+      if (nnz)
+        k_check_symmetric<<<static_cast<int>(std::min<int64_t>((nnz + 255) / 256, 148 * 64)), 256, 0, ms>>>(
             g->d_off, g->d_nbr, n, nnz, d_bad);
-        unsigned long long bad = 0;
-        const cudaError_t e1 = cudaGetLastError();
-        const cudaError_t e2 = cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost);
-        cudaFree(d_bad);
-        MQO_CUDA(e1);
-        MQO_CUDA(e2);
-        if (bad != ~0ull) throw std::logic_error("graph: adjacency not symmetric");
-        MQO_TRACE("graph upload: symmetry checked on the device");
-      }
+      MQO_CUDA(cudaGetLastError());
+      unsigned long long* h_bad = static_cast<unsigned long long*>(pinned_get(sizeof(unsigned long long)));
+      const cudaError_t e1 = cudaMemcpyAsync(h_bad, d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ms);
+      const cudaError_t e2 = cudaStreamSynchronize(ms);
+      const unsigned long long bad = *h_bad;
+      pinned_put(h_bad, sizeof(unsigned long long));
+      MQO_CUDA(e1);
+      MQO_CUDA(e2);
+      if (bad != ~0ull) throw std::logic_error("graph: adjacency not symmetric");
+      MQO_TRACE("graph upload: on the device, symmetry checked");
     } catch (...) {
       mqo_graph_free(g);
       throw;
@@ -213,12 +221,14 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
 extern "C" int mqo_graph_free(mqo_graph* g) {
   return guard([&] {
     if (!g) return;
-    if (g->device >= 0) cudaSetDevice(g->device);
-    cudaFree(g->d_off);
-    cudaFree(g->d_nbr);
-    cudaFree(g->d_order);
-    cudaFree(g->d_cta);
-    cudaFree(g->d_hmax);
+    if (g->device >= 0) {  // the graph outlives its batches: no kernel still reads it
+      cudaSetDevice(g->device);
+      const cudaStream_t ms = mem_stream(g->device);
+      for (void* p : {static_cast<void*>(g->d_off), static_cast<void*>(g->d_nbr),
+                      static_cast<void*>(g->d_order), static_cast<void*>(g->d_cta),
+                      static_cast<void*>(g->d_hmax)})
+        if (p) cudaFreeAsync(p, ms);
+    }
     delete g;
   });
 }

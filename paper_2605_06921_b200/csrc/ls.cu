@@ -1992,7 +1992,13 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
       std::lock_guard<std::mutex> lock(g->lazy_mu);
       if (!g->d_hmax) {  // once per graph, complete before any stream uses it
         int32_t* h = nullptr;
-        MQO_CUDA(cudaMalloc(&h, sizeof(int32_t) * std::max(n, 1)));
+        {  // pool allocation on the graph's memory stream (freed there with the graph)
+          const cudaStream_t ms = mem_stream(g->device);
+          void* p = nullptr;
+          MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max(n, 1), ms));
+          MQO_CUDA(cudaStreamSynchronize(ms));
+          h = static_cast<int32_t*>(p);
+        }
         k_hmax<<<ls_grid(n), 256, 0, st>>>(g->d_off, g->d_nbr, n, h);
         MQO_CUDA(cudaGetLastError());
         MQO_CUDA(cudaStreamSynchronize(st));

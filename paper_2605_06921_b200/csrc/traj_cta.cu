@@ -454,7 +454,13 @@ void ensure_cta_layout(mqo_graph* g) {
     for (int64_t e = g->h_off[v], k = 0; e < g->h_off[v + 1]; ++e, ++k)
       lay[static_cast<size_t>(base + 32 * k)] = slot[g->h_nbr[e]];
   }
-  MQO_CUDA(cudaMalloc(&g->d_cta, sizeof(int32_t) * lay.size()));
+  {  // pool allocation on the graph's memory stream (freed there with the graph)
+    const cudaStream_t ms = mem_stream(g->device);
+    void* p = nullptr;
+    MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * lay.size(), ms));
+    MQO_CUDA(cudaStreamSynchronize(ms));
+    g->d_cta = static_cast<int32_t*>(p);
+  }
   MQO_CUDA(cudaMemcpy(g->d_cta, lay.data(), sizeof(int32_t) * lay.size(), cudaMemcpyHostToDevice));
   g->cta_words = words;  // ELL end (the tail follows)
   g->h_cta_base.assign(lay.begin() + n, lay.begin() + n + S);
