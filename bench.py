@@ -444,10 +444,7 @@ def e2e_solve(args, P, _lib, c, g, rank, world, local_rank, maxed, summed):
                          seed=oc.seed, local_search=oc.local_search,
                          pool_batch=B_rank * world, pool_keep=oc.pool_keep,
                          max_outer_loops=oc.max_outer_loops)
-    comm = None
-    if world > 1:
-        from paper_2605_06921_b200.dist import nccl_comm
-        comm = nccl_comm(local_rank)
+    comm = make_comm(world, local_rank)
 
     def once():
         h = C.c_void_p()
@@ -495,7 +492,7 @@ def e2e_solve(args, P, _lib, c, g, rank, world, local_rank, maxed, summed):
             all(rep[k] == gold[k] for k in rep) and
             d["body_sha256"] == str(z[args.config + "_body_sha"]))
         out["reference_golden_wall_s"] = float(z[args.config + "_elapsed"][0])
-    if comm is not None:
+    if comm is not None and hasattr(comm, "close"):
         comm.close()
     return out
 
@@ -529,23 +526,38 @@ def e2e_trajectories(args, P, _lib, c, g, world, maxed, summed):
             "kind": "run_trajectories (max_iters 100, host x in / out)"}
 
 
+def torch_device():
+    import torch
+    return torch.cuda.current_device()
+
+
+def make_comm(world, device):
+    """The engine's communicator at N > 1: the library's native NCCL
+    communicator (one rank per GPU); under the gloo test hook (ranks sharing
+    a GPU, where NCCL refuses) the torch.distributed adapter."""
+    if world == 1:
+        return None
+    if os.environ.get("MQO_BENCH_BACKEND", "nccl") == "nccl":
+        from paper_2605_06921_b200.dist import nccl_comm
+        return nccl_comm(device)
+    from paper_2605_06921_b200.dist import TorchComm
+    return TorchComm()
+
+
 def ttq_solve(args, P, g, rank, world, maxed):
     cfg = P.SolverConfig(objective=P.PerturbedBias(0.001),
                          optimizer=P.OptimizerConfig(0.0025, 0.8),
                          reset_fraction=0.8, reset_rounds=90, seed=1,
                          time_budget_secs=args.ttq_secs, pool_batch=TTQ_CHAINS * world,
                          pool_keep=8)
-    comm = None
-    if world > 1:
-        from paper_2605_06921_b200.dist import nccl_comm
-        comm = nccl_comm()
+    comm = make_comm(world, torch_device())
     t0 = time.perf_counter()
     if world == 1:
         r = P.solve_pooled(g, cfg)
     else:
         r, _ = P.solve_replicas(g, cfg, comm=comm)
     wall = maxed(time.perf_counter() - t0)
-    if comm is not None:
+    if comm is not None and hasattr(comm, "close"):
         comm.close()
     return {"budget_s": args.ttq_secs, "best_cut": int(r.best_score), "wall_s": wall,
             "chains": TTQ_CHAINS * world, "trajectories": r.trajectories,

@@ -55,6 +55,11 @@ const bool g_scan_multi = [] {
   return !(e && *e == '0');
 }();
 
+const int g_scan_c = [] {
+  const char* e = std::getenv("MQO_SCAN_C");
+  return e ? std::atoi(e) : 8;
+}();
+
 __device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 1; }
 
 // ---------------------------------------------------------------- MaxCut
@@ -818,7 +823,7 @@ __device__ void warp_mark_after_flip2(const int64_t* off, const int32_t* nbr, ui
 }
 
 template <int NW, int C>
-__global__ void __launch_bounds__(32 * NW)
+__global__ void __launch_bounds__(32 * NW, 1)
     k_two_scan_multi(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
                      const int32_t* __restrict__ hmax, int32_t n, int32_t count,
                      uint8_t* side_all, int32_t* delta_all, uint8_t* cand_all,
@@ -1772,9 +1777,11 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
             d_cand, mask);
       if (g_scan_multi) {
         MQO_CUDA(cudaMemsetAsync(d_next, 0, cells, st));
-        k_two_scan_multi<32, 4><<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,
-                                                           side, delta, d_cand, d_next, d_live2,
-                                                           d_g2, d_stats);
+        // candidates per step = 32 warps x C (MQO_SCAN_C = 4 | 8 | 16)
+        auto kern = g_scan_c == 4 ? k_two_scan_multi<32, 4>
+                    : g_scan_c == 16 ? k_two_scan_multi<32, 16> : k_two_scan_multi<32, 8>;
+        kern<<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side, delta,
+                                        d_cand, d_next, d_live2, d_g2, d_stats);
       }
       else if (g_scan_cta == 16)
         k_two_scan_cta<16><<<count, 32 * 16, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count,

@@ -96,7 +96,8 @@ struct Tune {
   static constexpr int MINB = MINB_;
   static constexpr int MEM = MEM_;
   static constexpr bool HINT = MEM_ != 0;  // 256-bit path
-  static constexpr bool POLICY = MEM_ == 1;
+  static constexpr bool POLICY = MEM_ == 1 || MEM_ == 3;
+  static constexpr bool L2_64B = MEM_ == 3;  // neighbour gathers with the L2::64B fetch size
 };
 // Measured on B200 (scripts/tune_k1.py, profiles/r01_tune_k1.txt): 4
 // neighbours in flight x 3 CTAs/SM for the MaxCut objectives, 3 x 4 CTAs/SM
@@ -110,7 +111,7 @@ using TuneFor = std::conditional_t<KIND == MQO_MIS_QUBO, TuneMis, TuneDefault>;
 // streamed access (own row, velocity, stores) L2::evict_first, and nothing
 // allocates in L1 (random gathers have no L1 reuse).  One 256-bit access
 // per lane covers its 4 chains (one 32-byte sector).
-enum Pol : int { kPolNormal = 0, kPolLast = 1, kPolFirst = 2 };
+enum Pol : int { kPolNormal = 0, kPolLast = 1, kPolFirst = 2, kPolNormal64 = 3, kPolLast64 = 4 };
 
 template <int POL>
 __device__ __forceinline__ void ld4(const double* p, double (&o)[4]) {
@@ -119,6 +120,12 @@ __device__ __forceinline__ void ld4(const double* p, double (&o)[4]) {
                  : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
   else if constexpr (POL == kPolFirst)
     asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+  else if constexpr (POL == kPolNormal64)
+    asm volatile("ld.global.L1::no_allocate.L2::64B.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
+  else if constexpr (POL == kPolLast64)
+    asm volatile("ld.global.L1::no_allocate.L2::evict_last.L2::64B.v4.f64 {%0,%1,%2,%3}, [%4];"
                  : "=d"(o[0]), "=d"(o[1]), "=d"(o[2]), "=d"(o[3]) : "l"(p));
   else
     asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -218,9 +225,9 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
         const double* src = X + static_cast<int64_t>(us[j]) * a.Bp + col;
         if constexpr (HINT) {
           if (TU::POLICY && us[j] < a.hot_rows)
-            ld4<kPolLast>(src, val[j]);
+            ld4<TU::L2_64B ? kPolLast64 : kPolLast>(src, val[j]);
           else
-            ld4<kPolNormal>(src, val[j]);
+            ld4<TU::L2_64B ? kPolNormal64 : kPolNormal>(src, val[j]);
         } else {
           ldx<CPL>(src, val[j]);
         }
@@ -793,6 +800,8 @@ PassFn pass_fn(int kind, int cpl) {
       case 6: return pass_fn_tu<MODE, Tune<4, 3, 1>>(kind, cpl);
       case 7: return pass_fn_tu<MODE, Tune<7, 3, 1>>(kind, cpl);
       case 8: return pass_fn_tu<MODE, Tune<3, 4, 1>>(kind, cpl);
+      case 9: return pass_fn_tu<MODE, Tune<4, 3, 3>>(kind, cpl);   // L2::64B gathers
+      case 10: return pass_fn_tu<MODE, Tune<3, 4, 3>>(kind, cpl);
       default: break;
     }
   }

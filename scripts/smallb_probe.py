@@ -21,10 +21,13 @@ def main():
     ap.add_argument("--chains", default="4,8,16,32,64,128")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--traj", type=int, default=50, help="trajectory iterations (0: skip)")
+    ap.add_argument("--variant", type=int, default=0, help="mqo_tune k1_variant")
     args = ap.parse_args()
     import torch
     import paper_2605_06921_b200 as P
     c = bench.CONFIGS[args.graph]
+    if args.variant:
+        P.tune("k1_variant", args.variant)
     peak, _ = bench.load_peaks()
     g = bench.our_graph(P, c["graph"])
     n, nnz = g.n(), 2 * g.m()
