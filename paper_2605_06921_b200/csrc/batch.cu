@@ -188,8 +188,10 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
       dfree(b, b->d_flag);
       dfree(b, b->d_qmask);
       free_solver_buffers(b);
+      dfree(b, b->d_ls);
       cudaStreamSynchronize(b->stream);
     }
+    pinned_put(b->h_ls, b->ls_bytes);
     pinned_put(b->h_flag, sizeof(int32_t) * 4);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;

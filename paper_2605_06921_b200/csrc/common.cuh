@@ -212,6 +212,9 @@ struct mqo_batch {
   int32_t* d_lastw = nullptr;           // [Bp][n] reset scratch
   int32_t* d_jdraw = nullptr;           // [Bp][n] reset draws j_i
   int32_t* d_counter = nullptr;         // [4] device counters
+  uint64_t* d_ls = nullptr;             // mqo_local_search staging (device, grow-only)
+  uint64_t* h_ls = nullptr;             // ... and its pinned host mirror
+  size_t ls_bytes = 0;
 };
 
 namespace mqo_b200 {

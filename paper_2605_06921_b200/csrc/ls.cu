@@ -1390,60 +1390,12 @@ __device__ __forceinline__ void cta_copy(void* dst, const void* src, int64_t byt
 // per CTA) the CSR, selection, tightness and dirty list are staged in SMEM
 // first: the scan is a chain of dependent loads, ~30-cycle SMEM latency
 // instead of ~300+ for L2.  Generic pointers serve both placements.
-__global__ void k_mis_swap(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
-                           int32_t n, int32_t count, uint8_t* sel_all, int32_t* tight_all,
-                           uint8_t* dflag_all, int32_t* dlist_all, int32_t* freed_all,
-                           int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out,
-                           int32_t smem) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int lane = threadIdx.x & 31;
-  const int s = smem ? blockIdx.x : blockIdx.x * kLsWarps + (threadIdx.x >> 5);
-  if (s >= count) return;
-  uint8_t* sel_g = sel_all + static_cast<int64_t>(s) * n;
-  const int64_t* off = off_g;
-  const int32_t* nbr = nbr_g;
-  uint8_t* sel = sel_g;
-  int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
-  uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
-  int32_t* dlist = dlist_all + static_cast<int64_t>(s) * n;
-  int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
-  int32_t* dcount = dcount_all + s;
-  if (smem) {
-    auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
-    const int64_t nnz = off_g[n];
-    unsigned char* p = sm;
-    int64_t* o = reinterpret_cast<int64_t*>(p);
-    p += al(8 * (int64_t(n) + 1));
-    int32_t* nb = reinterpret_cast<int32_t*>(p);
-    p += al(4 * nnz);
-    int32_t* ti = reinterpret_cast<int32_t*>(p);
-    p += al(4 * int64_t(n));
-    int32_t* dl = reinterpret_cast<int32_t*>(p);
-    p += al(4 * int64_t(n));
-    int32_t* fr = reinterpret_cast<int32_t*>(p);
-    p += al(4 * (int64_t(max_degree) + 1));
-    uint8_t* se = p;
-    p += al(n);
-    uint8_t* df = p;
-    p += al(int64_t(n) + 4);
-    int32_t* dc = reinterpret_cast<int32_t*>(p);
-    cta_copy(o, off_g, 8 * (int64_t(n) + 1));
-    cta_copy(nb, nbr_g, 4 * nnz);
-    cta_copy(ti, tight, 4 * int64_t(n));
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) se[i] = sel_g[i];
-    for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) df[i] = 0;
-    if (threadIdx.x == 0) *dc = 0;
-    __syncthreads();
-    if (threadIdx.x >= 32) return;  // the other warps only helped stage
-    off = o;
-    nbr = nb;
-    sel = se;
-    tight = ti;
-    dflag = df;
-    dlist = dl;
-    freed = fr;
-    dcount = dc;
-  }
+// one_two_swap's scan (localsearch.cpp:88-137) on one warp: the lowest
+// swappable vertex among the dirty ones, else the next from the frontier;
+// returns the number of swaps.  Shared by k_mis_swap and k_swap_small.
+__device__ int64_t warp_swap_loop(const int64_t* off, const int32_t* nbr, uint8_t* sel,
+                                  int32_t* tight, uint8_t* dflag, int32_t* dlist,
+                                  int32_t* dcount, int32_t* freed, int32_t n, int lane) {
   int32_t frontier = 0;
   int64_t swaps = 0;
   for (;;) {
@@ -1515,6 +1467,64 @@ __global__ void k_mis_swap(const int64_t* __restrict__ off_g, const int32_t* __r
                     frontier, lane);
     ++swaps;
   }
+  return swaps;
+}
+
+__global__ void k_mis_swap(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
+                           int32_t n, int32_t count, uint8_t* sel_all, int32_t* tight_all,
+                           uint8_t* dflag_all, int32_t* dlist_all, int32_t* freed_all,
+                           int32_t* dcount_all, int32_t max_degree, int64_t* swaps_out,
+                           int32_t smem) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int lane = threadIdx.x & 31;
+  const int s = smem ? blockIdx.x : blockIdx.x * kLsWarps + (threadIdx.x >> 5);
+  if (s >= count) return;
+  uint8_t* sel_g = sel_all + static_cast<int64_t>(s) * n;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  uint8_t* sel = sel_g;
+  int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
+  uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
+  int32_t* dlist = dlist_all + static_cast<int64_t>(s) * n;
+  int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
+  int32_t* dcount = dcount_all + s;
+  if (smem) {
+    auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+    const int64_t nnz = off_g[n];
+    unsigned char* p = sm;
+    int64_t* o = reinterpret_cast<int64_t*>(p);
+    p += al(8 * (int64_t(n) + 1));
+    int32_t* nb = reinterpret_cast<int32_t*>(p);
+    p += al(4 * nnz);
+    int32_t* ti = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* dl = reinterpret_cast<int32_t*>(p);
+    p += al(4 * int64_t(n));
+    int32_t* fr = reinterpret_cast<int32_t*>(p);
+    p += al(4 * (int64_t(max_degree) + 1));
+    uint8_t* se = p;
+    p += al(n);
+    uint8_t* df = p;
+    p += al(int64_t(n) + 4);
+    int32_t* dc = reinterpret_cast<int32_t*>(p);
+    cta_copy(o, off_g, 8 * (int64_t(n) + 1));
+    cta_copy(nb, nbr_g, 4 * nnz);
+    cta_copy(ti, tight, 4 * int64_t(n));
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) se[i] = sel_g[i];
+    for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) df[i] = 0;
+    if (threadIdx.x == 0) *dc = 0;
+    __syncthreads();
+    if (threadIdx.x >= 32) return;  // the other warps only helped stage
+    off = o;
+    nbr = nb;
+    sel = se;
+    tight = ti;
+    dflag = df;
+    dlist = dl;
+    freed = fr;
+    dcount = dc;
+  }
+  const int64_t swaps = warp_swap_loop(off, nbr, sel, tight, dflag, dlist, dcount, freed, n, lane);
   if (lane == 0) swaps_out[s] = swaps;
   if (smem) {
     __syncwarp();
@@ -1950,10 +1960,348 @@ void launch_swap_cta(const mqo_graph* g, int32_t count, LsWork& w, int64_t* d_ou
   MQO_CUDA(cudaGetLastError());
 }
 
+// ---- single-launch local search for small bodies -------------------------
+// One call on one small body used to cost ~60 us before any work (workspace
+// allocations, unpack / gain / candidate / scan / pack launches, host round
+// trips between sweeps) -- more than the reference's whole scalar pass at
+// n = 1024.  These kernels do the complete operation in ONE launch, one CTA
+// per body, from the packed bodies to the packed bodies and the result:
+// unpack into SMEM, gain / tightness tables built by every thread, the
+// reference's sequential scans on one warp (a ballot finds the next move
+// among 32 vertices, the warp applies it; the other warps idle at the next
+// barrier), pack.  The CSR is staged in SMEM when it fits next to the state.
+constexpr int kSmallThreads = 512;
+constexpr int64_t kSmallSmemMax = 226 * 1024;
+constexpr int32_t kSmallMaxN = 16384;
+
+__device__ __forceinline__ void small_unpack(const uint64_t* __restrict__ packed, int64_t W,
+                                             int32_t n, uint8_t* dst) {
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+    dst[v] = static_cast<uint8_t>((packed[v >> 6] >> (63 - (v & 63))) & 1u);
+}
+__device__ __forceinline__ void small_pack(const uint8_t* src, int64_t W, int32_t n,
+                                           uint64_t* packed) {
+  for (int64_t w = threadIdx.x; w < W; w += blockDim.x) {
+    uint64_t word = 0;
+    for (int b = 0; b < 64; ++b) {
+      const int64_t v = w * 64 + b;
+      if (v < n && src[v]) word |= 1ull << (63 - b);
+    }
+    packed[w] = word;
+  }
+}
+
+// build_gain_table (localsearch.cpp:17-26), all threads
+__device__ __forceinline__ void small_gains(const int64_t* off, const int32_t* nbr, int32_t n,
+                                            const uint8_t* side, int32_t* delta) {
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+    const uint8_t sv = side[v];
+    int32_t same = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) same += side[nbr[e]] == sv ? 1 : -1;
+    delta[v] = same;
+  }
+}
+
+// apply_flip (localsearch.cpp:28-33) by one warp
+__device__ __forceinline__ void small_flip(const int64_t* off, const int32_t* nbr, uint8_t* side,
+                                           int32_t* delta, int32_t v, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    side[v] ^= 1;
+    delta[v] = -delta[v];
+  }
+  __syncwarp();
+  const uint8_t sv = side[v];
+  for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+    const int32_t u = nbr[e];
+    delta[u] += side[u] == sv ? 2 : -2;
+  }
+  __syncwarp();
+}
+
+// one_flip_pass (localsearch.cpp:139-157) on warp 0; every thread calls it
+__device__ long long small_one_flip(const int64_t* off, const int32_t* nbr, int32_t n,
+                                    uint8_t* side, int32_t* delta) {
+  const int lane = threadIdx.x & 31;
+  small_gains(off, nbr, n, side, delta);
+  __syncthreads();
+  long long total = 0;
+  if (threadIdx.x < 32) {
+    volatile int32_t* vd = delta;
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (int32_t c = 0; c < n; c += 32) {
+        unsigned done = 0;  // lanes already passed in this chunk
+        for (;;) {
+          const int32_t v = c + lane;
+          const bool ok = v < n && vd[v] > 0;
+          const unsigned m = __ballot_sync(0xffffffffu, ok) & ~done;
+          if (!m) break;
+          const int j = warp_first(m);
+          const int32_t u = c + j;
+          total += vd[u];
+          small_flip(off, nbr, side, delta, u, lane);
+          improved = true;
+          done = j == 31 ? ~0u : (2u << j) - 1u;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
+// two_flip_pass (localsearch.cpp:159-181) on warp 0; hmax[v] bounds delta_u
+// of v's higher neighbours (rows that cannot hit are skipped)
+__device__ long long small_two_flip(const int64_t* off, const int32_t* nbr,
+                                    const int32_t* __restrict__ hmax, int32_t n, uint8_t* side,
+                                    int32_t* delta) {
+  const int lane = threadIdx.x & 31;
+  small_gains(off, nbr, n, side, delta);
+  __syncthreads();
+  long long total = 0;
+  if (threadIdx.x < 32) {
+    volatile int32_t* vd = delta;
+    volatile uint8_t* vs = side;
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (int32_t c = 0; c < n; c += 32) {
+        unsigned done = 0;
+        for (;;) {
+          const int32_t v0 = c + lane;
+          const bool maybe = v0 < n && vd[v0] + hmax[v0] + 2 > 0;
+          const unsigned m = __ballot_sync(0xffffffffu, maybe) & ~done;
+          if (!m) break;
+          const int j = warp_first(m);
+          const int32_t v = c + j;
+          done = j == 31 ? ~0u : (2u << j) - 1u;
+          // v's row in order, continuing with the state after each joint flip
+          const int64_t e1 = off[v + 1];
+          for (int64_t e = off[v]; e < e1;) {
+            const int64_t my = e + lane;
+            bool hit = false;
+            int32_t u = 0, joint = 0;
+            if (my < e1) {
+              u = nbr[my];
+              if (u > v && vs[u] != vs[v]) {
+                joint = vd[v] + vd[u] + 2;
+                hit = joint > 0;
+              }
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            if (!hm) {
+              e += 32;
+              continue;
+            }
+            const int h = warp_first(hm);
+            const int32_t uu = __shfl_sync(0xffffffffu, u, h);
+            total += __shfl_sync(0xffffffffu, joint, h);
+            small_flip(off, nbr, side, delta, v, lane);
+            small_flip(off, nbr, side, delta, uu, lane);
+            improved = true;
+            e += h + 1;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return total;
+}
+
+// OP: MQO_LS_ONE_FLIP / TWO_FLIP / ONE_TWO_FLIP; out[s] = the gain
+template <int OP, bool CSR>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_flip_small(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
+                 const int32_t* __restrict__ hmax, int32_t n, int64_t W, uint64_t* packed,
+                 int64_t* out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int s = blockIdx.x;
+  int32_t* delta = reinterpret_cast<int32_t*>(sm);
+  uint8_t* side = sm + (4 * int64_t(n) + 15) / 16 * 16;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  if constexpr (CSR) {
+    unsigned char* p = side + (int64_t(n) + 15) / 16 * 16;
+    int64_t* o = reinterpret_cast<int64_t*>(p);
+    int32_t* nb = reinterpret_cast<int32_t*>(p + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
+    for (int64_t i = threadIdx.x; i < off_g[n]; i += blockDim.x) nb[i] = nbr_g[i];
+    off = o;
+    nbr = nb;
+  }
+  small_unpack(packed + s * W, W, n, side);
+  __syncthreads();
+  long long total = 0;
+  if constexpr (OP == MQO_LS_ONE_FLIP) total = small_one_flip(off, nbr, n, side, delta);
+  if constexpr (OP == MQO_LS_TWO_FLIP) total = small_two_flip(off, nbr, hmax, n, side, delta);
+  if constexpr (OP == MQO_LS_ONE_TWO_FLIP) {  // localsearch.cpp:183-190
+    for (;;) {
+      const long long r = small_one_flip(off, nbr, n, side, delta) +
+                          small_two_flip(off, nbr, hmax, n, side, delta);
+      total += r;
+      if (__syncthreads_or(r != 0) == 0) break;
+    }
+  }
+  small_pack(side, W, n, packed + s * W);
+  if (threadIdx.x == 0) out[s] = total;
+}
+
+// one_two_swap (localsearch.cpp:88-137) in one launch: tightness by every
+// thread, the input check (not independent / not maximal: bad[s] bits 0 / 1,
+// the body is then left as it is), the swap scan on warp 0, pack, |I|.
+template <bool CSR>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_swap_small(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
+                 int32_t max_degree, int64_t W, uint64_t* packed, int64_t* out, int32_t* bad) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+  const int s = blockIdx.x;
+  unsigned char* p = sm;
+  int32_t* tight = reinterpret_cast<int32_t*>(p);
+  p += al(4 * int64_t(n));
+  int32_t* dlist = reinterpret_cast<int32_t*>(p);
+  p += al(4 * int64_t(n));
+  int32_t* freed = reinterpret_cast<int32_t*>(p);
+  p += al(4 * (int64_t(max_degree) + 1));
+  uint8_t* sel = p;
+  p += al(n);
+  uint8_t* dflag = p;
+  p += al(int64_t(n) + 4);
+  int32_t* dcount = reinterpret_cast<int32_t*>(p);
+  p += 16;
+  const int64_t* off = off_g;
+  const int32_t* nbr = nbr_g;
+  if constexpr (CSR) {
+    int64_t* o = reinterpret_cast<int64_t*>(p);
+    int32_t* nb = reinterpret_cast<int32_t*>(p + al(8 * (int64_t(n) + 1)));
+    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
+    for (int64_t i = threadIdx.x; i < off_g[n]; i += blockDim.x) nb[i] = nbr_g[i];
+    off = o;
+    nbr = nb;
+  }
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    *dcount = 0;
+  }
+  small_unpack(packed + s * W, W, n, sel);
+  for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) dflag[i] = 0;
+  __syncthreads();
+  // build_tightness (localsearch.cpp:9-15) + require_maximal_is (76-84)
+  int flag = 0;
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+    int32_t t = 0;
+    for (int64_t e = off[v]; e < off[v + 1]; ++e) t += sel[nbr[e]];
+    tight[v] = t;
+    if (sel[v] && t) flag |= 1;
+    if (!sel[v] && !t) flag |= 2;
+  }
+  if (flag) atomicOr(&s_bad, flag);
+  __syncthreads();
+  const int b = s_bad;
+  if (!b && threadIdx.x < 32)
+    warp_swap_loop(off, nbr, sel, tight, dflag, dlist, dcount, freed, n, threadIdx.x & 31);
+  __syncthreads();
+  if (!b) small_pack(sel, W, n, packed + s * W);
+  __shared__ int s_size;
+  if (threadIdx.x == 0) s_size = 0;
+  __syncthreads();
+  int cnt = 0;
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) cnt += sel[v];
+  if (cnt) atomicAdd(&s_size, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[s] = s_size;
+    if (bad) bad[s] = b;
+  }
+}
+
+inline int64_t small_state_bytes(int op, int32_t n, int32_t max_degree) {
+  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
+  if (op == MQO_LS_ONE_TWO_SWAP)
+    return al(4 * int64_t(n)) * 2 + al(4 * (int64_t(max_degree) + 1)) + al(n) + al(int64_t(n) + 4) + 16;
+  return al(4 * int64_t(n)) + al(n);
+}
+inline int64_t small_csr_bytes(int32_t n, int64_t nnz) {
+  return (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
+}
+
 // d_bad (one_two_swap only, may be null, zeroed by the caller): when given,
 // the input check of k_tight is left in d_bad[count] (bit 0 not independent, bit 1 not maximal)
 // for the caller to raise after its copy-out, instead of a host round trip
 // here; flagged bodies are left untouched.
+// hmax (k_hmax) of the graph, built once, complete before any stream uses it
+void ensure_hmax(mqo_graph* g, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g->lazy_mu);
+  if (g->d_hmax) return;
+  int32_t* h = nullptr;
+  {  // pool allocation on the graph's memory stream (freed there with the graph)
+    const cudaStream_t ms = mem_stream(g->device);
+    void* p = nullptr;
+    MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max(g->n, 1), ms));
+    MQO_CUDA(cudaStreamSynchronize(ms));
+    h = static_cast<int32_t*>(p);
+  }
+  k_hmax<<<ls_grid(g->n), 256, 0, st>>>(g->d_off, g->d_nbr, g->n, h);
+  MQO_CUDA(cudaGetLastError());
+  MQO_CUDA(cudaStreamSynchronize(st));
+  g->d_hmax = h;
+}
+
+// MQO_LS_SMALL=0 disables the single-launch small-body kernels (A/B runs)
+const bool g_ls_small = [] {
+  const char* e = std::getenv("MQO_LS_SMALL");
+  return !(e && *e == '0');
+}();
+
+// The single-launch kernels apply (n <= kSmallMaxN, state in SMEM); returns
+// whether they were launched.  d_bad (one_two_swap) receives the input
+// check of every body.
+bool local_search_small(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
+                        int64_t* d_out, cudaStream_t st, int32_t* d_bad) {
+  mqo_graph* g = b->g;
+  const int32_t n = g->n;
+  if (!g_ls_small || n > kSmallMaxN || n == 0) return false;
+  const int64_t state = small_state_bytes(op, n, g->max_degree);
+  if (state > kSmallSmemMax) return false;
+  const bool csr = state + small_csr_bytes(n, 2 * g->m) <= kSmallSmemMax;
+  const size_t smem = static_cast<size_t>(csr ? state + small_csr_bytes(n, 2 * g->m) : state);
+  const int64_t W = body_words(n);
+  if (op != MQO_LS_ONE_FLIP && op != MQO_LS_ONE_TWO_SWAP) ensure_hmax(g, st);
+  auto launch = [&](auto kern) {
+    static std::mutex mu;  // the SMEM opt-in, once per kernel and device
+    static bool done[64] = {false};
+    int dev = 0;
+    MQO_CUDA(cudaGetDevice(&dev));
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (dev >= 64 || !done[dev]) {
+        MQO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kSmallSmemMax)));
+        if (dev < 64) done[dev] = true;
+      }
+    }
+    return kern;
+  };
+  if (op == MQO_LS_ONE_TWO_SWAP) {
+    auto k = csr ? launch(k_swap_small<true>) : launch(k_swap_small<false>);
+    k<<<count, kSmallThreads, smem, st>>>(g->d_off, g->d_nbr, n, g->max_degree, W, d_packed, d_out,
+                                          d_bad);
+  } else {
+    void (*k)(const int64_t*, const int32_t*, const int32_t*, int32_t, int64_t, uint64_t*,
+              int64_t*) = nullptr;
+    if (op == MQO_LS_ONE_FLIP) k = csr ? launch(k_flip_small<0, true>) : launch(k_flip_small<0, false>);
+    if (op == MQO_LS_TWO_FLIP) k = csr ? launch(k_flip_small<1, true>) : launch(k_flip_small<1, false>);
+    if (op == MQO_LS_ONE_TWO_FLIP)
+      k = csr ? launch(k_flip_small<2, true>) : launch(k_flip_small<2, false>);
+    k<<<count, kSmallThreads, smem, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, W, d_packed, d_out);
+  }
+  MQO_CUDA(cudaGetLastError());
+  MQO_TRACE("local search op %d on %d bodies: single-launch kernel queued", op, count);
+  return true;
+}
+
 void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
                          int64_t* d_out, cudaStream_t st, int32_t* d_bad) {
   mqo_graph* g = b->g;
@@ -1961,6 +2309,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   const int64_t W = body_words(n);
   if (count <= 0) return;
   MQO_TRACE("local search op %d on %d bodies", op, count);
+  if (local_search_small(b, op, count, d_packed, d_out, st, d_bad)) return;
   LsWork w;
   const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
   if (op == 0 && one_flip_cta_fits(n, count)) {
@@ -1995,23 +2344,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (op <= 2) {
     k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
     MQO_CUDA(cudaGetLastError());
-    {
-      std::lock_guard<std::mutex> lock(g->lazy_mu);
-      if (!g->d_hmax) {  // once per graph, complete before any stream uses it
-        int32_t* h = nullptr;
-        {  // pool allocation on the graph's memory stream (freed there with the graph)
-          const cudaStream_t ms = mem_stream(g->device);
-          void* p = nullptr;
-          MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max(n, 1), ms));
-          MQO_CUDA(cudaStreamSynchronize(ms));
-          h = static_cast<int32_t*>(p);
-        }
-        k_hmax<<<ls_grid(n), 256, 0, st>>>(g->d_off, g->d_nbr, n, h);
-        MQO_CUDA(cudaGetLastError());
-        MQO_CUDA(cudaStreamSynchronize(st));
-        g->d_hmax = h;
-      }
-    }
+    ensure_hmax(g, st);
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
   } else if (d_bad && g_swap_cta) {
     // the input check stays on the device: k_tight flags bad bodies in
@@ -2104,36 +2437,43 @@ extern "C" int mqo_local_search(mqo_batch* b, int32_t op, int32_t count, uint64_
     const int64_t W = body_words(b->g->n);
     const int64_t words = W * count;
     // one device buffer [bodies | results | input flags] so the copy-out is a
-    // single D2H
+    // single D2H; device and pinned staging persist with the batch, so a
+    // small call is memcpy, H2D, the launch(es), D2H and one sync
     const int64_t total = words + count + (count + 1) / 2;
-    uint64_t* d_packed = nullptr;
+    const size_t bytes = sizeof(uint64_t) * total;
     cudaStream_t st = b->stream;
-    MQO_CUDA(cudaMallocAsync(&d_packed, sizeof(uint64_t) * total, st));
+    if (b->ls_bytes < bytes) {
+      dfree(b, b->d_ls);
+      pinned_put(b->h_ls, b->ls_bytes);
+      dalloc(b, &b->d_ls, bytes);
+      b->h_ls = static_cast<uint64_t*>(pinned_get(bytes));
+      b->ls_bytes = bytes;
+    }
+    uint64_t* d_packed = b->d_ls;
+    uint64_t* h = b->h_ls;
     int64_t* d_out = reinterpret_cast<int64_t*>(d_packed + words);
     int32_t* d_bad = reinterpret_cast<int32_t*>(d_packed + words + count);
+    std::memcpy(h, packed, sizeof(uint64_t) * words);
     MQO_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t) * count, st));
-    MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * words, cudaMemcpyHostToDevice, st));
+    MQO_CUDA(cudaMemcpyAsync(d_packed, h, sizeof(uint64_t) * words, cudaMemcpyHostToDevice, st));
     MQO_TRACE("mqo_local_search: bodies uploaded");
     try {
       local_search_device(b, op, count, d_packed, d_out, st, op == 3 ? d_bad : nullptr);
     } catch (...) {
-      cudaFreeAsync(d_packed, st);
       cudaStreamSynchronize(st);
       throw;
     }
-    std::vector<uint64_t> h(total);
-    MQO_CUDA(cudaMemcpyAsync(h.data(), d_packed, sizeof(uint64_t) * total, cudaMemcpyDeviceToHost, st));
-    cudaFreeAsync(d_packed, st);
+    MQO_CUDA(cudaMemcpyAsync(h, d_packed, bytes, cudaMemcpyDeviceToHost, st));
     MQO_CUDA(cudaStreamSynchronize(st));
     // one_two_swap's input check (localsearch.cpp:88-96), raised before the
     // caller's buffer is touched
-    const int32_t* bad = reinterpret_cast<const int32_t*>(h.data() + words + count);
+    const int32_t* bad = reinterpret_cast<const int32_t*>(h + words + count);
     for (int32_t i = 0; i < count; ++i) {
       if (bad[i] & 1) throw std::invalid_argument("one_two_swap: input not an independent set");
       if (bad[i] & 2) throw std::invalid_argument("one_two_swap: input not maximal");
     }
-    std::memcpy(packed, h.data(), sizeof(uint64_t) * words);
-    std::memcpy(out, h.data() + words, sizeof(int64_t) * count);
+    std::memcpy(packed, h, sizeof(uint64_t) * words);
+    std::memcpy(out, h + words, sizeof(int64_t) * count);
     MQO_TRACE("mqo_local_search: done");
   });
 }
