@@ -64,17 +64,44 @@ __device__ __forceinline__ int warp_first(unsigned mask) { return __ffs(mask) - 
 
 // ---------------------------------------------------------------- MaxCut
 // build_gain_table (localsearch.cpp:17-26) for `count` solutions.
+// Rows longer than kGainWarpDeg are summed by a warp each (k_gain_heavy):
+// one thread walking a 3350-neighbour hub row set the table's critical path.
+constexpr int64_t kGainWarpDeg = 64;
+
 __global__ void k_gain(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
                        int32_t count, const uint8_t* __restrict__ side, int32_t* __restrict__ delta) {
   const int64_t total = static_cast<int64_t>(count) * n;
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = q / n, v = q % n;
+    if (off[v + 1] - off[v] > kGainWarpDeg) continue;  // k_gain_heavy
     const uint8_t* sd = side + s * n;
     const uint8_t sv = sd[v];
     int32_t same = 0;
     for (int64_t e = off[v]; e < off[v + 1]; ++e) same += sd[nbr[e]] == sv ? 1 : -1;
     delta[q] = same;
+  }
+}
+
+// the long rows (a prefix of the degree-descending order), a warp per
+// (body, row); integer sums, so the lane split does not change the value
+__global__ void k_gain_heavy(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                             const int32_t* __restrict__ order, int32_t heavy, int32_t n,
+                             int32_t count, const uint8_t* __restrict__ side,
+                             int32_t* __restrict__ delta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t total = static_cast<int64_t>(count) * heavy;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < total;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t s = w / heavy;
+    const int32_t v = order[w - s * heavy];
+    const uint8_t* sd = side + s * n;
+    const uint8_t sv = sd[v];
+    int32_t same = 0;
+    for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) same += sd[nbr[e]] == sv ? 1 : -1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) same += __shfl_xor_sync(0xffffffffu, same, o);
+    if (lane == 0) delta[s * n + v] = same;
   }
 }
 
@@ -456,10 +483,29 @@ __global__ void k_two_cand_heavy(const int64_t* __restrict__ off, const int32_t*
   }
 }
 
-// hmax (above), once per graph
+// hmax (above), once per graph; rows longer than 64 by k_hmax_heavy
+__global__ void k_hmax_heavy(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                             const int32_t* __restrict__ order, int32_t heavy,
+                             int32_t* __restrict__ hmax) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < heavy;
+       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int32_t v = order[w];
+    int32_t h = 0;
+    for (int64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+      const int32_t u = nbr[e];
+      if (u > v) h = max(h, static_cast<int32_t>(off[u + 1] - off[u]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h = max(h, __shfl_xor_sync(0xffffffffu, h, o));
+    if (lane == 0) hmax[v] = h;
+  }
+}
+
 __global__ void k_hmax(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr, int32_t n,
                        int32_t* __restrict__ hmax) {
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (off[v + 1] - off[v] > 64) continue;  // k_hmax_heavy
     int32_t h = 0;
     for (int64_t e = off[v + 1] - 1, e0 = off[v]; e >= e0; --e) {
       const int32_t u = nbr[e];
@@ -1715,6 +1761,19 @@ int ls_grid(int64_t work) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 32)));
 }
 
+// build_gain_table for `count` bodies: light rows a thread each, rows of
+// degree > kGainWarpDeg a warp each
+void launch_gain(const mqo_graph* g, int32_t count, const uint8_t* side, int32_t* delta,
+                 cudaStream_t st) {
+  const int64_t cells = std::max<int64_t>(1, int64_t(count) * g->n);
+  k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->n, count, side, delta);
+  const int32_t heavy = g->h_deg_ge.size() > size_t(kGainWarpDeg) + 1 ? g->h_deg_ge[kGainWarpDeg + 1] : 0;
+  if (heavy > 0)
+    k_gain_heavy<<<ls_grid(int64_t(count) * heavy * 32), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_order,
+                                                                       heavy, g->n, count, side, delta);
+  MQO_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
 // -------------------------------------------------------------- host side
@@ -1876,7 +1935,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       k_flip_commit<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_cand,
                                                    d_live, reinterpret_cast<unsigned long long*>(d_g1));
       k_flip_apply<<<ls_grid(cells), 256, 0, st>>>(n, count, side, d_cand, d_live);
-      k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta);
+      launch_gain(g, count, side, delta, st);
       MQO_CUDA(cudaGetLastError());
       MQO_CUDA(cudaMemcpyAsync(pg.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
       MQO_CUDA(cudaStreamSynchronize(st));
@@ -2244,6 +2303,9 @@ void ensure_hmax(mqo_graph* g, cudaStream_t st) {
     h = static_cast<int32_t*>(p);
   }
   k_hmax<<<ls_grid(g->n), 256, 0, st>>>(g->d_off, g->d_nbr, g->n, h);
+  const int32_t heavy = g->h_deg_ge.size() > size_t(kGainWarpDeg) + 1 ? g->h_deg_ge[kGainWarpDeg + 1] : 0;
+  if (heavy > 0)
+    k_hmax_heavy<<<ls_grid(int64_t(heavy) * 32), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_order, heavy, h);
   MQO_CUDA(cudaGetLastError());
   MQO_CUDA(cudaStreamSynchronize(st));
   g->d_hmax = h;
@@ -2342,7 +2404,7 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   MQO_CUDA(cudaGetLastError());
   const int blocks = (count + kLsWarps - 1) / kLsWarps;
   if (op <= 2) {
-    k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, w.bytes, w.ints);
+    launch_gain(g, count, w.bytes, w.ints, st);
     MQO_CUDA(cudaGetLastError());
     ensure_hmax(g, st);
     maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
@@ -2502,7 +2564,7 @@ extern "C" int mqo_build_tables(mqo_batch* b, int32_t kind, int32_t count, const
     MQO_CUDA(cudaMemcpyAsync(d_packed, packed, sizeof(uint64_t) * W * count, cudaMemcpyHostToDevice, st));
     k_unpack<<<ls_grid(cells), 256, 0, st>>>(d_packed, W, n, count, d_bytes);
     if (kind == 0)
-      k_gain<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, d_bytes, d_out);
+      launch_gain(g, count, d_bytes, d_out, st);
     else
       k_tight<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, d_bytes, d_out, d_flags);
     MQO_CUDA(cudaGetLastError());

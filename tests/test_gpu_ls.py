@@ -149,7 +149,8 @@ def test_swap_batch_input_check_leaves_caller_buffer(P):
     assert out.tolist() == [4, 4]
 
 
-@pytest.mark.parametrize("n,d,bodies", [(1024, 16, 1), (8000, 16, 1), (16384, 16, 16), (4096, 8, 20)])
+@pytest.mark.parametrize("n,d,bodies", [(1024, 16, 1), (8000, 16, 1), (16384, 16, 16), (4096, 8, 20),
+                                         (20000, 8, 16)])
 def test_one_flip_cta_variants_vs_oracle(O, P, n, d, bodies):
     # k_one_flip_cta with the CSR in shared memory (n = 1024, 4096) and read
     # from global memory (ER(8000, d=16): 512 KB of rows; 16 bodies at 16384),
@@ -164,3 +165,41 @@ def test_one_flip_cta_variants_vs_oracle(O, P, n, d, bodies):
     for k in range(bodies):
         ref_side, ref_gain = O.one_flip_pass(og, sides[k])
         assert gains[k] == ref_gain and (got[k] == ref_side).all(), k
+
+
+@pytest.mark.parametrize("n,d", [(1024, 16), (4096, 8), (16384, 8)])
+@pytest.mark.parametrize("op", ["two_flip", "one_two_flip", "swap"])
+@pytest.mark.parametrize("bodies", [1, 5])
+def test_single_launch_small_bodies_vs_oracle(O, P, n, d, op, bodies):
+    """The single-launch kernels (k_flip_small / k_swap_small, n <= 16384;
+    CSR staged in SMEM or read from global memory) against the oracle."""
+    from paper_2605_06921_b200 import _lib
+    og = O.generate_er(n, d / n, 5)
+    pg = P.generate(P.ErSpec(n, d / n), 5)
+    b = P.ChainBatch(pg, 1)
+    rng = np.random.default_rng(n * 7 + bodies)
+    if op == "swap":
+        starts = []
+        for k in range(bodies):  # greedy completions of random independent seeds
+            ind = np.zeros(n, np.uint8)
+            ind[rng.choice(n, 3, replace=False)] = 1
+            off, nbr = pg.csr()
+            for v in np.flatnonzero(ind):
+                if ind[nbr[off[v]:off[v + 1]]].any():
+                    ind[v] = 0
+            starts.append(O.greedy_maximalize(og, ind)[0])
+        start = np.array(starts, np.uint8)
+        packed, out = P.local_search(b, _lib.LS_ONE_TWO_SWAP, P.pack_bodies(start))
+        got = P.unpack_bodies(packed, n)
+        for k in range(bodies):
+            ref, size = O.one_two_swap(og, start[k])
+            assert out[k] == size and (got[k] == ref).all(), k
+        return
+    opc = _lib.LS_TWO_FLIP if op == "two_flip" else _lib.LS_ONE_TWO_FLIP
+    sides = rng.integers(0, 2, (bodies, n)).astype(np.uint8)
+    packed, gains = P.local_search(b, opc, P.pack_bodies(sides))
+    got = P.unpack_bodies(packed, n)
+    for k in range(bodies):
+        fn = O.two_flip_pass if op == "two_flip" else O.one_two_flip
+        ref, gain = fn(og, sides[k])
+        assert gains[k] == gain and (got[k] == ref).all(), k
