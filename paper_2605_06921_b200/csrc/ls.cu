@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 
@@ -247,46 +249,19 @@ inline bool one_flip_cta_fits(int32_t n, int32_t count) {
   return g_swap_smem && flip_cta_smem(n) <= kFlipCtaSmemMax && (n <= 8192 || count >= 16);
 }
 
-// `csr`: the CSR is staged in shared memory too (it fits next to the body
-// state); every row walk is then ~30-cycle SMEM loads instead of L2 trips.
-// CSR as a template parameter: the row walks then compile to LDS instead of
-// generic loads.
-template <bool CSR>
-__global__ void __launch_bounds__(kFlipCtaThreads, 1)
-    k_one_flip_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
-                   uint8_t* side_all, int32_t* delta_all, const int32_t* __restrict__ live,
-                   int64_t* __restrict__ gains) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  int32_t* d0 = reinterpret_cast<int32_t*>(sm);
-  int32_t* lo_cnt = d0 + n;
-  uint8_t* sd = sm + 8 * int64_t(n);
-  volatile uint8_t* st = sd + n;
-  int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
-  int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
-  const int64_t* off = CSR ? o : off_g;
-  const int32_t* nbr = CSR ? nb : nbr_g;
-  // live == nullptr: every body is live
-  if (CSR && (!live || live[blockIdx.x])) {
-    const int64_t nnz = off_g[n];
-    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
-#pragma unroll 4
-    for (int64_t i = threadIdx.x; i < nnz; i += blockDim.x) nb[i] = nbr_g[i];
-  }
+// one_flip_pass (localsearch.cpp:139-157) as CTA decision rounds on the
+// SMEM state of one body: sd[n] sides (in/out), lo_cnt[n] (lower-neighbour
+// counts, built here), d0[n] (left = the gain table of the final state),
+// st[n] decision bytes.  Returns the gain (the same on every thread).
+__device__ long long cta_one_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
+                                       uint8_t* sd, int32_t* d0, int32_t* lo_cnt,
+                                       volatile uint8_t* st) {
   __shared__ unsigned long long s_gain;
   __shared__ int s_flips;
-  const int s = blockIdx.x;
-  uint8_t* side = side_all + int64_t(s) * n;
-  int32_t* delta = delta_all + int64_t(s) * n;
-  if (live && !live[s]) {
-    if (threadIdx.x == 0) gains[s] = 0;
-    return;
-  }
-  __syncthreads();  // CSR staged
   // lower neighbours are a row prefix (rows ascend): their count, so the
   // round and commit walks below are counted loops the compiler can unroll
   // (independent loads in flight) instead of break-terminated chains
   for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
-    sd[v] = side[v];
     int64_t a = off[v], b = off[v + 1];
     const int64_t e0 = a;
     while (a < b) {  // first entry >= v
@@ -369,6 +344,45 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     __syncthreads();
     if (!any) break;  // a pass without a flip ends one_flip_pass
   }
+  return total;
+}
+
+// `csr`: the CSR is staged in shared memory too (it fits next to the body
+// state); every row walk is then ~30-cycle SMEM loads instead of L2 trips.
+// CSR as a template parameter: the row walks then compile to LDS instead of
+// generic loads.
+template <bool CSR>
+__global__ void __launch_bounds__(kFlipCtaThreads, 1)
+    k_one_flip_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
+                   uint8_t* side_all, int32_t* delta_all, const int32_t* __restrict__ live,
+                   int64_t* __restrict__ gains) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  int32_t* d0 = reinterpret_cast<int32_t*>(sm);
+  int32_t* lo_cnt = d0 + n;
+  uint8_t* sd = sm + 8 * int64_t(n);
+  volatile uint8_t* st = sd + n;
+  int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
+  int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+  const int64_t* off = CSR ? o : off_g;
+  const int32_t* nbr = CSR ? nb : nbr_g;
+  // live == nullptr: every body is live
+  if (CSR && (!live || live[blockIdx.x])) {
+    const int64_t nnz = off_g[n];
+    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < nnz; i += blockDim.x) nb[i] = nbr_g[i];
+  }
+  const int s = blockIdx.x;
+  uint8_t* side = side_all + int64_t(s) * n;
+  int32_t* delta = delta_all + int64_t(s) * n;
+  if (live && !live[s]) {
+    if (threadIdx.x == 0) gains[s] = 0;
+    return;
+  }
+  __syncthreads();  // CSR staged
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) sd[v] = side[v];
+  __syncthreads();
+  const long long total = cta_one_flip_pass(off, nbr, n, sd, d0, lo_cnt, st);
   // write back the sides and the gain table of the final state (after the
   // last pass flipped nothing, d0 is that table)
   for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
@@ -1438,7 +1452,7 @@ __device__ __forceinline__ void cta_copy(void* dst, const void* src, int64_t byt
 // instead of ~300+ for L2.  Generic pointers serve both placements.
 // one_two_swap's scan (localsearch.cpp:88-137) on one warp: the lowest
 // swappable vertex among the dirty ones, else the next from the frontier;
-// returns the number of swaps.  Shared by k_mis_swap and k_swap_small.
+// returns the number of swaps.
 __device__ int64_t warp_swap_loop(const int64_t* off, const int32_t* nbr, uint8_t* sel,
                                   int32_t* tight, uint8_t* dflag, int32_t* dlist,
                                   int32_t* dcount, int32_t* freed, int32_t n, int lane) {
@@ -2020,18 +2034,17 @@ void launch_swap_cta(const mqo_graph* g, int32_t count, LsWork& w, int64_t* d_ou
 }
 
 // ---- single-launch local search for small bodies -------------------------
-// One call on one small body used to cost ~60 us before any work (workspace
-// allocations, unpack / gain / candidate / scan / pack launches, host round
-// trips between sweeps) -- more than the reference's whole scalar pass at
-// n = 1024.  These kernels do the complete operation in ONE launch, one CTA
-// per body, from the packed bodies to the packed bodies and the result:
-// unpack into SMEM, gain / tightness tables built by every thread, the
-// reference's sequential scans on one warp (a ballot finds the next move
-// among 32 vertices, the warp applies it; the other warps idle at the next
-// barrier), pack.  The CSR is staged in SMEM when it fits next to the state.
-constexpr int kSmallThreads = 512;
+// A MaxCut call on small bodies used to be several launches (unpack, gain
+// table, candidate tests, one scan launch per 2-flip sweep, pack) with a
+// host round trip per sweep.  k_flip_small does the whole operation in ONE
+// launch, one CTA per body, packed bodies in and out: unpack into SMEM,
+// 1-flip passes as CTA decision rounds, 2-flip sweeps (rare moves) as the
+// reference's sequential scan on one warp (a ballot finds the next row with
+// a possible move among 32 vertices, the warp walks it), pack.  The CSR is
+// staged in SMEM when it fits next to the state.
 constexpr int64_t kSmallSmemMax = 226 * 1024;
 constexpr int32_t kSmallMaxN = 16384;
+constexpr int32_t kSmallTwoFlipMaxN = 4096;
 
 __device__ __forceinline__ void small_unpack(const uint64_t* __restrict__ packed, int64_t W,
                                              int32_t n, uint8_t* dst) {
@@ -2078,63 +2091,38 @@ __device__ __forceinline__ void small_flip(const int64_t* off, const int32_t* nb
   __syncwarp();
 }
 
-// one_flip_pass (localsearch.cpp:139-157) on warp 0; every thread calls it
-__device__ long long small_one_flip(const int64_t* off, const int32_t* nbr, int32_t n,
-                                    uint8_t* side, int32_t* delta) {
-  const int lane = threadIdx.x & 31;
-  small_gains(off, nbr, n, side, delta);
-  __syncthreads();
-  long long total = 0;
-  if (threadIdx.x < 32) {
-    volatile int32_t* vd = delta;
-    for (bool improved = true; improved;) {
-      improved = false;
-      for (int32_t c = 0; c < n; c += 32) {
-        unsigned done = 0;  // lanes already passed in this chunk
-        for (;;) {
-          const int32_t v = c + lane;
-          const bool ok = v < n && vd[v] > 0;
-          const unsigned m = __ballot_sync(0xffffffffu, ok) & ~done;
-          if (!m) break;
-          const int j = warp_first(m);
-          const int32_t u = c + j;
-          total += vd[u];
-          small_flip(off, nbr, side, delta, u, lane);
-          improved = true;
-          done = j == 31 ? ~0u : (2u << j) - 1u;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  return total;
-}
-
-// two_flip_pass (localsearch.cpp:159-181) on warp 0; hmax[v] bounds delta_u
-// of v's higher neighbours (rows that cannot hit are skipped)
+// two_flip_pass (localsearch.cpp:159-181) of one body: every thread tests
+// its vertices exactly (two_cand: a possible joint flip with a higher
+// neighbour), then warp 0 visits the marked vertices in order, walks each
+// row against the current state (continuing after each joint flip) and
+// re-marks the later vertices whose test a flip can change
+// (warp_mark_after_flip); sweeps repeat while one improves.  cand[n] bytes.
 __device__ long long small_two_flip(const int64_t* off, const int32_t* nbr,
                                     const int32_t* __restrict__ hmax, int32_t n, uint8_t* side,
-                                    int32_t* delta) {
+                                    int32_t* delta, uint8_t* cand) {
   const int lane = threadIdx.x & 31;
+  __shared__ int s_improved;
   small_gains(off, nbr, n, side, delta);
-  __syncthreads();
   long long total = 0;
-  if (threadIdx.x < 32) {
-    volatile int32_t* vd = delta;
-    volatile uint8_t* vs = side;
-    for (bool improved = true; improved;) {
-      improved = false;
+  for (;;) {
+    __syncthreads();
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+      cand[v] = two_cand(off, nbr, hmax, side, delta, v) ? 1 : 0;
+    if (threadIdx.x == 0) s_improved = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      volatile int32_t* vd = delta;
+      volatile uint8_t* vs = side;
+      volatile uint8_t* vc = cand;
+      bool improved = false;
       for (int32_t c = 0; c < n; c += 32) {
         unsigned done = 0;
         for (;;) {
-          const int32_t v0 = c + lane;
-          const bool maybe = v0 < n && vd[v0] + hmax[v0] + 2 > 0;
-          const unsigned m = __ballot_sync(0xffffffffu, maybe) & ~done;
+          const unsigned m = __ballot_sync(0xffffffffu, c + lane < n && vc[c + lane]) & ~done;
           if (!m) break;
           const int j = warp_first(m);
           const int32_t v = c + j;
           done = j == 31 ? ~0u : (2u << j) - 1u;
-          // v's row in order, continuing with the state after each joint flip
           const int64_t e1 = off[v + 1];
           for (int64_t e = off[v]; e < e1;) {
             const int64_t my = e + lane;
@@ -2157,131 +2145,70 @@ __device__ long long small_two_flip(const int64_t* off, const int32_t* nbr,
             total += __shfl_sync(0xffffffffu, joint, h);
             small_flip(off, nbr, side, delta, v, lane);
             small_flip(off, nbr, side, delta, uu, lane);
+            warp_mark_after_flip(off, nbr, cand, v, v, lane);
+            warp_mark_after_flip(off, nbr, cand, uu, v, lane);
             improved = true;
             e += h + 1;
           }
         }
       }
+      if (lane == 0 && improved) s_improved = 1;
     }
+    __syncthreads();
+    if (!s_improved) break;
   }
   __syncthreads();
   return total;
 }
 
-// OP: MQO_LS_ONE_FLIP / TWO_FLIP / ONE_TWO_FLIP; out[s] = the gain
+// OP: MQO_LS_ONE_FLIP / TWO_FLIP / ONE_TWO_FLIP; out[s] = the gain.  SMEM:
+// the k_one_flip_cta layout (d0 = the gain table, lo_cnt, sides, decision
+// bytes), then the CSR when it fits.  1-flip passes run as CTA decision
+// rounds (cta_one_flip_pass), 2-flip sweeps on warp 0 (2-flip moves are
+// rare next to 1-flip moves).
 template <int OP, bool CSR>
-__global__ void __launch_bounds__(kSmallThreads, 1)
+__global__ void __launch_bounds__(kFlipCtaThreads, 1)
     k_flip_small(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
                  const int32_t* __restrict__ hmax, int32_t n, int64_t W, uint64_t* packed,
                  int64_t* out) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int s = blockIdx.x;
-  int32_t* delta = reinterpret_cast<int32_t*>(sm);
-  uint8_t* side = sm + (4 * int64_t(n) + 15) / 16 * 16;
+  int32_t* d0 = reinterpret_cast<int32_t*>(sm);
+  int32_t* lo_cnt = d0 + n;
+  uint8_t* sd = sm + 8 * int64_t(n);
+  volatile uint8_t* st = sd + n;
   const int64_t* off = off_g;
   const int32_t* nbr = nbr_g;
   if constexpr (CSR) {
-    unsigned char* p = side + (int64_t(n) + 15) / 16 * 16;
-    int64_t* o = reinterpret_cast<int64_t*>(p);
-    int32_t* nb = reinterpret_cast<int32_t*>(p + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+    int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
+    int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+    const int64_t nnz = off_g[n];
     for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
-    for (int64_t i = threadIdx.x; i < off_g[n]; i += blockDim.x) nb[i] = nbr_g[i];
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < nnz; i += blockDim.x) nb[i] = nbr_g[i];
     off = o;
     nbr = nb;
   }
-  small_unpack(packed + s * W, W, n, side);
+  small_unpack(packed + s * W, W, n, sd);
   __syncthreads();
   long long total = 0;
-  if constexpr (OP == MQO_LS_ONE_FLIP) total = small_one_flip(off, nbr, n, side, delta);
-  if constexpr (OP == MQO_LS_TWO_FLIP) total = small_two_flip(off, nbr, hmax, n, side, delta);
+  if constexpr (OP == MQO_LS_ONE_FLIP) total = cta_one_flip_pass(off, nbr, n, sd, d0, lo_cnt, st);
+  uint8_t* cand = const_cast<uint8_t*>(st);  // the decision bytes double as 2-flip marks
+  if constexpr (OP == MQO_LS_TWO_FLIP) total = small_two_flip(off, nbr, hmax, n, sd, d0, cand);
   if constexpr (OP == MQO_LS_ONE_TWO_FLIP) {  // localsearch.cpp:183-190
     for (;;) {
-      const long long r = small_one_flip(off, nbr, n, side, delta) +
-                          small_two_flip(off, nbr, hmax, n, side, delta);
+      const long long r = cta_one_flip_pass(off, nbr, n, sd, d0, lo_cnt, st) +
+                          small_two_flip(off, nbr, hmax, n, sd, d0, cand);
       total += r;
       if (__syncthreads_or(r != 0) == 0) break;
     }
   }
-  small_pack(side, W, n, packed + s * W);
+  __syncthreads();
+  small_pack(sd, W, n, packed + s * W);
   if (threadIdx.x == 0) out[s] = total;
 }
 
-// one_two_swap (localsearch.cpp:88-137) in one launch: tightness by every
-// thread, the input check (not independent / not maximal: bad[s] bits 0 / 1,
-// the body is then left as it is), the swap scan on warp 0, pack, |I|.
-template <bool CSR>
-__global__ void __launch_bounds__(kSmallThreads, 1)
-    k_swap_small(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
-                 int32_t max_degree, int64_t W, uint64_t* packed, int64_t* out, int32_t* bad) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
-  const int s = blockIdx.x;
-  unsigned char* p = sm;
-  int32_t* tight = reinterpret_cast<int32_t*>(p);
-  p += al(4 * int64_t(n));
-  int32_t* dlist = reinterpret_cast<int32_t*>(p);
-  p += al(4 * int64_t(n));
-  int32_t* freed = reinterpret_cast<int32_t*>(p);
-  p += al(4 * (int64_t(max_degree) + 1));
-  uint8_t* sel = p;
-  p += al(n);
-  uint8_t* dflag = p;
-  p += al(int64_t(n) + 4);
-  int32_t* dcount = reinterpret_cast<int32_t*>(p);
-  p += 16;
-  const int64_t* off = off_g;
-  const int32_t* nbr = nbr_g;
-  if constexpr (CSR) {
-    int64_t* o = reinterpret_cast<int64_t*>(p);
-    int32_t* nb = reinterpret_cast<int32_t*>(p + al(8 * (int64_t(n) + 1)));
-    for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
-    for (int64_t i = threadIdx.x; i < off_g[n]; i += blockDim.x) nb[i] = nbr_g[i];
-    off = o;
-    nbr = nb;
-  }
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) {
-    s_bad = 0;
-    *dcount = 0;
-  }
-  small_unpack(packed + s * W, W, n, sel);
-  for (int64_t i = threadIdx.x; i < int64_t(n) + 4; i += blockDim.x) dflag[i] = 0;
-  __syncthreads();
-  // build_tightness (localsearch.cpp:9-15) + require_maximal_is (76-84)
-  int flag = 0;
-  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
-    int32_t t = 0;
-    for (int64_t e = off[v]; e < off[v + 1]; ++e) t += sel[nbr[e]];
-    tight[v] = t;
-    if (sel[v] && t) flag |= 1;
-    if (!sel[v] && !t) flag |= 2;
-  }
-  if (flag) atomicOr(&s_bad, flag);
-  __syncthreads();
-  const int b = s_bad;
-  if (!b && threadIdx.x < 32)
-    warp_swap_loop(off, nbr, sel, tight, dflag, dlist, dcount, freed, n, threadIdx.x & 31);
-  __syncthreads();
-  if (!b) small_pack(sel, W, n, packed + s * W);
-  __shared__ int s_size;
-  if (threadIdx.x == 0) s_size = 0;
-  __syncthreads();
-  int cnt = 0;
-  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) cnt += sel[v];
-  if (cnt) atomicAdd(&s_size, cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    out[s] = s_size;
-    if (bad) bad[s] = b;
-  }
-}
-
-inline int64_t small_state_bytes(int op, int32_t n, int32_t max_degree) {
-  auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
-  if (op == MQO_LS_ONE_TWO_SWAP)
-    return al(4 * int64_t(n)) * 2 + al(4 * (int64_t(max_degree) + 1)) + al(n) + al(int64_t(n) + 4) + 16;
-  return al(4 * int64_t(n)) + al(n);
-}
+inline int64_t small_state_bytes(int32_t n) { return flip_cta_smem(n); }
 inline int64_t small_csr_bytes(int32_t n, int64_t nnz) {
   return (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
 }
@@ -2317,48 +2244,44 @@ const bool g_ls_small = [] {
   return !(e && *e == '0');
 }();
 
-// The single-launch kernels apply (n <= kSmallMaxN, state in SMEM); returns
-// whether they were launched.  d_bad (one_two_swap) receives the input
-// check of every body.
+// The single-launch MaxCut kernels apply (n <= kSmallMaxN, state in SMEM);
+// returns whether they were launched.  (one_two_swap keeps its CTA kernel:
+// a swap is a sequential core on one warp either way, and the CTA searches
+// are the faster part.)
 bool local_search_small(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_packed,
-                        int64_t* d_out, cudaStream_t st, int32_t* d_bad) {
+                        int64_t* d_out, cudaStream_t st, int32_t* /*d_bad*/) {
   mqo_graph* g = b->g;
   const int32_t n = g->n;
-  if (!g_ls_small || n > kSmallMaxN || n == 0) return false;
-  const int64_t state = small_state_bytes(op, n, g->max_degree);
+  if (!g_ls_small || n > kSmallMaxN || n == 0 || op == MQO_LS_ONE_TWO_SWAP) return false;
+  // the 2-flip sweeps walk their moves on one warp: past a few thousand
+  // vertices the multi-commit sweeps (k_two_scan_multi) win
+  // (scripts/ls_small_probe.py: one_two_flip from random sides, n = 4096
+  // 3.46 vs 3.48 ms, n = 16384 22.1 vs 9.7 ms)
+  if (op != MQO_LS_ONE_FLIP && n > kSmallTwoFlipMaxN) return false;
+  const int64_t state = small_state_bytes(n);
   if (state > kSmallSmemMax) return false;
   const bool csr = state + small_csr_bytes(n, 2 * g->m) <= kSmallSmemMax;
   const size_t smem = static_cast<size_t>(csr ? state + small_csr_bytes(n, 2 * g->m) : state);
   const int64_t W = body_words(n);
-  if (op != MQO_LS_ONE_FLIP && op != MQO_LS_ONE_TWO_SWAP) ensure_hmax(g, st);
+  if (op != MQO_LS_ONE_FLIP) ensure_hmax(g, st);
   auto launch = [&](auto kern) {
-    static std::mutex mu;  // the SMEM opt-in, once per kernel and device
-    static bool done[64] = {false};
+    static std::mutex mu;  // the SMEM opt-in, once per (kernel, device)
+    static std::set<std::pair<const void*, int>> done;
     int dev = 0;
     MQO_CUDA(cudaGetDevice(&dev));
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      if (dev >= 64 || !done[dev]) {
-        MQO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(kSmallSmemMax)));
-        if (dev < 64) done[dev] = true;
-      }
-    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert({reinterpret_cast<const void*>(kern), dev}).second)
+      MQO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmallSmemMax)));
     return kern;
   };
-  if (op == MQO_LS_ONE_TWO_SWAP) {
-    auto k = csr ? launch(k_swap_small<true>) : launch(k_swap_small<false>);
-    k<<<count, kSmallThreads, smem, st>>>(g->d_off, g->d_nbr, n, g->max_degree, W, d_packed, d_out,
-                                          d_bad);
-  } else {
-    void (*k)(const int64_t*, const int32_t*, const int32_t*, int32_t, int64_t, uint64_t*,
-              int64_t*) = nullptr;
-    if (op == MQO_LS_ONE_FLIP) k = csr ? launch(k_flip_small<0, true>) : launch(k_flip_small<0, false>);
-    if (op == MQO_LS_TWO_FLIP) k = csr ? launch(k_flip_small<1, true>) : launch(k_flip_small<1, false>);
-    if (op == MQO_LS_ONE_TWO_FLIP)
-      k = csr ? launch(k_flip_small<2, true>) : launch(k_flip_small<2, false>);
-    k<<<count, kSmallThreads, smem, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, W, d_packed, d_out);
-  }
+  void (*k)(const int64_t*, const int32_t*, const int32_t*, int32_t, int64_t, uint64_t*,
+            int64_t*) = nullptr;
+  if (op == MQO_LS_ONE_FLIP) k = csr ? launch(k_flip_small<0, true>) : launch(k_flip_small<0, false>);
+  if (op == MQO_LS_TWO_FLIP) k = csr ? launch(k_flip_small<1, true>) : launch(k_flip_small<1, false>);
+  if (op == MQO_LS_ONE_TWO_FLIP)
+    k = csr ? launch(k_flip_small<2, true>) : launch(k_flip_small<2, false>);
+  k<<<count, kFlipCtaThreads, smem, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, W, d_packed, d_out);
   MQO_CUDA(cudaGetLastError());
   MQO_TRACE("local search op %d on %d bodies: single-launch kernel queued", op, count);
   return true;

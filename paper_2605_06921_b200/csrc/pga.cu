@@ -90,11 +90,12 @@ struct PassArgs {
 // minimum resident CTAs per SM (register cap), cache-policy hints.
 // MEM: 0 = two 128-bit ld.cg per lane, 1 = one 256-bit load with L2
 // eviction-priority policies, 2 = one 256-bit load without policies.
-template <int U_, int MINB_, int MEM_>
+template <int U_, int MINB_, int MEM_, bool PREFETCH_ = false>
 struct Tune {
   static constexpr int U = U_;
   static constexpr int MINB = MINB_;
   static constexpr int MEM = MEM_;
+  static constexpr bool PREFETCH = PREFETCH_;  // next batch's neighbour ids loaded early
   static constexpr bool HINT = MEM_ != 0;  // 256-bit path
   static constexpr bool POLICY = MEM_ == 1 || MEM_ == 3;
   static constexpr bool L2_64B = MEM_ == 3;  // neighbour gathers with the L2::64B fetch size
@@ -214,10 +215,20 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
   for (int c = 0; c < CPL; ++c) {
     s[c] = 0.0;
   }
+  // neighbour ids one batch ahead: the next batch's index loads are in
+  // flight while this batch's gathers are (one round trip per batch instead
+  // of two on rows longer than U)
+  int32_t nx[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) nx[j] = (e0 + j < e1) ? __ldg(a.nbr + e0 + j) : -1;
   for (int64_t e = e0; e < e1; e += U) {
     int32_t us[U];
 #pragma unroll
-    for (int j = 0; j < U; ++j) us[j] = (e + j < e1) ? __ldg(a.nbr + e + j) : -1;
+    for (int j = 0; j < U; ++j) us[j] = nx[j];
+    if constexpr (TU::PREFETCH) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) nx[j] = (e + U + j < e1) ? __ldg(a.nbr + e + U + j) : -1;
+    }
     double val[U][CPL];
 #pragma unroll
     for (int j = 0; j < U; ++j)
@@ -243,6 +254,10 @@ __device__ __forceinline__ void row_unit(const PassArgs& a, const double* __rest
           s[c] = ex_add(s[c], val[j][c]);               // graph.cpp:68
         if constexpr (CHECK) nbsel |= (val[j][c] > 0.5 ? 1u : 0u) << c;
       }
+    }
+    if constexpr (!TU::PREFETCH) {
+#pragma unroll
+      for (int j = 0; j < U; ++j) nx[j] = (e + U + j < e1) ? __ldg(a.nbr + e + U + j) : -1;
     }
   }
   if constexpr (CHECK) {
@@ -802,6 +817,8 @@ PassFn pass_fn(int kind, int cpl) {
       case 8: return pass_fn_tu<MODE, Tune<3, 4, 1>>(kind, cpl);
       case 9: return pass_fn_tu<MODE, Tune<4, 3, 3>>(kind, cpl);   // L2::64B gathers
       case 10: return pass_fn_tu<MODE, Tune<3, 4, 3>>(kind, cpl);
+      case 11: return pass_fn_tu<MODE, Tune<4, 3, 1, true>>(kind, cpl);  // index prefetch
+      case 12: return pass_fn_tu<MODE, Tune<3, 4, 1, true>>(kind, cpl);
       default: break;
     }
   }
