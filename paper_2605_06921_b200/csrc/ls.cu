@@ -256,8 +256,7 @@ inline bool one_flip_cta_fits(int32_t n, int32_t count) {
 __device__ long long cta_one_flip_pass(const int64_t* off, const int32_t* nbr, int32_t n,
                                        uint8_t* sd, int32_t* d0, int32_t* lo_cnt,
                                        volatile uint8_t* st) {
-  __shared__ unsigned long long s_gain;
-  __shared__ int s_flips;
+  __shared__ long long s_part[32];
   // lower neighbours are a row prefix (rows ascend): their count, so the
   // round and commit walks below are counted loops the compiler can unroll
   // (independent loads in flight) instead of break-terminated chains
@@ -283,10 +282,6 @@ __device__ long long cta_one_flip_pass(const int64_t* off, const int32_t* nbr, i
       for (int32_t k = 0; k < deg; ++k) same += sd[nbr[e0 + k]] == sv ? 1 : -1;
       d0[v] = same;
       st[v] = 0;
-    }
-    if (threadIdx.x == 0) {
-      s_gain = 0ull;
-      s_flips = 0;
     }
     __syncthreads();
     // decision rounds (k_flip_round)
@@ -334,13 +329,14 @@ __device__ long long cta_one_flip_pass(const int64_t* off, const int32_t* nbr, i
       }
       g += at;
     }
-    if (g) atomicAdd(&s_gain, static_cast<unsigned long long>(g));
-    if (flips) atomicAdd(&s_flips, flips);
-    __syncthreads();
+    // warp sums, then one partial per warp (a 64-bit shared atomicAdd is a
+    // CAS loop: 1024 contending threads serialised the pass)
+    for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = g;
+    const bool any = __syncthreads_or(flips) != 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += s_part[w];
     for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
       if (st[v] == 2) sd[v] ^= 1;
-    const bool any = s_flips != 0;
-    total += static_cast<long long>(s_gain);
     __syncthreads();
     if (!any) break;  // a pass without a flip ends one_flip_pass
   }
@@ -2091,6 +2087,141 @@ __device__ __forceinline__ void small_flip(const int64_t* off, const int32_t* nb
   __syncwarp();
 }
 
+// one_flip_pass (localsearch.cpp:139-157) for the single-launch kernel: the
+// CTA decision rounds of cta_one_flip_pass, restricted per pass to the
+// vertices that CAN flip.  P = the least set containing every v with
+// d0[v] + 2 * |{u in P : u < v, u ~ v, side[u] != side[v]}| > 0 (seeds: the
+// positive pass-start gains; each member raises its favourable upper
+// neighbours' counters, a counter crossing zero admits its vertex exactly
+// once).  By induction over the scan order every vertex the sequential pass
+// flips is in P (its gain when reached is at most that bound), so the rest
+// are decided "keep" before the rounds start and the rounds walk a compact
+// list.  Late passes flip a handful of vertices, so P is small; the
+// unrestricted rounds re-walked every undecided row (ncu r22: 30 rounds,
+// 252k cycles at n = 1024, d = 16).  SMEM (n <= 65535): d0, cnt [n] int32,
+// lo, list [n] uint16, side, st [n] bytes.  Leaves d0 = the gain table of
+// the final state.  Returns the gain on every thread.
+__host__ __device__ inline int64_t small_state_bytes(int32_t n) { return (14 * int64_t(n) + 15) / 16 * 16; }
+
+__device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr, int32_t n,
+                                          uint8_t* sd, int32_t* d0, int32_t* cnt, uint16_t* lo,
+                                          uint16_t* list, volatile uint8_t* st) {
+  __shared__ int s_len;
+  __shared__ long long s_part[32];
+  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {  // lower rows are row prefixes
+    int64_t a = off[v], b = off[v + 1];
+    const int64_t e0 = a;
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (nbr[mid] < v) a = mid + 1; else b = mid;
+    }
+    lo[v] = static_cast<uint16_t>(a - e0);
+  }
+  long long total = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_len = 0;
+    __syncthreads();
+    // build_gain_table (localsearch.cpp:17-26) + the seeds of P
+    for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+      const uint8_t sv = sd[v];
+      int32_t same = 0;
+      const int64_t e0 = off[v];
+      const int32_t deg = static_cast<int32_t>(off[v + 1] - e0);
+#pragma unroll 4
+      for (int32_t k = 0; k < deg; ++k) same += sd[nbr[e0 + k]] == sv ? 1 : -1;
+      d0[v] = same;
+      cnt[v] = same;
+      if (same > 0) {
+        st[v] = 0;
+        list[atomicAdd(&s_len, 1)] = static_cast<uint16_t>(v);
+      } else {
+        st[v] = 1;
+      }
+    }
+    // the closure, one frontier per step
+    for (int32_t a = 0;;) {
+      __syncthreads();
+      const int32_t b = s_len;
+      __syncthreads();  // every thread has b before anyone appends
+      if (a == b) break;
+      for (int32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const int32_t u = list[i];
+        const uint8_t su = sd[u];
+        const int64_t e1 = off[u + 1];
+        for (int64_t e = off[u] + lo[u]; e < e1; ++e) {
+          const int32_t v = nbr[e];
+          if (sd[v] == su) continue;
+          const int32_t old = atomicAdd(&cnt[v], 2);
+          if (old <= 0 && old > -2) {  // crossed zero: v joins P
+            st[v] = 0;
+            list[atomicAdd(&s_len, 1)] = static_cast<uint16_t>(v);
+          }
+        }
+      }
+      a = b;
+    }
+    const int32_t len = s_len;
+    // decision rounds (k_flip_round) over P
+    for (;;) {
+      int und = 0;
+      for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+        const int32_t v = list[i];
+        if (st[v]) continue;
+        const uint8_t sv = sd[v];
+        int32_t base = d0[v], dn = 0, up = 0;
+        const int64_t e0 = off[v];
+        const int32_t L = lo[v];
+#pragma unroll 4
+        for (int32_t k = 0; k < L; ++k) {
+          const int32_t u = nbr[e0 + k];
+          const int32_t c = sd[u] == sv ? -2 : 2;
+          const uint8_t su = st[u];
+          if (su == 2)
+            base += c;
+          else if (su == 0)
+            (c < 0 ? dn : up) += c;
+        }
+        if (base + dn > 0)
+          st[v] = 2;
+        else if (base + up <= 0)
+          st[v] = 1;
+        else
+          und = 1;
+      }
+      if (!__syncthreads_or(und)) break;
+    }
+    // the pass's gain (k_flip_commit), then its flips
+    long long g = 0;
+    int flips = 0;
+    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t v = list[i];
+      if (st[v] != 2) continue;
+      ++flips;
+      const uint8_t sv = sd[v];
+      int32_t at = d0[v];
+      const int64_t e0 = off[v];
+      const int32_t L = lo[v];
+#pragma unroll 4
+      for (int32_t k = 0; k < L; ++k) {
+        const int32_t u = nbr[e0 + k];
+        if (st[u] == 2) at += sd[u] == sv ? -2 : 2;
+      }
+      g += at;
+    }
+    for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = g;
+    const bool any = __syncthreads_or(flips) != 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += s_part[w];
+    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const int32_t v = list[i];
+      if (st[v] == 2) sd[v] ^= 1;
+    }
+    __syncthreads();
+    if (!any) break;  // a pass without a flip ends one_flip_pass
+  }
+  return total;
+}
+
 // two_flip_pass (localsearch.cpp:159-181) of one body: every thread tests
 // its vertices exactly (two_cand: a possible joint flip with a higher
 // neighbour), then warp 0 visits the marked vertices in order, walks each
@@ -2162,10 +2293,10 @@ __device__ long long small_two_flip(const int64_t* off, const int32_t* nbr,
 }
 
 // OP: MQO_LS_ONE_FLIP / TWO_FLIP / ONE_TWO_FLIP; out[s] = the gain.  SMEM:
-// the k_one_flip_cta layout (d0 = the gain table, lo_cnt, sides, decision
-// bytes), then the CSR when it fits.  1-flip passes run as CTA decision
-// rounds (cta_one_flip_pass), 2-flip sweeps on warp 0 (2-flip moves are
-// rare next to 1-flip moves).
+// d0 (the gain table), cnt, lo, list, sides, decision bytes
+// (small_state_bytes), then the CSR when it fits.  1-flip passes run as CTA
+// decision rounds over the vertices that can flip (cta_one_flip_closure),
+// 2-flip sweeps on warp 0 (2-flip moves are rare next to 1-flip moves).
 template <int OP, bool CSR>
 __global__ void __launch_bounds__(kFlipCtaThreads, 1)
     k_flip_small(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g,
@@ -2174,14 +2305,16 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   extern __shared__ __align__(16) unsigned char sm[];
   const int s = blockIdx.x;
   int32_t* d0 = reinterpret_cast<int32_t*>(sm);
-  int32_t* lo_cnt = d0 + n;
-  uint8_t* sd = sm + 8 * int64_t(n);
+  int32_t* cnt = d0 + n;
+  uint16_t* lo = reinterpret_cast<uint16_t*>(cnt + n);
+  uint16_t* list = lo + n;
+  uint8_t* sd = reinterpret_cast<uint8_t*>(list + n);
   volatile uint8_t* st = sd + n;
   const int64_t* off = off_g;
   const int32_t* nbr = nbr_g;
   if constexpr (CSR) {
-    int64_t* o = reinterpret_cast<int64_t*>(sm + flip_cta_smem(n));
-    int32_t* nb = reinterpret_cast<int32_t*>(sm + flip_cta_smem(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
+    int64_t* o = reinterpret_cast<int64_t*>(sm + small_state_bytes(n));
+    int32_t* nb = reinterpret_cast<int32_t*>(sm + small_state_bytes(n) + (8 * (int64_t(n) + 1) + 15) / 16 * 16);
     const int64_t nnz = off_g[n];
     for (int64_t i = threadIdx.x; i <= n; i += blockDim.x) o[i] = off_g[i];
 #pragma unroll 4
@@ -2192,13 +2325,13 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   small_unpack(packed + s * W, W, n, sd);
   __syncthreads();
   long long total = 0;
-  if constexpr (OP == MQO_LS_ONE_FLIP) total = cta_one_flip_pass(off, nbr, n, sd, d0, lo_cnt, st);
+  auto one_flip = [&] { return cta_one_flip_closure(off, nbr, n, sd, d0, cnt, lo, list, st); };
+  if constexpr (OP == MQO_LS_ONE_FLIP) total = one_flip();
   uint8_t* cand = const_cast<uint8_t*>(st);  // the decision bytes double as 2-flip marks
   if constexpr (OP == MQO_LS_TWO_FLIP) total = small_two_flip(off, nbr, hmax, n, sd, d0, cand);
   if constexpr (OP == MQO_LS_ONE_TWO_FLIP) {  // localsearch.cpp:183-190
     for (;;) {
-      const long long r = cta_one_flip_pass(off, nbr, n, sd, d0, lo_cnt, st) +
-                          small_two_flip(off, nbr, hmax, n, sd, d0, cand);
+      const long long r = one_flip() + small_two_flip(off, nbr, hmax, n, sd, d0, cand);
       total += r;
       if (__syncthreads_or(r != 0) == 0) break;
     }
@@ -2208,7 +2341,6 @@ __global__ void __launch_bounds__(kFlipCtaThreads, 1)
   if (threadIdx.x == 0) out[s] = total;
 }
 
-inline int64_t small_state_bytes(int32_t n) { return flip_cta_smem(n); }
 inline int64_t small_csr_bytes(int32_t n, int64_t nnz) {
   return (8 * (int64_t(n) + 1) + 15) / 16 * 16 + 4 * nnz;
 }
