@@ -2098,17 +2098,40 @@ __device__ __forceinline__ void small_flip(const int64_t* off, const int32_t* nb
 // are decided "keep" before the rounds start and the rounds walk a compact
 // list.  Late passes flip a handful of vertices, so P is small; the
 // unrestricted rounds re-walked every undecided row (ncu r22: 30 rounds,
-// 252k cycles at n = 1024, d = 16).  SMEM (n <= 65535): d0, cnt [n] int32,
-// lo, list [n] uint16, side, st [n] bytes.  Leaves d0 = the gain table of
-// the final state.  Returns the gain on every thread.
+// 252k cycles at n = 1024, d = 16).
+//
+// Every phase is a chain of dependent SMEM loads per row, so a phase costs
+// its longest row walk: each list item gets a group of G lanes (G = the
+// largest power of two <= threads / items, <= 32) that stride its row and
+// reduce with shuffles, so a short list still spreads over the CTA.  The
+// gain table is built once and then updated from each pass's flips (a
+// flipped row recomputed, its unflipped neighbours +-2), not rebuilt.
+// SMEM (n <= 65535): d0, cnt [n] int32, lo, list [n] uint16, side, st [n]
+// bytes.  Leaves d0 = the gain table of the final state.  Returns the gain
+// on every thread.
 __host__ __device__ inline int64_t small_state_bytes(int32_t n) { return (14 * int64_t(n) + 15) / 16 * 16; }
+
+// lanes per item for `items` items over the CTA
+__device__ __forceinline__ int group_lanes(int32_t items) {
+  const int32_t per = items > 0 ? static_cast<int32_t>(blockDim.x) / items : 32;
+  if (per >= 32) return 32;
+  if (per <= 1) return 1;
+  return 1 << (31 - __clz(per));
+}
+
+// sum over the G-lane group (G a power of two); every lane of the warp calls it
+__device__ __forceinline__ int32_t group_sum(int32_t x, int G) {
+  for (int o = 1; o < G; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
 
 __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr, int32_t n,
                                           uint8_t* sd, int32_t* d0, int32_t* cnt, uint16_t* lo,
                                           uint16_t* list, volatile uint8_t* st) {
   __shared__ int s_len;
   __shared__ long long s_part[32];
-  for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {  // lower rows are row prefixes
+  const int32_t T = static_cast<int32_t>(blockDim.x);
+  for (int32_t v = threadIdx.x; v < n; v += T) {  // lower rows are row prefixes
     int64_t a = off[v], b = off[v + 1];
     const int64_t e0 = a;
     while (a < b) {
@@ -2116,22 +2139,23 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
       if (nbr[mid] < v) a = mid + 1; else b = mid;
     }
     lo[v] = static_cast<uint16_t>(a - e0);
+    // build_gain_table (localsearch.cpp:17-26), once
+    const uint8_t sv = sd[v];
+    int32_t same = 0;
+    const int32_t deg = static_cast<int32_t>(off[v + 1] - e0);
+#pragma unroll 4
+    for (int32_t k = 0; k < deg; ++k) same += sd[nbr[e0 + k]] == sv ? 1 : -1;
+    d0[v] = same;
   }
   long long total = 0;
   for (;;) {
     if (threadIdx.x == 0) s_len = 0;
     __syncthreads();
-    // build_gain_table (localsearch.cpp:17-26) + the seeds of P
-    for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
-      const uint8_t sv = sd[v];
-      int32_t same = 0;
-      const int64_t e0 = off[v];
-      const int32_t deg = static_cast<int32_t>(off[v + 1] - e0);
-#pragma unroll 4
-      for (int32_t k = 0; k < deg; ++k) same += sd[nbr[e0 + k]] == sv ? 1 : -1;
-      d0[v] = same;
-      cnt[v] = same;
-      if (same > 0) {
+    // the seeds of P; everything else "keep" until admitted
+    for (int32_t v = threadIdx.x; v < n; v += T) {
+      const int32_t d = d0[v];
+      cnt[v] = d;
+      if (d > 0) {
         st[v] = 0;
         list[atomicAdd(&s_len, 1)] = static_cast<uint16_t>(v);
       } else {
@@ -2144,11 +2168,13 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
       const int32_t b = s_len;
       __syncthreads();  // every thread has b before anyone appends
       if (a == b) break;
-      for (int32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+      const int G = group_lanes(b - a);
+      const int32_t gl = threadIdx.x & (G - 1);
+      for (int32_t i = a + static_cast<int32_t>(threadIdx.x) / G; i < b; i += T / G) {
         const int32_t u = list[i];
         const uint8_t su = sd[u];
         const int64_t e1 = off[u + 1];
-        for (int64_t e = off[u] + lo[u]; e < e1; ++e) {
+        for (int64_t e = off[u] + lo[u] + gl; e < e1; e += G) {
           const int32_t v = nbr[e];
           if (sd[v] == su) continue;
           const int32_t old = atomicAdd(&cnt[v], 2);
@@ -2161,63 +2187,105 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
       a = b;
     }
     const int32_t len = s_len;
+    const int G = group_lanes(len);
+    const int32_t gl = threadIdx.x & (G - 1);
+    const int32_t ng = T / G;
+    // warp-uniform trip counts (the group sums shuffle over whole warps)
+    const int32_t steps = (len + ng - 1) / ng;
     // decision rounds (k_flip_round) over P
     for (;;) {
       int und = 0;
-      for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
-        const int32_t v = list[i];
-        if (st[v]) continue;
-        const uint8_t sv = sd[v];
-        int32_t base = d0[v], dn = 0, up = 0;
-        const int64_t e0 = off[v];
-        const int32_t L = lo[v];
-#pragma unroll 4
-        for (int32_t k = 0; k < L; ++k) {
-          const int32_t u = nbr[e0 + k];
-          const int32_t c = sd[u] == sv ? -2 : 2;
-          const uint8_t su = st[u];
-          if (su == 2)
-            base += c;
-          else if (su == 0)
-            (c < 0 ? dn : up) += c;
+      for (int32_t t = 0; t < steps; ++t) {
+        const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
+        int32_t v = -1;
+        if (i < len) {
+          v = list[i];
+          if (st[v]) v = -1;
         }
-        if (base + dn > 0)
-          st[v] = 2;
-        else if (base + up <= 0)
-          st[v] = 1;
-        else
-          und = 1;
+        int32_t add = 0, span = 0;  // span: up in the low 16 bits, -dn above
+        uint8_t sv = 0;
+        if (v >= 0) {
+          sv = sd[v];
+          const int64_t e0 = off[v];
+          const int32_t L = lo[v];
+#pragma unroll 4
+          for (int32_t k = gl; k < L; k += G) {
+            const int32_t u = nbr[e0 + k];
+            const bool same = sd[u] == sv;
+            const uint8_t su = st[u];
+            if (su == 2)
+              add += same ? -2 : 2;
+            else if (su == 0)
+              span += same ? (2 << 16) : 2;
+          }
+        }
+        add = group_sum(add, G);
+        span = group_sum(span, G);
+        if (v >= 0 && gl == 0) {
+          const int32_t base = d0[v] + add, dn = -(span >> 16), up = span & 0xffff;
+          if (base + dn > 0)
+            st[v] = 2;
+          else if (base + up <= 0)
+            st[v] = 1;
+          else
+            und = 1;
+        }
       }
       if (!__syncthreads_or(und)) break;
     }
-    // the pass's gain (k_flip_commit), then its flips
+    // the pass's gain (k_flip_commit)
     long long g = 0;
     int flips = 0;
-    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
-      const int32_t v = list[i];
-      if (st[v] != 2) continue;
-      ++flips;
-      const uint8_t sv = sd[v];
-      int32_t at = d0[v];
-      const int64_t e0 = off[v];
-      const int32_t L = lo[v];
+    for (int32_t t = 0; t < steps; ++t) {
+      const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
+      const int32_t v = i < len && st[list[i]] == 2 ? list[i] : -1;
+      int32_t at = 0;
+      if (v >= 0) {
+        const uint8_t sv = sd[v];
+        const int64_t e0 = off[v];
+        const int32_t L = lo[v];
 #pragma unroll 4
-      for (int32_t k = 0; k < L; ++k) {
-        const int32_t u = nbr[e0 + k];
-        if (st[u] == 2) at += sd[u] == sv ? -2 : 2;
+        for (int32_t k = gl; k < L; k += G) {
+          const int32_t u = nbr[e0 + k];
+          if (st[u] == 2) at += sd[u] == sv ? -2 : 2;
+        }
       }
-      g += at;
+      at = group_sum(at, G);
+      if (v >= 0 && gl == 0) {
+        g += d0[v] + at;
+        ++flips;
+      }
     }
     for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
     if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = g;
     const bool any = __syncthreads_or(flips) != 0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += s_part[w];
-    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+    for (int w = 0; w < (T >> 5); ++w) total += s_part[w];
+    if (!any) break;  // a pass without a flip ends one_flip_pass
+    for (int32_t i = threadIdx.x; i < len; i += T) {
       const int32_t v = list[i];
       if (st[v] == 2) sd[v] ^= 1;
     }
     __syncthreads();
-    if (!any) break;  // a pass without a flip ends one_flip_pass
+    // the gain table of the new sides: flipped rows recomputed, their
+    // unflipped neighbours +-2 (apply_flip, localsearch.cpp:28-33)
+    for (int32_t t = 0; t < steps; ++t) {
+      const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
+      const int32_t v = i < len && st[list[i]] == 2 ? list[i] : -1;
+      int32_t same = 0;
+      if (v >= 0) {
+        const uint8_t sv = sd[v];
+        const int64_t e0 = off[v], e1 = off[v + 1];
+        for (int64_t e = e0 + gl; e < e1; e += G) {
+          const int32_t u = nbr[e];
+          const bool eq = sd[u] == sv;
+          same += eq ? 1 : -1;
+          if (st[u] != 2) atomicAdd(&d0[u], eq ? 2 : -2);
+        }
+      }
+      same = group_sum(same, G);
+      if (v >= 0 && gl == 0) d0[v] = same;
+    }
+    __syncthreads();
   }
   return total;
 }
