@@ -2108,7 +2108,7 @@ __device__ __forceinline__ void small_flip(const int64_t* off, const int32_t* nb
 // flipped row recomputed, its unflipped neighbours +-2), not rebuilt.
 // SMEM (n <= 65535): d0, cnt [n] int32, lo, list [n] uint16, side, st [n]
 // bytes.  Leaves d0 = the gain table of the final state.  Returns the gain
-// on every thread.
+// on warp 0 (0 elsewhere).
 __host__ __device__ inline int64_t small_state_bytes(int32_t n) { return (14 * int64_t(n) + 15) / 16 * 16; }
 
 // lanes per item for `items` items over the CTA
@@ -2162,8 +2162,20 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
         st[v] = 1;
       }
     }
+    // many seeds (a pass from a random state): P is most of the graph, and
+    // its closure steps cost more than they save -- every vertex is listed
+    __syncthreads();
+    const bool all = int64_t(s_len) * 4 > n;
+    if (all) {
+      for (int32_t v = threadIdx.x; v < n; v += T) {
+        list[v] = static_cast<uint16_t>(v);
+        st[v] = 0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) s_len = n;
+    }
     // the closure, one frontier per step
-    for (int32_t a = 0;;) {
+    for (int32_t a = all ? n : 0;;) {
       __syncthreads();
       const int32_t b = s_len;
       __syncthreads();  // every thread has b before anyone appends
@@ -2190,12 +2202,14 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
     const int G = group_lanes(len);
     const int32_t gl = threadIdx.x & (G - 1);
     const int32_t ng = T / G;
-    // warp-uniform trip counts (the group sums shuffle over whole warps)
+    // warp-uniform trip counts (the group sums shuffle over whole warps);
+    // a warp whose groups are all past the list skips the step
     const int32_t steps = (len + ng - 1) / ng;
+    const int32_t wg0 = static_cast<int32_t>(threadIdx.x & ~31u) / G;  // the warp's first group
     // decision rounds (k_flip_round) over P
     for (;;) {
       int und = 0;
-      for (int32_t t = 0; t < steps; ++t) {
+      for (int32_t t = 0; t < steps && t * ng + wg0 < len; ++t) {
         const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
         int32_t v = -1;
         if (i < len) {
@@ -2236,7 +2250,7 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
     // the pass's gain (k_flip_commit)
     long long g = 0;
     int flips = 0;
-    for (int32_t t = 0; t < steps; ++t) {
+    for (int32_t t = 0; t < steps && t * ng + wg0 < len; ++t) {
       const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
       const int32_t v = i < len && st[list[i]] == 2 ? list[i] : -1;
       int32_t at = 0;
@@ -2259,7 +2273,11 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
     for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
     if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = g;
     const bool any = __syncthreads_or(flips) != 0;
-    for (int w = 0; w < (T >> 5); ++w) total += s_part[w];
+    if (threadIdx.x < 32) {  // the warp partials, summed on warp 0 only
+      long long p = threadIdx.x < (T >> 5) ? s_part[threadIdx.x] : 0;
+      for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+      total += p;
+    }
     if (!any) break;  // a pass without a flip ends one_flip_pass
     for (int32_t i = threadIdx.x; i < len; i += T) {
       const int32_t v = list[i];
@@ -2268,7 +2286,7 @@ __device__ long long cta_one_flip_closure(const int64_t* off, const int32_t* nbr
     __syncthreads();
     // the gain table of the new sides: flipped rows recomputed, their
     // unflipped neighbours +-2 (apply_flip, localsearch.cpp:28-33)
-    for (int32_t t = 0; t < steps; ++t) {
+    for (int32_t t = 0; t < steps && t * ng + wg0 < len; ++t) {
       const int32_t i = t * ng + static_cast<int32_t>(threadIdx.x) / G;
       const int32_t v = i < len && st[list[i]] == 2 ? list[i] : -1;
       int32_t same = 0;
