@@ -1265,6 +1265,65 @@ __device__ bool lane_swap_pair(const int64_t* off, const int32_t* nbr, const uin
   return false;
 }
 
+// lane_swap_pair without the dependent chain per neighbour: the row is
+// read four entries at a time (four independent selection/tightness loads in
+// flight), the first four candidates are kept in registers, and their six
+// pairs are tested together (independent binary searches), the first
+// non-adjacent one in (i, j) order winning.  Rows with more than four
+// candidates whose first four are pairwise adjacent (rare: two random
+// neighbours are adjacent with probability ~ degree / n) fall back to the
+// exact serial search.  Callers order every access to sel / tight with
+// barriers (no concurrent writer), so the loads are plain.
+__device__ bool lane_swap_pair_fast(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+                                    const int32_t* tight, int32_t x, int32_t& pu, int32_t& pw) {
+  if (!sel[x]) return false;
+  const int64_t e0 = off[x], e1 = off[x + 1];
+  int32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;  // the first four candidates
+  int k = 0;
+  bool more = false;  // a fifth candidate may exist (scan stopped at four)
+  for (int64_t a = e0; a < e1; a += 4) {
+    if (k >= 4) {
+      more = true;
+      break;
+    }
+    int32_t u[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) u[q] = a + q < e1 ? nbr[a + q] : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ok[q] = u[q] >= 0 && !sel[u[q]] && tight[u[q]] == 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (ok[q]) {
+        if (k == 0) c0 = u[q];
+        if (k == 1) c1 = u[q];
+        if (k == 2) c2 = u[q];
+        if (k == 3) c3 = u[q];
+        if (k == 4) more = true;
+        ++k;
+      }
+    }
+  }
+  if (k < 2) return false;
+  // the pairs among the first four in swap_pair_for's (i, j) order, tested
+  // together: (0,1) (0,2) (0,3) (1,2) (1,3) (2,3)
+  const bool t02 = k >= 3, t03 = k >= 4;
+  const bool a01 = has_edge(off, nbr, c0, c1);
+  const bool a02 = t02 ? has_edge(off, nbr, c0, c2) : true;
+  const bool a03 = t03 ? has_edge(off, nbr, c0, c3) : true;
+  const bool a12 = t02 ? has_edge(off, nbr, c1, c2) : true;
+  if (!a01) { pu = c0; pw = c1; return true; }
+  if (!a02) { pu = c0; pw = c2; return true; }
+  if (!a03) { pu = c0; pw = c3; return true; }
+  if (more) return lane_swap_pair(off, nbr, sel, tight, x, pu, pw);  // (0, j >= 4) come next
+  if (!a12) { pu = c1; pw = c2; return true; }
+  if (t03) {
+    if (!has_edge(off, nbr, c1, c3)) { pu = c1; pw = c3; return true; }
+    if (!has_edge(off, nbr, c2, c3)) { pu = c2; pw = c3; return true; }
+  }
+  return false;
+}
+
 // Adds vertex z to the set: sel[z] = 1, tight[N(z)] += 1 (warp-parallel).
 __device__ __forceinline__ void warp_select(const int64_t* off, const int32_t* nbr, uint8_t* sel,
                                             int32_t* tight, int32_t z, int delta, int lane) {
@@ -1674,7 +1733,7 @@ __global__ void __launch_bounds__(32 * W)
     for (int32_t k = threadIdx.x; k < nd; k += blockDim.x) {
       const int32_t x = dl[cur][k];
       int32_t pu = 0, pw = 0;
-      if (lane_swap_pair(off, nbr, sel, tight, x, pu, pw)) {
+      if (lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw)) {
         dl[cur ^ 1][atomicAdd(&s_keep, 1)] = x;  // re-checked after the next swap
         if (x < mx) {
           mx = x;
@@ -1707,7 +1766,7 @@ __global__ void __launch_bounds__(32 * W)
     for (int32_t base = frontier; base < n; base += blockDim.x) {
       const int32_t x = base + threadIdx.x;
       int32_t pu = 0, pw = 0;
-      if (x < n && lane_swap_pair(off, nbr, sel, tight, x, pu, pw)) {
+      if (x < n && lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw)) {
         atomicMin(&s_best, x);
         mx = x;
         mu = pu;
