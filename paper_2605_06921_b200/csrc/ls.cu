@@ -1274,7 +1274,7 @@ __device__ bool lane_swap_pair(const int64_t* off, const int32_t* nbr, const uin
 // neighbours are adjacent with probability ~ degree / n) fall back to the
 // exact serial search.  Callers order every access to sel / tight with
 // barriers (no concurrent writer), so the loads are plain.
-__device__ bool lane_swap_pair_fast(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+__device__ __forceinline__ bool lane_swap_pair_fast(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
                                     const int32_t* tight, int32_t x, int32_t& pu, int32_t& pw) {
   if (!sel[x]) return false;
   const int64_t e0 = off[x], e1 = off[x + 1];
@@ -1403,7 +1403,7 @@ __device__ void warp_apply_swap(const int64_t* off, const int32_t* nbr, const in
 // whole CTA (cta_mark_dirty), against the final selection: only selected
 // vertices need re-examination, and every vertex whose swap pair could
 // have changed is within two hops of x, u, w or a re-added vertex.
-__device__ void warp_swap_core(const int64_t* off, const int32_t* nbr, uint8_t* sel,
+__device__ __forceinline__ void warp_swap_core(const int64_t* off, const int32_t* nbr, uint8_t* sel,
                                int32_t* tight, int32_t* freed, int32_t x, int32_t u, int32_t w,
                                int lane, int32_t* nadd) {
   warp_select(off, nbr, sel, tight, x, -1, lane);
@@ -1446,7 +1446,7 @@ __device__ void warp_swap_core(const int64_t* off, const int32_t* nbr, uint8_t* 
 
 // Dirty marks for the 2-hop neighbourhood of t by the whole CTA: warps over
 // s in {t} U N(t), lanes over y in {s} U N(s).
-__device__ void cta_mark_dirty(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
+__device__ __forceinline__ void cta_mark_dirty(const int64_t* off, const int32_t* nbr, const uint8_t* sel,
                                uint8_t* dflag, int32_t* dlist, int32_t* dcount, int32_t t,
                                int32_t frontier) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1466,7 +1466,7 @@ __device__ void cta_mark_dirty(const int64_t* off, const int32_t* nbr, const uin
 }
 
 // A full swap by the CTA: the core on warp 0, then the marks by everyone.
-__device__ void cta_apply_swap(const int64_t* off, const int32_t* nbr, uint8_t* sel, int32_t* tight,
+__device__ __forceinline__ void cta_apply_swap(const int64_t* off, const int32_t* nbr, uint8_t* sel, int32_t* tight,
                                uint8_t* dflag, int32_t* dlist, int32_t* dcount, int32_t* freed,
                                int32_t x, int32_t u, int32_t w, int32_t frontier, int32_t* s_nadd) {
   if ((threadIdx.x >> 5) == 0)
@@ -1658,7 +1658,7 @@ __host__ __device__ inline int64_t swap_cta_smem_bytes(int32_t n, int64_t nnz, i
   return swap_smem_bytes(n, nnz, max_degree) + (4 * int64_t(n) + 15) / 16 * 16;
 }
 
-template <int W>
+template <int W, bool SM>
 __global__ void __launch_bounds__(32 * W)
     k_mis_swap_cta(const int64_t* __restrict__ off_g, const int32_t* __restrict__ nbr_g, int32_t n,
                    int32_t count, uint8_t* sel_all, int32_t* tight_all, uint8_t* dflag_all,
@@ -1677,10 +1677,14 @@ __global__ void __launch_bounds__(32 * W)
   uint8_t* sel = sel_g;
   int32_t* tight = tight_all + static_cast<int64_t>(s) * n;
   uint8_t* dflag = dflag_all + static_cast<int64_t>(s) * (n + 4);
-  int32_t* dl[2] = {dlist_all + static_cast<int64_t>(s) * n, dlist2_all + static_cast<int64_t>(s) * n};
+  // two dirty lists, swapped by `cur` (selects, not an indexed array: the
+  // compiler then keeps their SMEM address space)
+  int32_t* dla = dlist_all + static_cast<int64_t>(s) * n;
+  int32_t* dlb = dlist2_all + static_cast<int64_t>(s) * n;
   int32_t* freed = freed_all + static_cast<int64_t>(s) * (max_degree + 1);
   int32_t* dcount = dcount_all + s;
-  if (smem) {
+  (void)smem;
+  if constexpr (SM) {  // SMEM-resident state: the pointers below compile to LDS/STS
     auto al = [](int64_t b) { return (b + 15) / 16 * 16; };
     const int64_t nnz = off_g[n];
     unsigned char* p = sm;
@@ -1712,8 +1716,8 @@ __global__ void __launch_bounds__(32 * W)
     sel = se;
     tight = ti;
     dflag = df;
-    dl[0] = d0;
-    dl[1] = d1;
+    dla = d0;
+    dlb = d1;
     freed = fr;
     dcount = dc;
   }
@@ -1731,10 +1735,10 @@ __global__ void __launch_bounds__(32 * W)
     __syncthreads();
     int32_t mx = INT_MAX, mu = 0, mw = 0;
     for (int32_t k = threadIdx.x; k < nd; k += blockDim.x) {
-      const int32_t x = dl[cur][k];
+      const int32_t x = (cur ? dlb : dla)[k];
       int32_t pu = 0, pw = 0;
       if (lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw)) {
-        dl[cur ^ 1][atomicAdd(&s_keep, 1)] = x;  // re-checked after the next swap
+        (cur ? dla : dlb)[atomicAdd(&s_keep, 1)] = x;  // re-checked after the next swap
         if (x < mx) {
           mx = x;
           mu = pu;
@@ -1754,7 +1758,7 @@ __global__ void __launch_bounds__(32 * W)
     cur ^= 1;
     __syncthreads();
     if (s_best != INT_MAX) {
-      cta_apply_swap(off, nbr, sel, tight, dflag, dl[cur], dcount, freed, s_best, s_bu, s_bw,
+      cta_apply_swap(off, nbr, sel, tight, dflag, (cur ? dlb : dla), dcount, freed, s_best, s_bu, s_bw,
                      frontier, &s_nadd);
       ++swaps;
       continue;
@@ -1788,12 +1792,12 @@ __global__ void __launch_bounds__(32 * W)
     __syncthreads();
     if (found == INT_MAX) break;
     frontier = found + 1;
-    cta_apply_swap(off, nbr, sel, tight, dflag, dl[cur], dcount, freed, found, s_bu, s_bw, frontier,
+    cta_apply_swap(off, nbr, sel, tight, dflag, (cur ? dlb : dla), dcount, freed, found, s_bu, s_bw, frontier,
                    &s_nadd);
     ++swaps;
   }
   if (threadIdx.x == 0) swaps_out[s] = swaps;
-  if (smem)
+  if constexpr (SM)
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) sel_g[i] = sel[i];
 }
 
@@ -2070,19 +2074,18 @@ void launch_swap_cta(const mqo_graph* g, int32_t count, LsWork& w, int64_t* d_ou
   alloc_swap_lists(g, count, w, st, true);
   const int64_t cbytes = swap_cta_smem_bytes(g->n, 2 * g->m, g->max_degree);
   const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
-  {
+  auto kern = csm ? k_mis_swap_cta<16, true> : k_mis_swap_cta<16, false>;
+  if (csm) {  // the SMEM opt-in, once per device
     static std::mutex mu;
-    static bool done[64] = {false};
+    static std::set<int> done;
     int dev = 0;
     MQO_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lock(mu);
-    if (dev >= 64 || !done[dev]) {
-      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (done.insert(dev).second)
+      MQO_CUDA(cudaFuncSetAttribute(k_mis_swap_cta<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSwapSmemMax - 1024)));
-      if (dev < 64) done[dev] = true;
-    }
   }
-  k_mis_swap_cta<16><<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
+  kern<<<count, 512, csm ? static_cast<size_t>(cbytes) : 0, st>>>(
       g->d_off, g->d_nbr, g->n, count, w.bytes, w.ints, w.dflag, w.dlist, w.dlist2, w.freed,
       w.small, g->max_degree, d_out, csm ? 1 : 0, d_bad);
   MQO_CUDA(cudaGetLastError());
