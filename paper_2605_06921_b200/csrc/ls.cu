@@ -1763,14 +1763,16 @@ __global__ void __launch_bounds__(32 * W)
       ++swaps;
       continue;
     }
-    // 2. first swappable vertex at or after the frontier, W*32 per step
+    // 2. first swappable vertex at or after the frontier.  The next one is
+    // usually a few vertices on, so the window starts at two warps and
+    // doubles up to the CTA (a step costs its slowest row search)
     if (threadIdx.x == 0) s_best = INT_MAX;
     __syncthreads();
     int32_t found = INT_MAX;
-    for (int32_t base = frontier; base < n; base += blockDim.x) {
+    for (int32_t base = frontier, win = 64; base < n; base += win, win = min(2 * win, static_cast<int32_t>(blockDim.x))) {
       const int32_t x = base + threadIdx.x;
       int32_t pu = 0, pw = 0;
-      if (x < n && lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw)) {
+      if (static_cast<int32_t>(threadIdx.x) < win && x < n && lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw)) {
         atomicMin(&s_best, x);
         mx = x;
         mu = pu;
