@@ -1525,7 +1525,7 @@ __device__ int64_t warp_swap_loop(const int64_t* off, const int32_t* nbr, uint8_
       bool ok = false;
       if (k < nd) {
         x = dlist[k];
-        ok = lane_swap_pair(off, nbr, sel, tight, x, pu, pw);
+        ok = lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw);
       }
       if (ok && x < best) {
         best = x;
@@ -1566,7 +1566,7 @@ __device__ int64_t warp_swap_loop(const int64_t* off, const int32_t* nbr, uint8_
     for (int32_t cb = frontier; cb < n; cb += 32) {
       const int32_t x = cb + lane;
       int32_t pu = 0, pw = 0;
-      const bool ok = x < n && lane_swap_pair(off, nbr, sel, tight, x, pu, pw);
+      const bool ok = x < n && lane_swap_pair_fast(off, nbr, sel, tight, x, pu, pw);
       const unsigned m = __ballot_sync(0xffffffffu, ok);
       if (m) {
         const int i = warp_first(m);
