@@ -168,7 +168,7 @@ def test_one_flip_cta_variants_vs_oracle(O, P, n, d, bodies):
 
 
 @pytest.mark.parametrize("n,d", [(1024, 16), (4096, 8), (16384, 8)])
-@pytest.mark.parametrize("op", ["two_flip", "one_two_flip", "swap"])
+@pytest.mark.parametrize("op", ["one_flip", "two_flip", "one_two_flip", "swap"])
 @pytest.mark.parametrize("bodies", [1, 5])
 def test_single_launch_small_bodies_vs_oracle(O, P, n, d, op, bodies):
     """The single-launch kernels (k_flip_small / k_swap_small, n <= 16384;
@@ -195,11 +195,48 @@ def test_single_launch_small_bodies_vs_oracle(O, P, n, d, op, bodies):
             ref, size = O.one_two_swap(og, start[k])
             assert out[k] == size and (got[k] == ref).all(), k
         return
-    opc = _lib.LS_TWO_FLIP if op == "two_flip" else _lib.LS_ONE_TWO_FLIP
+    opc = {"one_flip": _lib.LS_ONE_FLIP, "two_flip": _lib.LS_TWO_FLIP,
+           "one_two_flip": _lib.LS_ONE_TWO_FLIP}[op]
     sides = rng.integers(0, 2, (bodies, n)).astype(np.uint8)
     packed, gains = P.local_search(b, opc, P.pack_bodies(sides))
     got = P.unpack_bodies(packed, n)
     for k in range(bodies):
-        fn = O.two_flip_pass if op == "two_flip" else O.one_two_flip
+        fn = {"one_flip": O.one_flip_pass, "two_flip": O.two_flip_pass,
+              "one_two_flip": O.one_two_flip}[op]
         ref, gain = fn(og, sides[k])
         assert gains[k] == gain and (got[k] == ref).all(), k
+
+
+@pytest.mark.parametrize("graph", ["ba", "er_dense"])
+def test_small_bodies_hubs_and_dense_vs_oracle(O, P, graph):
+    """Single-launch 1-flip (closure + grouped rounds) and the swap kernel's
+    batched pair search where rows are long and candidate pairs are often
+    adjacent: BA(3000, 6) hubs, ER(400, 0.15)."""
+    from paper_2605_06921_b200 import _lib
+    if graph == "ba":
+        og, pg, n = O.generate_ba(3000, 6, 9), P.generate(P.BaSpec(3000, 6), 9), 3000
+    else:
+        og, pg, n = O.generate_er(400, 0.15, 9), P.generate(P.ErSpec(400, 0.15), 9), 400
+    b = P.ChainBatch(pg, 1)
+    rng = np.random.default_rng(5)
+    sides = rng.integers(0, 2, (4, n)).astype(np.uint8)
+    for opc, fn in ((_lib.LS_ONE_FLIP, O.one_flip_pass), (_lib.LS_ONE_TWO_FLIP, O.one_two_flip)):
+        packed, gains = P.local_search(b, opc, P.pack_bodies(sides))
+        got = P.unpack_bodies(packed, n)
+        for k in range(4):
+            ref, gain = fn(og, sides[k])
+            assert gains[k] == gain and (got[k] == ref).all(), (opc, k)
+    starts = []
+    for k in range(4):
+        ind = np.zeros(n, np.uint8)
+        for v in rng.permutation(n)[: n // 10]:
+            ind[v] = 1
+            if not O.is_independent(og, ind):
+                ind[v] = 0
+        starts.append(O.greedy_maximalize(og, ind)[0])
+    starts = np.array(starts, np.uint8)
+    packed, sizes = P.local_search(b, _lib.LS_ONE_TWO_SWAP, P.pack_bodies(starts))
+    got = P.unpack_bodies(packed, n)
+    for k in range(4):
+        ref, size = O.one_two_swap(og, starts[k])
+        assert sizes[k] == size and (got[k] == ref).all(), k
