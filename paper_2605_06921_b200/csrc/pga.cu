@@ -105,6 +105,11 @@ struct Tune {
 // for MIS (its checker counters add registers).
 using TuneDefault = Tune<4, 3, 1>;
 using TuneMis = Tune<3, 4, 1>;
+// Hub graphs (BA-like degree skew), MaxCut objectives: the next batch's
+// neighbour ids loaded one batch early (C4 16 chains 0.278 -> 0.247 ms, 128
+// chains 1.956 -> 1.941 ms; on ER graphs it costs registers for nothing:
+// C3 x 256 0.221 -> 0.272 ms, so those keep TuneDefault).
+using TuneHub = Tune<4, 3, 1, true>;
 template <int KIND>
 using TuneFor = std::conditional_t<KIND == MQO_MIS_QUBO, TuneMis, TuneDefault>;
 
@@ -803,8 +808,21 @@ PassFn pass_fn_tu(int kind, int cpl) {
   throw std::invalid_argument("objective: unknown kind");
 }
 
+// A degree distribution with hubs: the maximum far above the mean (the
+// same test as the persistent-trajectory split).
+// (MQO_HUB_TUNE=0: TuneDefault everywhere, for A/B runs)
+const bool g_hub_tune = [] {
+  const char* e = std::getenv("MQO_HUB_TUNE");
+  return !(e && *e == '0');
+}();
+bool hub_graph(const mqo_graph* g) {
+  if (!g_hub_tune) return false;
+  const double avg_deg = g->n ? 2.0 * static_cast<double>(g->m) / g->n : 0.0;
+  return g->max_degree > 32.0 * avg_deg + 32.0;
+}
+
 template <int MODE>
-PassFn pass_fn(int kind, int cpl) {
+PassFn pass_fn(int kind, int cpl, bool hubs = false) {
   if constexpr (MODE == kStep) {
     switch (k1_variant()) {
       case 1: return pass_fn_tu<MODE, Tune<8, 2, 0>>(kind, cpl);  // round-1 kernel
@@ -823,12 +841,16 @@ PassFn pass_fn(int kind, int cpl) {
     }
   }
   if (kind == MQO_MIS_QUBO) return pass_fn_tu<MODE, TuneMis>(kind, cpl);
+  if constexpr (MODE == kStep)
+    if (hubs) return pass_fn_tu<MODE, TuneHub>(kind, cpl);
   return pass_fn_tu<MODE, TuneDefault>(kind, cpl);
 }
 
-PassFn traj_pass_fn(int kind, int cpl) {
-#define MQO_K(K) \
-  case K:        \
+PassFn traj_pass_fn(int kind, int cpl, bool hubs) {
+#define MQO_K(K)                                                                             \
+  case K:                                                                                    \
+    if constexpr (K != MQO_MIS_QUBO)                                                         \
+      if (hubs) return cpl == 4 ? k_traj_pass<K, 4, TuneHub> : k_traj_pass<K, 1, TuneHub>; \
     return cpl == 4 ? k_traj_pass<K, 4, TuneFor<K>> : k_traj_pass<K, 1, TuneFor<K>>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
@@ -1076,7 +1098,7 @@ void launch_step(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& op
   a.alpha = opt.alpha;
   a.beta = opt.beta;
   if (b->g->n == 0) return;
-  PassFn fn = pass_fn<kStep>(obj.kind, b->cpl);
+  PassFn fn = pass_fn<kStep>(obj.kind, b->cpl, hub_graph(b->g));
   a.Qg = group_quads(b);
   a.hot_rows = hot_rows(b, a.Qg);
   const int blocks = pass_blocks(b, a.Qg);
@@ -1130,7 +1152,7 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
       (cells <= persistent_cells() ||
        (g_persistent_cells == (int64_t(1) << 22) && cells <= (int64_t(1) << 25) &&
         group_quads(b) == b->Q && g->max_degree <= 32.0 * avg_deg + 32.0));
-  PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl);
+  PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl, hub_graph(g));
   const size_t smem = base_smem;
   if (!persistent) {  // chain tiling (see group_quads)
     a.Qg = group_quads(b);
