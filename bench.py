@@ -368,6 +368,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "dram_frac": (traffic["dram_bytes_per_launch"] / launch_s / 1e9 / peak
                               if traffic.get("dram_bytes_per_launch") else None),
                 "kernel": traffic.get("kernel", "k_pass (fused PGA step)")}
+    if traffic.get("l2_bytes_per_launch"):
+        # the chain-tiled gathers are served by L2: its bytes (ncu lts__t_bytes
+        # of the same kernel) against the measured L2 read bandwidth
+        l2 = traffic["l2_bytes_per_launch"] / launch_s / 1e9
+        roofline["l2"] = {"bytes_per_launch": traffic["l2_bytes_per_launch"], "achieved": l2,
+                          "peak": traffic["l2_read_peak_gbs"], "unit": "GB/s",
+                          "frac": l2 / traffic["l2_read_peak_gbs"],
+                          "peak_source": traffic.get("l2_peak_source")}
     del batch
     torch.cuda.synchronize()
 
