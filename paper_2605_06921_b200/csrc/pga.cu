@@ -108,8 +108,15 @@ using TuneMis = Tune<3, 4, 1>;
 // Hub graphs (BA-like degree skew), MaxCut objectives: the next batch's
 // neighbour ids loaded one batch early (C4 16 chains 0.278 -> 0.247 ms, 128
 // chains 1.956 -> 1.941 ms; on ER graphs it costs registers for nothing:
-// C3 x 256 0.221 -> 0.272 ms, so those keep TuneDefault).
-using TuneHub = Tune<4, 3, 1, true>;
+// C3 x 256 0.221 -> 0.272 ms, so those keep TuneDefault), and with the
+// prefetch hiding a round trip, 5 neighbours in flight beat 4 (C4 0.250 ->
+// 0.245 / 0.965 -> 0.954 / 1.939 -> 1.922 ms at 16 / 64 / 128 chains; 4x4,
+// 6x2, 6x3, 8x2 and 3x4 measured slower or spilling: smallb_probe variants).
+using TuneHub = Tune<5, 3, 1, true>;
+// The trajectory pass carries the stop-rule state too: at 5 in flight it
+// spills (79 regs + 32 B stack) and runs slower than 4 (C4 per pass 0.262 /
+// 0.986 / 1.975 ms at 4 vs 0.264 / 1.003 / 1.993 at 5).
+using TuneHubTraj = Tune<4, 3, 1, true>;
 template <int KIND>
 using TuneFor = std::conditional_t<KIND == MQO_MIS_QUBO, TuneMis, TuneDefault>;
 
@@ -837,6 +844,8 @@ PassFn pass_fn(int kind, int cpl, bool hubs = false) {
       case 10: return pass_fn_tu<MODE, Tune<3, 4, 3>>(kind, cpl);
       case 11: return pass_fn_tu<MODE, Tune<4, 3, 1, true>>(kind, cpl);  // index prefetch
       case 12: return pass_fn_tu<MODE, Tune<3, 4, 1, true>>(kind, cpl);
+      case 13: return pass_fn_tu<MODE, Tune<5, 3, 1, true>>(kind, cpl);  // TuneHub
+      case 14: return pass_fn_tu<MODE, Tune<6, 3, 1, true>>(kind, cpl);
       default: break;
     }
   }
@@ -850,7 +859,7 @@ PassFn traj_pass_fn(int kind, int cpl, bool hubs) {
 #define MQO_K(K)                                                                             \
   case K:                                                                                    \
     if constexpr (K != MQO_MIS_QUBO)                                                         \
-      if (hubs) return cpl == 4 ? k_traj_pass<K, 4, TuneHub> : k_traj_pass<K, 1, TuneHub>; \
+      if (hubs) return cpl == 4 ? k_traj_pass<K, 4, TuneHubTraj> : k_traj_pass<K, 1, TuneHubTraj>; \
     return cpl == 4 ? k_traj_pass<K, 4, TuneFor<K>> : k_traj_pass<K, 1, TuneFor<K>>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
