@@ -117,6 +117,10 @@ using TuneHub = Tune<5, 3, 1, true>;
 // spills (79 regs + 32 B stack) and runs slower than 4 (C4 per pass 0.262 /
 // 0.986 / 1.975 ms at 4 vs 0.264 / 1.003 / 1.993 at 5).
 using TuneHubTraj = Tune<4, 3, 1, true>;
+// MIS with chain-tiled (L2-resident) gathers: the prefetch trims the L2
+// round trips (C3 x 256 0.221 -> 0.214 ms, at the measured L2 read
+// bandwidth); untiled ER graphs keep TuneMis (C5 16 chains 4.61 vs 4.91 ms).
+using TuneMisTiled = Tune<3, 4, 1, true>;
 template <int KIND>
 using TuneFor = std::conditional_t<KIND == MQO_MIS_QUBO, TuneMis, TuneDefault>;
 
@@ -829,7 +833,7 @@ bool hub_graph(const mqo_graph* g) {
 }
 
 template <int MODE>
-PassFn pass_fn(int kind, int cpl, bool hubs = false) {
+PassFn pass_fn(int kind, int cpl, bool hubs = false, bool tiled = false) {
   if constexpr (MODE == kStep) {
     switch (k1_variant()) {
       case 1: return pass_fn_tu<MODE, Tune<8, 2, 0>>(kind, cpl);  // round-1 kernel
@@ -849,17 +853,21 @@ PassFn pass_fn(int kind, int cpl, bool hubs = false) {
       default: break;
     }
   }
+  if constexpr (MODE == kStep)
+    if (kind == MQO_MIS_QUBO && tiled) return pass_fn_tu<MODE, TuneMisTiled>(kind, cpl);
   if (kind == MQO_MIS_QUBO) return pass_fn_tu<MODE, TuneMis>(kind, cpl);
   if constexpr (MODE == kStep)
     if (hubs) return pass_fn_tu<MODE, TuneHub>(kind, cpl);
   return pass_fn_tu<MODE, TuneDefault>(kind, cpl);
 }
 
-PassFn traj_pass_fn(int kind, int cpl, bool hubs) {
+PassFn traj_pass_fn(int kind, int cpl, bool hubs, bool tiled) {
 #define MQO_K(K)                                                                             \
   case K:                                                                                    \
     if constexpr (K != MQO_MIS_QUBO)                                                         \
       if (hubs) return cpl == 4 ? k_traj_pass<K, 4, TuneHubTraj> : k_traj_pass<K, 1, TuneHubTraj>; \
+    if constexpr (K == MQO_MIS_QUBO)                                                         \
+      if (tiled) return cpl == 4 ? k_traj_pass<K, 4, TuneMisTiled> : k_traj_pass<K, 1, TuneMisTiled>; \
     return cpl == 4 ? k_traj_pass<K, 4, TuneFor<K>> : k_traj_pass<K, 1, TuneFor<K>>;
   switch (kind) {
     MQO_K(MQO_MIS_QUBO)
@@ -1107,8 +1115,8 @@ void launch_step(mqo_batch* b, const mqo_objective& obj, const mqo_optimizer& op
   a.alpha = opt.alpha;
   a.beta = opt.beta;
   if (b->g->n == 0) return;
-  PassFn fn = pass_fn<kStep>(obj.kind, b->cpl, hub_graph(b->g));
   a.Qg = group_quads(b);
+  PassFn fn = pass_fn<kStep>(obj.kind, b->cpl, hub_graph(b->g), g_hub_tune && a.Qg < b->Q);
   a.hot_rows = hot_rows(b, a.Qg);
   const int blocks = pass_blocks(b, a.Qg);
   launch_groups(b, a, blocks, 0, fn);
@@ -1161,7 +1169,8 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
       (cells <= persistent_cells() ||
        (g_persistent_cells == (int64_t(1) << 22) && cells <= (int64_t(1) << 25) &&
         group_quads(b) == b->Q && g->max_degree <= 32.0 * avg_deg + 32.0));
-  PassFn fn = persistent ? traj_fn(obj.kind, b->cpl) : traj_pass_fn(obj.kind, b->cpl, hub_graph(g));
+  PassFn fn = persistent ? traj_fn(obj.kind, b->cpl)
+                         : traj_pass_fn(obj.kind, b->cpl, hub_graph(g), g_hub_tune && group_quads(b) < b->Q);
   const size_t smem = base_smem;
   if (!persistent) {  // chain tiling (see group_quads)
     a.Qg = group_quads(b);
