@@ -78,9 +78,11 @@ typedef struct {
 
 /* ---- graph store (graph.hpp:20-63) ------------------------------------
  * Uploads an immutable CSR (int64 offsets[n+1], int32 neighbours[2m], rows
- * strictly ascending, no self loops) to `device`.  The invariants of
- * Graph::check_invariants (graph.cpp:44-56) are verified on the host first
- * and a violation returns MQO_ERR_LOGIC with the reference's message.
+ * strictly ascending, no self loops, symmetric) to `device`.  The
+ * invariants of Graph::check_invariants (graph.cpp:44-56) and symmetry are
+ * verified -- on the device for device graphs, on host threads for
+ * host-only ones -- and the first violation in (row, entry) order returns
+ * MQO_ERR_LOGIC / MQO_ERR_INVALID with the reference's message.
 
  * device < 0 keeps a host-only graph (CSR readable, no batches).
  * Replaces: Graph storage + Graph::from_edges's output (graph.cpp:8-42). */
@@ -91,6 +93,10 @@ int mqo_graph_free(mqo_graph* g);
 int mqo_graph_info(const mqo_graph* g, int32_t* n, int64_t* m, int32_t* max_degree);
 /* Copies the canonical CSR back (offsets[n+1], neighbors[2m]). */
 int mqo_graph_csr(const mqo_graph* g, int64_t* offsets, int32_t* neighbors);
+/* The kernels' row schedule of a device graph: vertices by degree
+ * descending, ties by id (order[n]).  Diagnostic; no reference
+ * counterpart. */
+int mqo_graph_row_order(const mqo_graph* g, int32_t* order);
 
 /* Graph::from_edges (graph.hpp:26, graph.cpp:8-42): edges in any order and
  * orientation, duplicates collapsed, self loops rejected

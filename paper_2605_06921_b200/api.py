@@ -167,6 +167,8 @@ lib.mqo_graph_from_edges.argtypes = [C.c_int32, C.c_int64, _I32, _I32, C.c_int32
 lib.mqo_graph_from_edges.restype = C.c_int
 lib.mqo_graph_csr.argtypes = [C.c_void_p, _I64, _I32]
 lib.mqo_graph_csr.restype = C.c_int
+lib.mqo_graph_row_order.argtypes = [C.c_void_p, _I32]
+lib.mqo_graph_row_order.restype = C.c_int
 lib.mqo_graph_save.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
 lib.mqo_graph_save.restype = C.c_int
 lib.mqo_graph_load.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]
@@ -241,6 +243,12 @@ class Graph:
             check(lib.mqo_graph_csr(self._h, _ptr(off, _I64), _ptr(nbr, _I32)))
             self._csr = (off, nbr[: 2 * self._m].copy())
         return self._csr
+
+    def row_order(self) -> np.ndarray:
+        """The kernels' row schedule (device graphs): degree descending, ties by id."""
+        out = np.empty(max(self._n, 1), np.int32)
+        check(lib.mqo_graph_row_order(self._h, _ptr(out, _I32)))
+        return out[: self._n]
 
     def degree(self, v: int) -> int:
         off, _ = self.csr()

@@ -174,12 +174,21 @@ struct mqo_graph {
   int32_t* d_hmax = nullptr;  // max degree over higher neighbours (2-flip filter, lazy)
   int64_t cta_words = 0;
   std::vector<int32_t> h_cta_rows, h_cta_base;  // per-slice rows / ELL base (host copy)
+  // host copy of the CSR: filled at upload for host-only graphs, downloaded on
+  // first use (mqo_b200::host_csr) for device graphs -- the upload itself
+  // never touches the caller's neighbour array on the host
   std::vector<int64_t> h_off;
   std::vector<int32_t> h_nbr;
+  bool h_csr = false;
+  std::mutex host_mu;
   std::vector<int32_t> h_deg_ge;  // [max_degree + 2]: rows of degree >= d (heavy-row planning)
   std::mutex lazy_mu;  // guards the lazily built fields (d_cta, d_hmax): a graph may be
                        // shared by solves running on several host threads
 };
+namespace mqo_b200 {
+// the host CSR of g (downloaded once for device graphs; thread-safe)
+void host_csr(const mqo_graph* g);
+}  // namespace mqo_b200
 
 struct mqo_batch {
   mqo_graph* g = nullptr;

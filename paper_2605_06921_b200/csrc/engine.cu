@@ -727,6 +727,7 @@ extern "C" int mqo_solve_devices(mqo_graph* g, const mqo_solver_config* cfg, con
           if (devices[q] == devices[r]) graphs[r] = graphs[q];
         if (graphs[r]) continue;
         mqo_graph* copy = nullptr;
+        host_csr(g);
         if (mqo_graph_upload(g->n, g->h_off.data(), g->h_nbr.data(), devices[r], &copy) != MQO_OK)
           throw CudaError(mqo_last_error());
         owned.push_back(copy);
@@ -782,6 +783,7 @@ extern "C" int mqo_init_state_host(const mqo_graph* g, int32_t problem, double s
     if (g->n == 0) throw std::invalid_argument("init_state: empty graph");
     if (g->max_degree < 1)
       throw std::invalid_argument("init_state: edgeless graph (strip isolated vertices upstream)");
+    host_csr(g);
     host_init_state(g->h_off.data(), g->n, g->max_degree, problem, sigma, *st, x);
   });
 }

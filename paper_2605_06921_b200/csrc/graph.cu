@@ -12,6 +12,8 @@
 #include <ctime>
 #include <thread>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace mqo_b200 {
@@ -62,11 +64,190 @@ __global__ void k_check_symmetric(const int64_t* __restrict__ off, const int32_t
     if (a == off[u + 1] || nbr[a] != v) atomicMin(bad, static_cast<unsigned long long>(e));
   }
 }
+
+// Graph::check_invariants (graph.cpp:44-56) + range checks of an uploaded
+// CSR, a warp per row: *bad = the smallest (row << 32 | code) over the
+// violations, code 0 = the row's offsets decrease (or leave [0, nnz]), else
+// 1 + the entry's position in the row -- the order a sequential scan meets
+// them; *maxdeg = the largest degree.
+__global__ void k_check_rows(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                             int32_t n, int64_t nnz, unsigned long long* bad, int32_t* maxdeg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  int32_t dmax = 0;
+  for (int64_t v = w0; v < n; v += nw) {
+    const int64_t b = off[v], e = off[v + 1];
+    if (e < b || b < 0 || e > nnz) {
+      if (lane == 0) atomicMin(bad, static_cast<unsigned long long>(v) << 32);
+      continue;
+    }
+    dmax = max(dmax, static_cast<int32_t>(e - b));
+    for (int64_t c = b; c < e; c += 32) {
+      const int64_t i = c + lane;
+      bool wrong = false;
+      if (i < e) {
+        const int32_t u = nbr[i];
+        wrong = u < 0 || u >= n || u == v || (i > b && nbr[i - 1] >= u);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, wrong);
+      if (m) {
+        if (lane == 0)
+          atomicMin(bad, (static_cast<unsigned long long>(v) << 32) |
+                             static_cast<unsigned long long>(c + __ffs(m) - b));
+        break;
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if (lane == 0 && dmax) atomicMax(maxdeg, dmax);
+}
+
+// sort keys of the degree-descending row order (stable radix sort by
+// max_degree - degree) and the degree histogram
+__global__ void k_order_keys(const int64_t* __restrict__ off, int32_t n, int32_t max_degree,
+                             uint32_t* __restrict__ keys, int32_t* __restrict__ ids,
+                             int32_t* __restrict__ hist) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t d = static_cast<int32_t>(off[v + 1] - off[v]);
+    keys[v] = static_cast<uint32_t>(max_degree - d);
+    ids[v] = static_cast<int32_t>(v);
+    atomicAdd(hist + d, 1);
+  }
+}
 }  // namespace
+
+namespace mqo_b200 {
+void host_csr(const mqo_graph* cg) {
+  auto* g = const_cast<mqo_graph*>(cg);
+  std::lock_guard<std::mutex> lock(g->host_mu);
+  if (g->h_csr) return;
+  int prev = 0;
+  MQO_CUDA(cudaGetDevice(&prev));
+  MQO_CUDA(cudaSetDevice(g->device));
+  g->h_off.resize(static_cast<size_t>(g->n) + 1);
+  g->h_nbr.resize(static_cast<size_t>(2 * g->m));
+  const cudaError_t e1 =
+      cudaMemcpy(g->h_off.data(), g->d_off, sizeof(int64_t) * (g->n + 1), cudaMemcpyDeviceToHost);
+  const cudaError_t e2 = g->m ? cudaMemcpy(g->h_nbr.data(), g->d_nbr, sizeof(int32_t) * 2 * g->m,
+                                           cudaMemcpyDeviceToHost)
+                              : cudaSuccess;
+  cudaSetDevice(prev);
+  MQO_CUDA(e1);
+  MQO_CUDA(e2);
+  g->h_csr = true;
+}
+}  // namespace mqo_b200
 
 extern "C" const char* mqo_last_error(void) { return g_last_error.c_str(); }
 extern "C" int32_t mqo_last_error_line(void) { return g_last_error_line; }
 extern "C" const char* mqo_version(void) { return "mqo_b200 0.1 sm_100a"; }
+
+namespace {
+// A device graph: the CSR goes to HBM as given and every check runs there
+// (k_check_rows, then k_check_symmetric), the degree-descending row order is
+// a stable radix sort on the device, and the host reads back a few words --
+// the caller's neighbour array is never walked on the host (bench.py's e2e
+// leg uploads the C4 graph every step: 32 ms with host checks, copies and a
+// host counting sort).  Errors are the host path's, in the same order: the
+// smallest failing (row, entry) is classified from the caller's row.
+mqo_graph* upload_device(int32_t n, const int64_t* offsets, const int32_t* neighbors, int64_t nnz,
+                         int32_t device) {
+  auto* g = new mqo_graph;
+  g->device = device;
+  g->n = n;
+  g->m = nnz / 2;
+  void* scratch[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t ms = nullptr;
+  unsigned long long* h_w = nullptr;  // pinned read-back words
+  const size_t h_words = 4;
+  auto cleanup = [&] {
+    if (ms) {
+      for (void* p : scratch)
+        if (p) cudaFreeAsync(p, ms);
+    }
+    if (h_w) pinned_put(h_w, sizeof(unsigned long long) * h_words);
+  };
+  try {
+    MQO_CUDA(cudaSetDevice(device));
+    ms = mem_stream(device);
+    void* p = nullptr;
+    MQO_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), ms));
+    g->d_off = static_cast<int64_t*>(p);
+    MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), ms));
+    g->d_nbr = static_cast<int32_t*>(p);
+    MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int32_t>(n, 1) + 16, ms));
+    g->d_order = static_cast<int32_t*>(p);
+    MQO_CUDA(cudaMemcpyAsync(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ms));
+    if (nnz)
+      MQO_CUDA(cudaMemcpyAsync(g->d_nbr, neighbors, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, ms));
+    // flag words: [0] invariant key, [1] symmetry entry, [2] max degree
+    MQO_CUDA(cudaMallocAsync(&scratch[0], sizeof(unsigned long long) * 4, ms));
+    auto* d_w = static_cast<unsigned long long*>(scratch[0]);
+    MQO_CUDA(cudaMemsetAsync(d_w, 0xff, sizeof(unsigned long long) * 2, ms));
+    MQO_CUDA(cudaMemsetAsync(d_w + 2, 0, sizeof(unsigned long long) * 2, ms));
+    const int grid = 148 * 16;
+    if (n) k_check_rows<<<grid, 256, 0, ms>>>(g->d_off, g->d_nbr, n, nnz, d_w, reinterpret_cast<int32_t*>(d_w + 2));
+    MQO_CUDA(cudaGetLastError());
+    h_w = static_cast<unsigned long long*>(pinned_get(sizeof(unsigned long long) * h_words));
+    MQO_CUDA(cudaMemcpyAsync(h_w, d_w, sizeof(unsigned long long) * 3, cudaMemcpyDeviceToHost, ms));
+    MQO_CUDA(cudaStreamSynchronize(ms));
+    if (h_w[0] != ~0ull) {  // the first violation in (row, entry) order
+      const int64_t v = static_cast<int64_t>(h_w[0] >> 32);
+      const int64_t code = static_cast<int64_t>(h_w[0] & 0xffffffffull);
+      if (code == 0) throw std::logic_error("graph: offsets not monotone");
+      const int64_t i = offsets[v] + code - 1;
+      const int32_t u = neighbors[i];
+      if (u < 0 || u >= n) throw std::invalid_argument("graph: vertex index out of range");
+      if (u == v) throw std::logic_error("graph: self-loop");
+      throw std::logic_error("graph: neighbor list not strictly ascending");
+    }
+    g->max_degree = static_cast<int32_t>(h_w[2] & 0xffffffffull);
+    const int32_t D = g->max_degree;
+    MQO_TRACE("graph upload: on the device, invariants checked");
+    // symmetry, one thread per entry
+    if (nnz)
+      k_check_symmetric<<<static_cast<int>(std::min<int64_t>((nnz + 255) / 256, 148 * 64)), 256, 0, ms>>>(
+          g->d_off, g->d_nbr, n, nnz, d_w + 1);
+    // row order: stable radix sort of (D - degree, id), and the degree histogram
+    MQO_CUDA(cudaMallocAsync(&scratch[1], sizeof(uint32_t) * 2 * std::max<int32_t>(n, 1), ms));
+    MQO_CUDA(cudaMallocAsync(&scratch[2], sizeof(int32_t) * (std::max<int32_t>(n, 1) + D + 2), ms));
+    auto* keys = static_cast<uint32_t*>(scratch[1]);
+    auto* ids = static_cast<int32_t*>(scratch[2]);
+    int32_t* hist = ids + std::max<int32_t>(n, 1);
+    MQO_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (D + 2), ms));
+    if (n) {
+      k_order_keys<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, ms>>>(
+          g->d_off, n, D, keys, ids, hist);
+      int bits = 1;
+      while (bits < 32 && (uint32_t(1) << bits) <= static_cast<uint32_t>(D)) ++bits;
+      size_t tmp = 0;
+      MQO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys + n, ids, g->d_order, n, 0,
+                                               bits, ms));
+      MQO_CUDA(cudaMallocAsync(&scratch[3], std::max<size_t>(tmp, 16), ms));
+      MQO_CUDA(cub::DeviceRadixSort::SortPairs(scratch[3], tmp, keys, keys + n, ids, g->d_order, n,
+                                               0, bits, ms));
+    }
+    MQO_CUDA(cudaGetLastError());
+    g->h_deg_ge.assign(static_cast<size_t>(D) + 2, 0);
+    MQO_CUDA(cudaMemcpyAsync(h_w, d_w + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ms));
+    MQO_CUDA(cudaMemcpyAsync(g->h_deg_ge.data(), hist, sizeof(int32_t) * (D + 1),
+                             cudaMemcpyDeviceToHost, ms));
+    MQO_CUDA(cudaStreamSynchronize(ms));
+    if (h_w[0] != ~0ull) throw std::logic_error("graph: adjacency not symmetric");
+    for (int64_t d = D; d >= 0; --d) g->h_deg_ge[d] += g->h_deg_ge[d + 1];
+    MQO_TRACE("graph upload: on the device, symmetry checked, rows ordered");
+  } catch (...) {
+    if (ms) cudaStreamSynchronize(ms);
+    cleanup();
+    mqo_graph_free(g);
+    throw;
+  }
+  cleanup();
+  return g;
+}
+}  // namespace
 
 extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t* neighbors,
                                 int32_t device, mqo_graph** out) {
@@ -78,11 +259,16 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
     const int64_t nnz = offsets[n];
     if (nnz < 0 || (nnz & 1)) throw std::logic_error("graph: degree sum != 2m");
     if (nnz > 0 && !neighbors) throw std::invalid_argument("mqo_graph_upload: null neighbors");
-    // Graph::check_invariants (graph.cpp:44-56) + range checks, then
-    // symmetry (u in N(v) <=> v in N(u)), which from_edges guarantees and the
-    // local-search kernels rely on.  Rows are checked in parallel chunks on
-    // host threads; the first violation in (row, entry) order is reported,
-    // invariant violations before symmetry ones, as a sequential scan would.
+    if (device >= 0) {
+      *out = upload_device(n, offsets, neighbors, nnz, device);
+      return;
+    }
+    // Host-only graph: Graph::check_invariants (graph.cpp:44-56) + range
+    // checks, then symmetry (u in N(v) <=> v in N(u)), which from_edges
+    // guarantees and the local-search kernels rely on.  Rows are checked in
+    // parallel chunks on host threads; the first violation in (row, entry)
+    // order is reported, invariant violations before symmetry ones, as a
+    // sequential scan would.
     struct Bad {
       int64_t at = INT64_MAX;  // global entry index (or row for "not monotone")
       int kind = 0;            // 1 not monotone, 2 range, 3 self-loop, 4 not ascending
@@ -130,7 +316,7 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
     }
     const int32_t max_degree = *std::max_element(dmax.begin(), dmax.end());
     MQO_TRACE("graph upload: invariants checked (%d threads)", T);
-    if (device < 0) {  // host-only graph: symmetry on the host threads
+    {  // symmetry on the host threads
       run([&](int t) {
         for (int32_t v = cut[t]; v < cut[t + 1]; ++v)
           for (int64_t i = offsets[v]; i < offsets[v + 1]; ++i) {
@@ -144,7 +330,7 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
       for (const Bad& x : sym)
         if (x.kind) throw std::logic_error("graph: adjacency not symmetric");
       MQO_TRACE("graph upload: symmetry checked");
-    }  // device graphs: k_check_symmetric after the upload below
+    }
     auto* g = new mqo_graph;
     g->device = device;
     g->n = n;
@@ -153,67 +339,11 @@ extern "C" int mqo_graph_upload(int32_t n, const int64_t* offsets, const int32_t
     g->h_off.assign(offsets, offsets + n + 1);
     g->h_nbr.assign(neighbors, neighbors + nnz);
 
-    // Degree-descending row order (counting sort, stable in id).
-    std::vector<int32_t> order(static_cast<size_t>(n));
-    {
-      std::vector<int64_t> count(static_cast<size_t>(max_degree) + 2, 0);
-      for (int32_t v = 0; v < n; ++v) ++count[max_degree - (offsets[v + 1] - offsets[v])];
-      int64_t acc = 0;
-      for (auto& c : count) {
-        const int64_t t = c;
-        c = acc;
-        acc += t;
-      }
-      for (int32_t v = 0; v < n; ++v)
-        order[count[max_degree - (offsets[v + 1] - offsets[v])]++] = v;
-    }
-    MQO_TRACE("graph upload: host copies + row order");
+    MQO_TRACE("graph upload: host copies");
     g->h_deg_ge.assign(static_cast<size_t>(max_degree) + 2, 0);
     for (int32_t v = 0; v < n; ++v) ++g->h_deg_ge[static_cast<size_t>(offsets[v + 1] - offsets[v])];
     for (int64_t d = max_degree; d >= 0; --d) g->h_deg_ge[d] += g->h_deg_ge[d + 1];
-    if (device < 0) {  // host-only graph: CSR kept for host-side users, no HBM copy
-      *out = g;
-      return;
-    }
-    try {
-      MQO_CUDA(cudaSetDevice(device));
-      // stream-ordered pool allocations on the device's memory stream
-      // (mem.cu): no page mapping per upload, no device-wide sync per free
-      const cudaStream_t ms = mem_stream(device);
-      void* p = nullptr;
-      MQO_CUDA(cudaMallocAsync(&p, sizeof(int64_t) * (n + 1), ms));
-      g->d_off = static_cast<int64_t*>(p);
-      MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int64_t>(nnz, 1), ms));
-      g->d_nbr = static_cast<int32_t*>(p);
-      MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max<int32_t>(n, 1) + 16, ms));
-      g->d_order = static_cast<int32_t*>(p);
-      MQO_CUDA(cudaMemcpyAsync(g->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, ms));
-      if (nnz)
-        MQO_CUDA(cudaMemcpyAsync(g->d_nbr, neighbors, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, ms));
-      if (n)
-        MQO_CUDA(cudaMemcpyAsync(g->d_order, order.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ms));
-      // symmetry, one thread per entry on the device; the flag word rides
-      // behind the order array
-      unsigned long long* d_bad = reinterpret_cast<unsigned long long*>(
-          reinterpret_cast<char*>(g->d_order) + (sizeof(int32_t) * std::max<int32_t>(n, 1) + 7) / 8 * 8);
-      MQO_CUDA(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), ms));
-      if (nnz)
-        k_check_symmetric<<<static_cast<int>(std::min<int64_t>((nnz + 255) / 256, 148 * 64)), 256, 0, ms>>>(
-            g->d_off, g->d_nbr, n, nnz, d_bad);
-      MQO_CUDA(cudaGetLastError());
-      unsigned long long* h_bad = static_cast<unsigned long long*>(pinned_get(sizeof(unsigned long long)));
-      const cudaError_t e1 = cudaMemcpyAsync(h_bad, d_bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ms);
-      const cudaError_t e2 = cudaStreamSynchronize(ms);
-      const unsigned long long bad = *h_bad;
-      pinned_put(h_bad, sizeof(unsigned long long));
-      MQO_CUDA(e1);
-      MQO_CUDA(e2);
-      if (bad != ~0ull) throw std::logic_error("graph: adjacency not symmetric");
-      MQO_TRACE("graph upload: on the device, symmetry checked");
-    } catch (...) {
-      mqo_graph_free(g);
-      throw;
-    }
+    g->h_csr = true;  // host-only graph: CSR kept for host-side users, no HBM copy
     *out = g;
   });
 }
@@ -230,6 +360,16 @@ extern "C" int mqo_graph_free(mqo_graph* g) {
         if (p) cudaFreeAsync(p, ms);
     }
     delete g;
+  });
+}
+
+extern "C" int mqo_graph_row_order(const mqo_graph* g, int32_t* order) {
+  return guard([&] {
+    if (!g || !order) throw std::invalid_argument("mqo_graph_row_order: null argument");
+    if (g->device < 0) throw std::invalid_argument("mqo_graph_row_order: host-only graph");
+    MQO_CUDA(cudaSetDevice(g->device));
+    if (g->n)
+      MQO_CUDA(cudaMemcpy(order, g->d_order, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -263,6 +263,7 @@ extern "C" int mqo_generate(const mqo_gen_spec* spec, int32_t device, mqo_graph*
 extern "C" int mqo_graph_csr(const mqo_graph* g, int64_t* offsets, int32_t* neighbors) {
   return guard([&] {
     if (!g) throw std::invalid_argument("mqo_graph_csr: null graph");
+    host_csr(g);
     if (offsets) std::memcpy(offsets, g->h_off.data(), sizeof(int64_t) * g->h_off.size());
     if (neighbors) std::memcpy(neighbors, g->h_nbr.data(), sizeof(int32_t) * g->h_nbr.size());
   });
@@ -275,6 +276,7 @@ extern "C" int mqo_graph_csr(const mqo_graph* g, int64_t* offsets, int32_t* neig
 extern "C" int mqo_graph_save(const mqo_graph* g, const char* path, int32_t format) {
   return guard([&] {
     if (!g || !path) throw std::invalid_argument("mqo_graph_save: null argument");
+    host_csr(g);
     FILE* f = std::fopen(path, format == 0 ? "wb" : "w");
     if (!f) throw std::runtime_error(std::string("cannot open output file: ") + path);
     bool ok = true;

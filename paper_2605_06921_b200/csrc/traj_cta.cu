@@ -427,6 +427,7 @@ void ensure_cta_layout(mqo_graph* g) {
   const int32_t n = g->n;
   const int32_t S = (n + 31) / 32;
   const int32_t Z = 32 * S;
+  host_csr(g);
   std::vector<int32_t> order(static_cast<size_t>(n)), slot(static_cast<size_t>(n));
   MQO_CUDA(cudaMemcpy(order.data(), g->d_order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
   for (int32_t i = 0; i < n; ++i) slot[order[i]] = i;
