@@ -57,6 +57,14 @@ const bool g_scan_multi = [] {
   return !(e && *e == '0');
 }();
 
+// lanes per candidate in the multi-commit sweep's simulation (MQO_SCAN_G =
+// 8 | 16 | 32; with 32, MQO_SCAN_C picks the window).  8: BA(1e6)
+// one_two_flip x 8 0.136 -> 0.131 s (scripts/ls_bench.py); the step is bound
+// by its barriers after the commit phase, not by the row simulation.
+const int g_scan_g = [] {
+  const char* e = std::getenv("MQO_SCAN_G");
+  return e && *e ? std::atoi(e) : 8;
+}();
 const int g_scan_c = [] {
   const char* e = std::getenv("MQO_SCAN_C");
   return e ? std::atoi(e) : 8;
@@ -841,13 +849,14 @@ __device__ __forceinline__ bool row_has(const int32_t* __restrict__ nbr, int64_t
 // kMultiScanRow -- hubs, whose 2-hop walk would stall the whole step --
 // answer v + 1.
 constexpr int64_t kMultiScanRow = 256;
+template <int G = 32>
 __device__ __forceinline__ int32_t affected_min(const int64_t* __restrict__ off,
                                                 const int32_t* __restrict__ nbr, int32_t t,
                                                 int32_t v, int lane) {
   int32_t m = INT_MAX;
   const int64_t e0 = off[t], e1 = off[t + 1];
   if (e1 - e0 > kMultiScanRow) return v + 1;
-  for (int64_t a = e0 - 1 + lane; a < e1; a += 32) {
+  for (int64_t a = e0 - 1 + lane; a < e1; a += G) {
     const int32_t y = a < e0 ? t : nbr[a];
     if (y <= v) continue;
     m = min(m, y);
@@ -868,17 +877,29 @@ __device__ void warp_mark_after_flip2(const int64_t* off, const int32_t* nbr, ui
     const int32_t y = a < e0 ? t : nbr[a];
     if (y > v) cand[y] = 1;
     next[y] = 1;
-    for (int64_t c = off[y]; c < off[y + 1]; ++c) {
-      const int32_t w = nbr[c];
-      if (w >= y) break;  // rows ascending: only w < y
-      if (w > v) cand[w] = 1;
-      next[w] = 1;
+    // y's lower neighbours (a row prefix: rows ascend), four loads in
+    // flight instead of one load per step of a break-terminated chain
+    for (int64_t c = off[y], c1 = off[y + 1]; c < c1; c += 4) {
+      int32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = c + q < c1 ? nbr[c + q] : INT_MAX;
+      bool stop = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (w[q] < y) {
+          if (w[q] > v) cand[w[q]] = 1;
+          next[w[q]] = 1;
+        } else {
+          stop = true;
+        }
+      }
+      if (stop) break;
     }
   }
   __syncwarp();
 }
 
-template <int NW, int C>
+template <int NW, int C, int G>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_two_scan_multi(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
                      const int32_t* __restrict__ hmax, int32_t n, int32_t count,
@@ -904,9 +925,10 @@ __global__ void __launch_bounds__(32 * NW, 1)
   __shared__ int32_t w_cnt[NW], w_tot;
   __shared__ int32_t s_steps, s_commits;
   __shared__ long long s_cyc[4];  // MQO_TRACE: cycles in phases A-D
-  // per-warp simulation scratch: partner rows [pb, pe) and sides after flip
-  __shared__ int64_t w_pb[NW][kMultiMaxFlips], w_pe[NW][kMultiMaxFlips];
-  __shared__ uint8_t w_pside[NW][kMultiMaxFlips];
+  // per-group simulation scratch: partner rows [pb, pe) and sides after flip
+  constexpr int GPW = 32 / G;  // candidate groups per warp
+  __shared__ int64_t w_pb[NW * GPW][kMultiMaxFlips], w_pe[NW * GPW][kMultiMaxFlips];
+  __shared__ uint8_t w_pside[NW * GPW][kMultiMaxFlips];
   if (threadIdx.x == 0) {
     s_pos = 0;
     s_epos = -1;
@@ -989,82 +1011,99 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const int Kc = s_k;
     if (Kc == 0) break;
     long long t_b = clock64();
-    // B. simulate each candidate's row against the current state (read only)
-    for (int k = warp; k < Kc; k += NW) {
-      const int32_t v = c_v[k];
-      const int64_t e1 = off[v + 1];
-      const bool resumed = c_e[k] >= 0;
-      int64_t e = resumed ? c_e[k] : off[v];
-      int32_t dv = delta[v];
-      uint8_t sv = side[v];
-      int nf = 0, flips_v = 0;
-      int32_t gain = 0;
-      int32_t* part = r_part[k];  // partners (SMEM: indexed at run time)
-      int64_t resume = -1;
-      if (!resumed && dv + hmax[v] + 2 <= 0) e = e1;  // delta_u <= hmax[v]: no hit in the row
-      while (e < e1) {
-        const int64_t my = e + lane;
-        bool ok = false;
-        int32_t u = -1, du = 0;
-        if (my < e1) {
-          u = nbr[my];
-          if (u > v) {
-            const uint8_t su = side[u];
-            if (su != sv) {
-              du = delta[u];
-              // v flipped an odd number of times: the net +-2 of its flips
-              if (flips_v & 1) du += su == sv ? 2 : -2;
-              for (int f = 0; f < nf; ++f)
-                if (row_has(nbr, w_pb[warp][f], w_pe[warp][f], u))
-                  du += su == w_pside[warp][f] ? 2 : -2;
-              ok = dv + du + 2 > 0;
+    // B. simulate each candidate's row against the current state (read
+    // only): a candidate per G-lane group, 32/G groups of a warp side by side
+    // (rows are mostly short, and each candidate is a chain of dependent L2
+    // trips: candidates in parallel, not lanes idling on one row)
+    {
+      const int grp = lane / G, gl = lane % G;
+      const int gid = warp * GPW + grp;
+      const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (grp * G);
+      for (int kb = warp * GPW; kb < Kc; kb += NW * GPW) {  // warp-uniform
+        const int k = kb + grp;
+        const bool valid = k < Kc;
+        int32_t v = 0, dv = 0, gain = 0;
+        int64_t e = 0, e1 = 0, resume = -1;
+        uint8_t sv = 0;
+        int nf = 0, flips_v = 0;
+        bool done = !valid;
+        int32_t* part = r_part[valid ? k : 0];  // partners (SMEM: indexed at run time)
+        if (valid) {
+          v = c_v[k];
+          e1 = off[v + 1];
+          const bool resumed = c_e[k] >= 0;
+          e = resumed ? c_e[k] : off[v];
+          dv = delta[v];
+          sv = side[v];
+          if (!resumed && dv + hmax[v] + 2 <= 0) e = e1;  // delta_u <= hmax[v]: no hit in the row
+        }
+        for (;;) {
+          const bool act = !done && e < e1;
+          if (!__any_sync(0xffffffffu, act)) break;
+          const int64_t my = e + gl;
+          bool ok = false;
+          int32_t u = -1, du = 0;
+          if (act && my < e1) {
+            u = nbr[my];
+            if (u > v) {
+              const uint8_t su = side[u];
+              if (su != sv) {
+                du = delta[u];
+                // v flipped an odd number of times: the net +-2 of its flips
+                if (flips_v & 1) du += su == sv ? 2 : -2;
+                for (int f = 0; f < nf; ++f)
+                  if (row_has(nbr, w_pb[gid][f], w_pe[gid][f], u))
+                    du += su == w_pside[gid][f] ? 2 : -2;
+                ok = dv + du + 2 > 0;
+              }
             }
           }
+          const unsigned hit = __ballot_sync(0xffffffffu, ok) & gmask;
+          const int j = hit ? __ffs(hit) - 1 : grp * G;  // lane of the group's first hit
+          const int32_t uh = __shfl_sync(0xffffffffu, u, j);
+          const int32_t dh = __shfl_sync(0xffffffffu, du, j);
+          if (act) {
+            if (!hit) {
+              e += G;
+            } else if (nf == kMultiMaxFlips) {  // partner list full: finish the row next step
+              resume = e + (j - grp * G);
+              done = true;
+            } else {
+              gain += dv + dh + 2;
+              // apply_flip(v), then apply_flip(uh) as seen from v (localsearch.cpp:28-33)
+              sv ^= 1;
+              dv = -dv;
+              ++flips_v;
+              const uint8_t su_new = side[uh] ^ 1;
+              dv += sv == su_new ? 2 : -2;
+              if (gl == 0) {
+                part[nf] = uh;
+                w_pside[gid][nf] = su_new;
+                w_pb[gid][nf] = off[uh];
+                w_pe[gid][nf] = off[uh + 1];
+              }
+              ++nf;
+              e = e + (j - grp * G) + 1;
+            }
+          }
+          __syncwarp();
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, ok);
-        if (!hit) {
-          e += 32;
-          continue;
+        // m(v): smallest position above v whose decision the flips can change
+        int32_t m = INT_MAX;
+        if (valid && nf > 0) {
+          m = affected_min<G>(off, nbr, v, v, gl);
+          for (int f = 0; f < nf; ++f) m = min(m, affected_min<G>(off, nbr, part[f], v, gl));
         }
-        const int j = warp_first(hit);
-        const int32_t uh = __shfl_sync(0xffffffffu, u, j);
-        const int32_t dh = __shfl_sync(0xffffffffu, du, j);
-        if (nf == kMultiMaxFlips) {  // partner list full: finish the row next step
-          resume = e + j;
-          break;
-        }
-        gain += dv + dh + 2;
-        // apply_flip(v), then apply_flip(uh) as seen from v (localsearch.cpp:28-33)
-        sv ^= 1;
-        dv = -dv;
-        ++flips_v;
-        const uint8_t su_new = side[uh] ^ 1;
-        dv += sv == su_new ? 2 : -2;
-        if (lane == 0) {
-          part[nf] = uh;
-          w_pside[warp][nf] = su_new;
-          w_pb[warp][nf] = off[uh];
-          w_pe[warp][nf] = off[uh + 1];
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (valid && gl == 0) {
+          r_m[k] = m;
+          r_gain[k] = gain;
+          r_nf[k] = nf;
+          r_resume[k] = resume;
         }
         __syncwarp();
-        ++nf;
-        e = e + j + 1;
       }
-      // m(v): smallest position above v whose decision the flips can change
-      int32_t m = INT_MAX;
-      if (nf > 0) {
-        m = affected_min(off, nbr, v, v, lane);
-        for (int f = 0; f < nf; ++f) m = min(m, affected_min(off, nbr, part[f], v, lane));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-      }
-      if (lane == 0) {
-        r_m[k] = m;
-        r_gain[k] = gain;
-        r_nf[k] = nf;
-        r_resume[k] = resume;
-      }
-      __syncwarp();
     }
     __syncthreads();
     long long t_c = clock64();
@@ -1667,7 +1706,6 @@ __global__ void __launch_bounds__(32 * W)
                    const int32_t* __restrict__ bad) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int32_t s_best, s_bu, s_bw, s_keep, s_nadd;
-  const int lane = threadIdx.x & 31;
   const int s = blockIdx.x;
   if (s >= count) return;
   if (bad && bad[s]) return;  // not a maximal independent set: the host throws
@@ -1922,8 +1960,11 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       if (g_scan_multi) {
         MQO_CUDA(cudaMemsetAsync(d_next, 0, cells, st));
         // candidates per step = 32 warps x C (MQO_SCAN_C = 4 | 8 | 16)
-        auto kern = g_scan_c == 4 ? k_two_scan_multi<32, 4>
-                    : g_scan_c == 16 ? k_two_scan_multi<32, 16> : k_two_scan_multi<32, 8>;
+        auto kern = g_scan_g == 8    ? k_two_scan_multi<32, 8, 8>
+                    : g_scan_g == 16 ? k_two_scan_multi<32, 8, 16>
+                    : g_scan_c == 4  ? k_two_scan_multi<32, 4, 32>
+                    : g_scan_c == 16 ? k_two_scan_multi<32, 16, 32>
+                                     : k_two_scan_multi<32, 8, 32>;
         kern<<<count, 32 * 32, 0, st>>>(g->d_off, g->d_nbr, g->d_hmax, n, count, side, delta,
                                         d_cand, d_next, d_live2, d_g2, d_stats);
       }
