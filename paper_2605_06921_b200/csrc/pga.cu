@@ -789,9 +789,14 @@ int g_k1_variant = [] {
   const char* e = std::getenv("MQO_K1_VARIANT");
   return e ? std::atoi(e) : 0;
 }();
+// Fraction of the L2 given to evict_last gathers (hot_rows).  C4 (BA(1e6,5))
+// per step / trajectory pass at 16 | 64 | 128 chains, MQO_HOT_FRAC sweep r32:
+// 0.5 (round 1): 0.244 / 0.259 | 0.957 / 0.99 | 1.921 / 1.966 ms;
+// 0.2: 0.239 / 0.253 | 0.938 / 0.966 | 1.893 / 1.939 ms (0.05 .. 0.9 measured;
+// ER configs C3 / C5 flat).
 double g_hot_frac = [] {
   const char* e = std::getenv("MQO_HOT_FRAC");
-  return e ? std::atof(e) : 0.5;
+  return e ? std::atof(e) : 0.2;
 }();
 // CTAs per SM of the per-pass grids; 0 = automatic: 8 for a sweep over all
 // chains, 4 per group for chain-tiled sweeps (profiles/r08_tune_grid.txt:
@@ -987,7 +992,7 @@ void validate_optimizer(const mqo_optimizer& c) {  // pga.cpp:9-18
 
 // Rows whose gathers are marked L2::evict_last: a prefix of the vertex
 // order (hubs come first in preferential-attachment labelings) sized to
-// MQO_HOT_FRAC (default 0.3) of the L2.
+// MQO_HOT_FRAC (default 0.2) of the L2.
 int32_t hot_rows(const mqo_batch* b, int Qg) {
   const double frac = g_hot_frac;
   static int l2[64] = {0};
