@@ -57,6 +57,13 @@ const bool g_scan_multi = [] {
   return !(e && *e == '0');
 }();
 
+// MQO_FLIP_CLOSURE=0: the grid 1-flip passes round over every vertex and
+// rebuild the gain table (A/B runs)
+const bool g_flip_closure = [] {
+  const char* e = std::getenv("MQO_FLIP_CLOSURE");
+  return !(e && *e == '0');
+}();
+
 // lanes per candidate in the multi-commit sweep's simulation (MQO_SCAN_G =
 // 8 | 16 | 32; with 32, MQO_SCAN_C picks the window).  8: BA(1e6)
 // one_two_flip x 8 0.136 -> 0.131 s (scripts/ls_bench.py); the step is bound
@@ -153,7 +160,8 @@ __device__ __forceinline__ void warp_flip(const int64_t* __restrict__ off, const
 // earlier in the same round is safe; state bytes are 0 undecided, 1 keep,
 // 2 flip (one byte: a reader never sees a half-written decision).
 __global__ void k_flip_round(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                             int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                             const int32_t* __restrict__ lo_cnt, int32_t n, int32_t count,
+                             const uint8_t* __restrict__ side_all,
                              const int32_t* __restrict__ d0_all, uint8_t* st_all,
                              const int32_t* __restrict__ live, int32_t* undecided) {
   const int64_t total = static_cast<int64_t>(count) * n;
@@ -166,9 +174,13 @@ __global__ void k_flip_round(const int64_t* __restrict__ off, const int32_t* __r
     const uint8_t* side = side_all + s * n;
     const uint8_t sv = side[v];
     int32_t base = d0_all[q], lo = 0, hi = 0;
-    for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
-      const int32_t u = nbr[e];
-      if (u >= v) break;  // rows ascend: the lower neighbours are a prefix
+    // rows ascend: the lower neighbours are a prefix, of known length, so
+    // the walk is a counted loop with four loads in flight
+    const int64_t e0 = off[v];
+    const int32_t L = lo_cnt[v];
+#pragma unroll 4
+    for (int32_t k = 0; k < L; ++k) {
+      const int32_t u = nbr[e0 + k];
       const int32_t c = side[u] == sv ? -2 : 2;
       const uint8_t su = st[u];
       if (su == 2)
@@ -188,7 +200,8 @@ __global__ void k_flip_round(const int64_t* __restrict__ off, const int32_t* __r
 // Gain of the pass: sum over flipped v of delta_v at its turn
 // (d0_v + sum of c_u(v) over flipped lower neighbours), per body.
 __global__ void k_flip_commit(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
-                              int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                              const int32_t* __restrict__ lo_cnt, int32_t n, int32_t count,
+                              const uint8_t* __restrict__ side_all,
                               const int32_t* __restrict__ d0_all, const uint8_t* __restrict__ st_all,
                               const int32_t* __restrict__ live, unsigned long long* gain) {
   const int64_t total = static_cast<int64_t>(count) * n;
@@ -205,9 +218,11 @@ __global__ void k_flip_commit(const int64_t* __restrict__ off, const int32_t* __
         const uint8_t* side = side_all + s * n;
         const uint8_t sv = side[v];
         int32_t at = d0_all[q];
-        for (int64_t e = off[v], e1 = off[v + 1]; e < e1; ++e) {
-          const int32_t u = nbr[e];
-          if (u >= v) break;
+        const int64_t e0 = off[v];
+        const int32_t L = lo_cnt[v];
+#pragma unroll 4
+        for (int32_t k = 0; k < L; ++k) {
+          const int32_t u = nbr[e0 + k];
           if (st[u] == 2) at += side[u] == sv ? -2 : 2;
         }
         g = at;
@@ -232,6 +247,104 @@ __global__ void k_flip_apply(int32_t n, int32_t count, uint8_t* side_all,
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
        q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     if (st_all[q] == 2 && live[q / n]) side_all[q] ^= 1;
+  }
+}
+
+// ---- 1-flip passes over the vertices that can flip (grid version) --------
+// The closure P of cta_one_flip_closure for many large bodies: seeds are the
+// positive pass-start gains, each member raises its favourable upper
+// neighbours' counters, a counter crossing zero admits its vertex once; the
+// rest are "keep" (st = 1) before the rounds, so a round's work is P's.  The
+// gain table is then updated from the pass's flips (k_flip_update) instead of
+// rebuilt.  Per body: len / fa / fb (list length, frontier [fa, fb)).
+__global__ void k_flip_seed(int32_t n, int32_t count, const int32_t* __restrict__ delta_all,
+                            uint8_t* st_all, int32_t* cnt_all, int32_t* list_all, int32_t* len,
+                            const int32_t* __restrict__ live) {
+  const int64_t total = static_cast<int64_t>(count) * n;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < total;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = q / n;
+    if (!live[s]) continue;
+    const int32_t d = delta_all[q];
+    cnt_all[q] = d;
+    if (d > 0) {
+      st_all[q] = 0;
+      list_all[s * n + atomicAdd(len + s, 1)] = static_cast<int32_t>(q - s * n);
+    } else {
+      st_all[q] = 1;
+    }
+  }
+}
+
+// next frontier: [fa, fb) = [fb, len)
+__global__ void k_flip_front(int32_t count, const int32_t* __restrict__ len, int32_t* fa,
+                             int32_t* fb) {
+  for (int s = threadIdx.x; s < count; s += blockDim.x) {
+    fa[s] = fb[s];
+    fb[s] = len[s];
+  }
+}
+
+// one closure step, a warp per frontier vertex (hub rows are long)
+__global__ void k_flip_close(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                             const int32_t* __restrict__ lo_cnt, int32_t n, int32_t count,
+                             const uint8_t* __restrict__ side_all, uint8_t* st_all,
+                             int32_t* cnt_all, int32_t* list_all, int32_t* len,
+                             const int32_t* __restrict__ fa, const int32_t* __restrict__ fb,
+                             const int32_t* __restrict__ live) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int32_t s = 0; s < count; ++s) {
+    if (!live[s]) continue;
+    const int64_t base = int64_t(s) * n;
+    const uint8_t* side = side_all + base;
+    for (int64_t i = fa[s] + w0; i < fb[s]; i += nw) {
+      const int32_t u = list_all[base + i];
+      const uint8_t su = side[u];
+      for (int64_t e = off[u] + lo_cnt[u] + lane, e1 = off[u + 1]; e < e1; e += 32) {
+        const int32_t v = nbr[e];
+        if (side[v] == su) continue;
+        const int32_t old = atomicAdd(cnt_all + base + v, 2);
+        if (old <= 0 && old > -2) {  // crossed zero: v joins P
+          st_all[base + v] = 0;
+          list_all[base + atomicAdd(len + s, 1)] = v;
+        }
+      }
+    }
+  }
+}
+
+// the gain table after the pass's flips (sides already applied), a warp per
+// listed vertex: a flipped row recomputed, its unflipped neighbours +-2
+// (apply_flip, localsearch.cpp:28-33)
+__global__ void k_flip_update(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                              int32_t n, int32_t count, const uint8_t* __restrict__ side_all,
+                              const uint8_t* __restrict__ st_all, int32_t* delta_all,
+                              const int32_t* __restrict__ list_all, const int32_t* __restrict__ len,
+                              const int32_t* __restrict__ live) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int32_t s = 0; s < count; ++s) {
+    if (!live[s]) continue;
+    const int64_t base = int64_t(s) * n;
+    const uint8_t* side = side_all + base;
+    const uint8_t* st = st_all + base;
+    for (int64_t i = w0; i < len[s]; i += nw) {
+      const int32_t v = list_all[base + i];
+      if (st[v] != 2) continue;  // warp-uniform
+      const uint8_t sv = side[v];
+      int32_t same = 0;
+      for (int64_t e = off[v] + lane, e1 = off[v + 1]; e < e1; e += 32) {
+        const int32_t u = nbr[e];
+        const bool eq = side[u] == sv;
+        same += eq ? 1 : -1;
+        if (st[u] != 2) atomicAdd(delta_all + base + u, eq ? 2 : -2);
+      }
+      for (int o = 16; o; o >>= 1) same += __shfl_xor_sync(0xffffffffu, same, o);
+      if (lane == 0) delta_all[base + v] = same;
+    }
   }
 }
 
@@ -1913,6 +2026,8 @@ struct LsWork {
 // host-driven sweeps of (grid candidate test, warp candidate scan) until a
 // sweep flips nothing; one_two_flip alternates per body until a round gains
 // nothing.  gains[s] = total gain.
+void ensure_lo(mqo_graph* g, cudaStream_t st);
+
 void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* side, int32_t* delta,
                            int64_t* d_out, cudaStream_t st) {
   const int32_t n = g->n;
@@ -1921,6 +2036,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   int32_t *d_live = nullptr, *d_live2 = nullptr, *d_und = nullptr;
   int64_t *d_g1 = nullptr, *d_g2 = nullptr;
   uint8_t* d_cand = nullptr;
+  int32_t *d_cnt = nullptr, *d_list = nullptr, *d_len3 = nullptr;  // 1-flip closure (lazy)
   MQO_CUDA(cudaMallocAsync(&d_live, sizeof(int32_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_live2, sizeof(int32_t) * count, st));
   MQO_CUDA(cudaMallocAsync(&d_und, sizeof(int32_t) * count, st));
@@ -2023,7 +2139,16 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       MQO_TRACE("one_flip (CTA path)");
       return;
     }
-    std::vector<int32_t> plive = who, und(count);
+    ensure_lo(g, st);
+    if (!d_cnt) {  // closure state: counters, lists, [len | fa | fb] per body
+      MQO_CUDA(cudaMallocAsync(&d_cnt, sizeof(int32_t) * cells, st));
+      MQO_CUDA(cudaMallocAsync(&d_list, sizeof(int32_t) * cells, st));
+      MQO_CUDA(cudaMallocAsync(&d_len3, sizeof(int32_t) * 3 * count, st));
+    }
+    int32_t* d_len = d_len3;
+    int32_t* d_fa = d_len3 + count;
+    int32_t* d_fb = d_len3 + 2 * count;
+    std::vector<int32_t> plive = who, und(count), lens(3 * count);
     std::vector<int64_t> pg(count);
     std::fill(g1.begin(), g1.end(), 0);
     for (int pass = 0;; ++pass) {
@@ -2032,13 +2157,41 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       if (!any) break;
       MQO_CUDA(cudaMemcpyAsync(d_live, plive.data(), sizeof(int32_t) * count,
                                cudaMemcpyHostToDevice, st));
-      MQO_CUDA(cudaMemsetAsync(d_cand, 0, cells, st));  // decision bytes
       MQO_CUDA(cudaMemsetAsync(d_g1, 0, sizeof(int64_t) * count, st));
+      // the seeds of P; a pass with many (a quarter of a body: the first
+      // pass from a harvested state) runs the rounds over every vertex
+      MQO_CUDA(cudaMemsetAsync(d_len3, 0, sizeof(int32_t) * 3 * count, st));
+      k_flip_seed<<<ls_grid(cells), 256, 0, st>>>(n, count, delta, d_cand, d_cnt, d_list, d_len,
+                                                  d_live);
+      MQO_CUDA(cudaGetLastError());
+      MQO_CUDA(cudaMemcpyAsync(lens.data(), d_len, sizeof(int32_t) * count, cudaMemcpyDeviceToHost, st));
+      MQO_CUDA(cudaStreamSynchronize(st));
+      bool listed = g_flip_closure;
+      for (int i = 0; i < count; ++i) listed &= !plive[i] || int64_t(lens[i]) * 4 <= n;
+      if (listed) {  // the closure, four frontier steps per check
+        for (int step = 0;; step += 4) {
+          for (int r = 0; r < 4; ++r) {
+            k_flip_front<<<1, 32, 0, st>>>(count, d_len, d_fa, d_fb);
+            k_flip_close<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_lo, n, count,
+                                                        side, d_cand, d_cnt, d_list, d_len, d_fa,
+                                                        d_fb, d_live);
+          }
+          MQO_CUDA(cudaGetLastError());
+          MQO_CUDA(cudaMemcpyAsync(lens.data(), d_len3, sizeof(int32_t) * 3 * count,
+                                   cudaMemcpyDeviceToHost, st));
+          MQO_CUDA(cudaStreamSynchronize(st));
+          bool more = false;
+          for (int i = 0; i < count; ++i) more |= lens[i] != lens[2 * count + i];  // len != fb
+          if (!more) break;
+        }
+      } else {
+        MQO_CUDA(cudaMemsetAsync(d_cand, 0, cells, st));  // every vertex undecided
+      }
       int rounds = 0;
       for (;;) {  // four rounds per check; surplus rounds skip decided cells
         for (int r = 0; r < 4; ++r, ++rounds) {
           if (r == 3) MQO_CUDA(cudaMemsetAsync(d_und, 0, sizeof(int32_t) * count, st));
-          k_flip_round<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta,
+          k_flip_round<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_lo, n, count, side, delta,
                                                       d_cand, d_live, d_und);
         }
         MQO_CUDA(cudaGetLastError());
@@ -2048,10 +2201,14 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
         for (int i = 0; i < count; ++i) left |= und[i] != 0;
         if (!left) break;
       }
-      k_flip_commit<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, n, count, side, delta, d_cand,
+      k_flip_commit<<<ls_grid(cells), 256, 0, st>>>(g->d_off, g->d_nbr, g->d_lo, n, count, side, delta, d_cand,
                                                    d_live, reinterpret_cast<unsigned long long*>(d_g1));
       k_flip_apply<<<ls_grid(cells), 256, 0, st>>>(n, count, side, d_cand, d_live);
-      launch_gain(g, count, side, delta, st);
+      if (listed)  // every flip is listed: update the gains around them
+        k_flip_update<<<ls_grid(int64_t(count) * 32 * 1024), 256, 0, st>>>(
+            g->d_off, g->d_nbr, n, count, side, d_cand, delta, d_list, d_len, d_live);
+      else
+        launch_gain(g, count, side, delta, st);
       MQO_CUDA(cudaGetLastError());
       MQO_CUDA(cudaMemcpyAsync(pg.data(), d_g1, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
       MQO_CUDA(cudaStreamSynchronize(st));
@@ -2095,6 +2252,8 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   cudaFreeAsync(d_cand, st);
   if (d_next) cudaFreeAsync(d_next, st);
   if (d_stats) cudaFreeAsync(d_stats, st);
+  for (void* p : {static_cast<void*>(d_cnt), static_cast<void*>(d_list), static_cast<void*>(d_len3)})
+    if (p) cudaFreeAsync(p, st);
 }
 
 // Scratch of the (1,2)-swap kernels: dirty flags, the dirty list(s) and the
@@ -2540,6 +2699,36 @@ inline int64_t small_csr_bytes(int32_t n, int64_t nnz) {
 // the input check of k_tight is left in d_bad[count] (bit 0 not independent, bit 1 not maximal)
 // for the caller to raise after its copy-out, instead of a host round trip
 // here; flagged bodies are left untouched.
+// lower-neighbour count per row (binary search for the first entry >= v)
+__global__ void k_lower_counts(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                               int32_t n, int32_t* __restrict__ lo) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < n;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t a = off[v], b = off[v + 1];
+    const int64_t e0 = a;
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (nbr[mid] < v) a = mid + 1; else b = mid;
+    }
+    lo[v] = static_cast<int32_t>(a - e0);
+  }
+}
+
+// lower-neighbour counts of the graph (k_lower_counts), built once
+void ensure_lo(mqo_graph* g, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g->lazy_mu);
+  if (g->d_lo) return;
+  void* p = nullptr;
+  const cudaStream_t ms = mem_stream(g->device);
+  MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * std::max(g->n, 1), ms));
+  MQO_CUDA(cudaStreamSynchronize(ms));
+  auto* lo = static_cast<int32_t*>(p);
+  if (g->n) k_lower_counts<<<ls_grid(g->n), 256, 0, st>>>(g->d_off, g->d_nbr, g->n, lo);
+  MQO_CUDA(cudaGetLastError());
+  MQO_CUDA(cudaStreamSynchronize(st));
+  g->d_lo = lo;
+}
+
 // hmax (k_hmax) of the graph, built once, complete before any stream uses it
 void ensure_hmax(mqo_graph* g, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(g->lazy_mu);
