@@ -173,6 +173,7 @@ struct mqo_graph {
   int32_t* d_cta = nullptr;   // slot layout of the SMEM trajectory path (lazy)
   int32_t* d_hmax = nullptr;  // max degree over higher neighbours (2-flip filter, lazy)
   int32_t* d_lo = nullptr;    // lower-neighbour count per row (1-flip rounds, lazy)
+  int32_t* d_crow = nullptr;  // row of every 32nd CSR entry (edge-parallel cut, lazy)
   int64_t cta_words = 0;
   std::vector<int32_t> h_cta_rows, h_cta_base;  // per-slice rows / ELL base (host copy)
   // host copy of the CSR: filled at upload for host-only graphs, downloaded on

@@ -356,7 +356,8 @@ extern "C" int mqo_graph_free(mqo_graph* g) {
       const cudaStream_t ms = mem_stream(g->device);
       for (void* p : {static_cast<void*>(g->d_off), static_cast<void*>(g->d_nbr),
                       static_cast<void*>(g->d_order), static_cast<void*>(g->d_cta),
-                      static_cast<void*>(g->d_hmax), static_cast<void*>(g->d_lo)})
+                      static_cast<void*>(g->d_hmax), static_cast<void*>(g->d_lo),
+                      static_cast<void*>(g->d_crow)})
         if (p) cudaFreeAsync(p, ms);
     }
     delete g;

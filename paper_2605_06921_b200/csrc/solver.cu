@@ -460,14 +460,32 @@ __global__ void k_pack(const uint8_t* __restrict__ st, const double* __restrict_
 __global__ void k_side_bits(const double* __restrict__ X, int32_t n, int32_t B, int32_t Bp,
                             int32_t words, uint32_t* __restrict__ sides) {
   const int lane = threadIdx.x & 31;
-  const int64_t total = static_cast<int64_t>(n) * words;
-  for (int64_t q = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; q < total;
-       q += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const int64_t v = q / words;
-    const int c = static_cast<int>(q % words) * 32 + lane;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  if (Bp < 32) {
+    // 32 / Bp rows per ballot (Bp is 4, 8 or 16 here): lane l reads chain
+    // l % Bp of row v0 + l / Bp; the words past the chains stay zero (the
+    // buffer is cleared when allocated)
+    const int per = 32 / Bp;
+    for (int64_t v0 = w0 * per; v0 < n; v0 += nw * per) {
+      const int64_t v = v0 + lane / Bp;
+      const int c = lane % Bp;
+      const bool on = v < n && c < B && X[v * Bp + c] > 0.0;
+      const uint32_t bits = __ballot_sync(0xffffffffu, on);
+      if (lane < per && v0 + lane < n)
+        sides[(v0 + lane) * words] = (bits >> (lane * Bp)) & ((1u << Bp) - 1u);
+    }
+    return;
+  }
+  const int used = (B + 31) / 32;  // words holding chains; the others stay zero
+  const int64_t total = static_cast<int64_t>(n) * used;
+  for (int64_t q = w0; q < total; q += nw) {
+    const int64_t v = q / used;
+    const int wd = static_cast<int>(q % used);
+    const int c = wd * 32 + lane;
     const bool on = c < B && X[v * Bp + c] > 0.0;
     const uint32_t bits = __ballot_sync(0xffffffffu, on);
-    if (lane == 0) sides[q] = bits;
+    if (lane == 0) sides[v * words + wd] = bits;
   }
 }
 
@@ -486,21 +504,26 @@ __global__ void k_cut_vm(const int64_t* __restrict__ off, const int32_t* __restr
     uint32_t cnt[4] = {0, 0, 0, 0};
     for (int64_t v = warp; v < n; v += nwarps) {
       const uint4 sv = __ldg(reinterpret_cast<const uint4*>(sides + v * words + c4));
+      // each edge counted once, from its higher endpoint: the lower
+      // neighbours are a row prefix (rows ascend), and a hub's lower row is
+      // short -- counted from the lower endpoint, one warp walked a hub's
+      // thousands of neighbours while the grid waited
       const int64_t e0 = off[v], e1 = off[v + 1];
       for (int64_t base = e0; base < e1; base += 32) {
-        const int32_t mine = base + lane < e1 ? __ldg(nbr + base + lane) : -1;
-        const int k = e1 - base < 32 ? static_cast<int>(e1 - base) : 32;
+        const int32_t mine = base + lane < e1 ? __ldg(nbr + base + lane) : INT_MAX;
+        const unsigned below = __ballot_sync(0xffffffffu, mine < v);
+        if (!below) break;  // the rest of the row is above v
+        const int k = __popc(below);  // a prefix of the chunk
 #pragma unroll 8
         for (int j = 0; j < k; ++j) {
           const int32_t u = __shfl_sync(0xffffffffu, mine, j);
-          if (u > v) {
-            const uint4 su = __ldg(reinterpret_cast<const uint4*>(sides + int64_t(u) * words + c4));
-            cnt[0] += ((sv.x ^ su.x) >> lane) & 1u;
-            cnt[1] += ((sv.y ^ su.y) >> lane) & 1u;
-            cnt[2] += ((sv.z ^ su.z) >> lane) & 1u;
-            cnt[3] += ((sv.w ^ su.w) >> lane) & 1u;
-          }
+          const uint4 su = __ldg(reinterpret_cast<const uint4*>(sides + int64_t(u) * words + c4));
+          cnt[0] += ((sv.x ^ su.x) >> lane) & 1u;
+          cnt[1] += ((sv.y ^ su.y) >> lane) & 1u;
+          cnt[2] += ((sv.z ^ su.z) >> lane) & 1u;
+          cnt[3] += ((sv.w ^ su.w) >> lane) & 1u;
         }
+        if (k < 32) break;
       }
     }
 #pragma unroll
@@ -513,21 +536,118 @@ __global__ void k_cut_vm(const int64_t* __restrict__ off, const int32_t* __restr
   }
 }
 
+// K5b for up to 32 chains (one side word per vertex), edge-parallel: a warp
+// takes 32 consecutive CSR entries (the whole grid strides over the entry
+// range, so hub rows spread over many warps), finds each entry's row among
+// the chunk's few rows (crow[q] = the row holding entry 32q, a per-graph
+// index; the offsets of rows crow[q]..crow[q+1] are shuffled between lanes),
+// keeps the edge when its neighbour is lower (each edge once) and XORs the
+// two side words; per chain c the warp sums bit c over its lanes with one
+// ballot.  (k_cut_vm, a warp walking a row's neighbours one broadcast load
+// at a time: 0.41 ms at C4 x 16; row blocks per warp: hub blocks 1.4 ms.)
+__global__ void k_cut_edges(const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                            const int32_t* __restrict__ crow, int64_t nnz, int32_t B,
+                            int32_t words, const uint32_t* __restrict__ sides,
+                            int64_t* __restrict__ cut) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t chunks = (nnz + 31) / 32;
+  uint32_t cnt = 0;  // chain `lane`
+  for (int64_t q = w0; q < chunks; q += nw) {
+    const int32_t r0 = crow[q], r1 = crow[q + 1];  // rows r0..r1 hold the chunk
+    const int span = r1 - r0 + 1;
+    const int64_t ent = q * 32 + lane;
+    int32_t v = r0;
+    if (span <= 32) {
+      const int64_t my_off = lane < span ? off[r0 + lane] : INT64_MAX;
+      int r = 0;  // the last of the span's offsets <= ent
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int64_t o = __shfl_sync(0xffffffffu, my_off, r + step < 32 ? r + step : 31);
+        if (r + step < span && o <= ent) r += step;
+      }
+      v = r0 + r;
+    } else if (ent < nnz) {  // many empty / one-entry rows: search the offsets
+      int32_t lo = r0, hi = r1;
+      while (lo < hi) {
+        const int32_t mid = lo + (hi - lo + 1) / 2;
+        if (off[mid] <= ent) lo = mid; else hi = mid - 1;
+      }
+      v = lo;
+    }
+    uint32_t x = 0;
+    if (ent < nnz) {
+      const int32_t u = nbr[ent];
+      if (u < v) x = sides[int64_t(v) * words] ^ sides[int64_t(u) * words];
+    }
+    for (int ch = 0; ch < B; ++ch) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, (x >> ch) & 1u);
+      if (lane == ch) cnt += __popc(bits);
+    }
+  }
+  if (lane < B && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(cut + lane),
+                                 static_cast<unsigned long long>(cnt));
+}
+
+// crow[q] = the row holding CSR entry 32q (q < chunks), crow[chunks] = the
+// row of the last entry
+__global__ void k_chunk_rows(const int64_t* __restrict__ off, int32_t n, int64_t nnz,
+                             int32_t* __restrict__ crow) {
+  const int64_t chunks = (nnz + 31) / 32;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q <= chunks;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ent = q < chunks ? q * 32 : nnz - 1;
+    int32_t lo = 0, hi = n - 1;  // the last row with off[row] <= ent
+    while (lo < hi) {
+      const int32_t mid = lo + (hi - lo + 1) / 2;
+      if (off[mid] <= ent) lo = mid; else hi = mid - 1;
+    }
+    crow[q] = lo;
+  }
+}
+
 int grid_for(int64_t work, int threads = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, 148 * 32)));
+}
+
+// the chunk -> row index of k_cut_edges, built once per graph
+void ensure_chunk_rows(mqo_graph* g, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g->lazy_mu);
+  if (g->d_crow) return;
+  const int64_t chunks = (2 * g->m + 31) / 32;
+  void* p = nullptr;
+  const cudaStream_t ms = mem_stream(g->device);
+  MQO_CUDA(cudaMallocAsync(&p, sizeof(int32_t) * (chunks + 1), ms));
+  MQO_CUDA(cudaStreamSynchronize(ms));
+  auto* crow = static_cast<int32_t*>(p);
+  k_chunk_rows<<<grid_for(chunks + 1), 256, 0, st>>>(g->d_off, g->n, 2 * g->m, crow);
+  MQO_CUDA(cudaGetLastError());
+  MQO_CUDA(cudaStreamSynchronize(st));
+  g->d_crow = crow;
 }
 
 // Cut values of the current iterates into d_scores (zeroed by the caller).
 void launch_cut(mqo_batch* b, const double* X) {
   const mqo_graph* g = b->g;
   const int32_t words = ((b->B + 31) / 32 + 3) / 4 * 4;
-  if (!b->d_sides)
-    dalloc(b, &b->d_sides, sizeof(uint32_t) * std::max<int64_t>(1, int64_t(g->n) * words));
-  k_side_bits<<<grid_for(int64_t(g->n) * words * 32), 256, 0, b->stream>>>(X, g->n, b->B, b->Bp,
-                                                                          words, b->d_sides);
+  if (!b->d_sides) {  // zeroed once: k_side_bits writes only the words holding chains
+    const size_t bytes = sizeof(uint32_t) * std::max<int64_t>(1, int64_t(g->n) * words);
+    dalloc(b, &b->d_sides, bytes);
+    MQO_CUDA(cudaMemsetAsync(b->d_sides, 0, bytes, b->stream));
+  }
+  const int64_t rows_per_warp = b->Bp < 32 ? 32 / b->Bp : 1;
+  k_side_bits<<<grid_for(int64_t(g->n) * ((b->B + 31) / 32) * 32 / rows_per_warp), 256, 0, b->stream>>>(
+      X, g->n, b->B, b->Bp, words, b->d_sides);
   MQO_CUDA(cudaGetLastError());
-  k_cut_vm<<<148 * 8, 256, 0, b->stream>>>(g->d_off, g->d_nbr, g->n, b->B, words, b->d_sides,
-                                           b->d_scores);
+  const int64_t nnz = 2 * g->m;
+  if (b->B <= 32 && nnz > 0) {
+    ensure_chunk_rows(const_cast<mqo_graph*>(g), b->stream);
+    k_cut_edges<<<grid_for((nnz + 31) / 32 * 32), 256, 0, b->stream>>>(
+        g->d_off, g->d_nbr, g->d_crow, nnz, b->B, words, b->d_sides, b->d_scores);
+  } else
+    k_cut_vm<<<148 * 8, 256, 0, b->stream>>>(g->d_off, g->d_nbr, g->n, b->B, words, b->d_sides,
+                                             b->d_scores);
   MQO_CUDA(cudaGetLastError());
 }
 
