@@ -1311,6 +1311,57 @@ __global__ void __launch_bounds__(32 * NW, 1)
       if (!r_commit[k]) continue;
       const int32_t v = c_v[k];
       const int nf = r_nf[k];
+      if (nf == 1) {
+        // one joint flip (v, u), u in N(v): the sequential pair apply_flip(v),
+        // apply_flip(u) in closed form -- the two rows' neighbour updates
+        // commute (no other commit of the step is adjacent to v or u, so
+        // every other side read here is final), only the v-u edge terms
+        // depend on the order -- so both rows and both mark walks run in
+        // one pass instead of two chains of dependent L2 trips
+        const int32_t u = r_part[k][0];
+        const uint8_t svn = side[v] ^ 1, sun = side[u] ^ 1, su = sun ^ 1;
+        const int64_t vb = off[v], ve = off[v + 1], ub = off[u], ue = off[u + 1];
+        __syncwarp();  // every lane has read the old sides
+        if (lane == 0) {
+          side[v] = svn;
+          side[u] = sun;
+          const int32_t dv0 = delta[v], du0 = delta[u];
+          delta[v] = -dv0 + (svn == sun ? 2 : -2);
+          delta[u] = -(du0 + (su == svn ? 2 : -2));
+        }
+        const int64_t nv = ve - vb, tot = nv + (ue - ub);
+        for (int64_t i = lane; i < tot; i += 32) {
+          const bool in_v = i < nv;
+          const int32_t y = in_v ? nbr[vb + i] : nbr[ub + (i - nv)];
+          if (y == (in_v ? u : v)) continue;  // the v-u edge: done above
+          atomicAdd(delta + y, side[y] == (in_v ? svn : sun) ? 2 : -2);
+        }
+        __syncwarp();
+        // the re-marks of both changed sets: y over {v} U N(v) U {u} U N(u)
+        for (int64_t i = lane; i < tot + 2; i += 32) {
+          const int32_t y = i == 0 ? v : i <= nv ? nbr[vb + i - 1] : i == nv + 1 ? u : nbr[ub + (i - nv - 2)];
+          if (y > v) cand[y] = 1;
+          next_marks[y] = 1;
+          for (int64_t c = off[y], c1 = off[y + 1]; c < c1; c += 4) {
+            int32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = c + q < c1 ? nbr[c + q] : INT_MAX;
+            bool stop = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (w[q] < y) {
+                if (w[q] > v) cand[w[q]] = 1;
+                next_marks[w[q]] = 1;
+              } else {
+                stop = true;
+              }
+            }
+            if (stop) break;
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       for (int f = 0; f < nf; ++f) {
         for (int step = 0; step < 2; ++step) {
           const int32_t t = step == 0 ? v : r_part[k][f];

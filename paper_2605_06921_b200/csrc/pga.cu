@@ -84,6 +84,7 @@ struct PassArgs {
   int32_t hblocks, lblocks;  // CTAs per chain group for heavy / light rows (lblocks 0: rest)
   int32_t stage_doubles;     // SMEM staging capacity (doubles) of a heavy CTA
   int32_t stage_off;         // byte offset of the staging buffer in dynamic SMEM
+  int32_t fuse_ctl;          // k_traj_pass: the last CTA of the pass runs k_traj_ctl's work
 };
 
 // Compile-time tuning of the fused kernels: neighbours in flight per lane,
@@ -662,6 +663,8 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj(PassArgs a) {
 // long enough that launch latency is irrelevant and the hardware block
 // scheduler balances rows better than a static persistent split.  The stop
 // decisions of pass p run in k_traj_ctl right after it (same stream).
+__device__ void traj_ctl_cta(const PassArgs& a);
+
 template <int KIND, int CPL, class TU>
 __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
   constexpr bool MIS = KIND == MQO_MIS_QUBO;
@@ -696,6 +699,22 @@ __global__ void __launch_bounds__(kThreads, TU::MINB) k_traj_pass(PassArgs a) {
     uint32_t* gv = a.viol + slot * a.Bp + b;
     if (*reinterpret_cast<volatile uint32_t*>(gv) == 0u) atomicOr(gv, 1u);
   }
+  if (a.fuse_ctl) {
+    // the pass's stop decisions by its last CTA (threadfence reduction):
+    // one launch per pass instead of the pass + k_traj_ctl
+    __shared__ unsigned s_ticket;
+    __threadfence();  // every thread's accumulator atomics before the ticket
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_ticket = atomicAdd(reinterpret_cast<unsigned*>(a.flag + 3), 1u);
+    }
+    __syncthreads();
+    if (s_ticket == gridDim.x - 1) {
+      __threadfence();
+      traj_ctl_cta(a);
+      if (threadIdx.x == 0) a.flag[3] = 0;
+    }
+  }
 }
 
 // Active-chain mask per quad from ChainCtl (one CTA; after a __syncthreads
@@ -718,9 +737,13 @@ __global__ void k_qmask(const ChainCtl* ctl, int32_t B, int32_t Q, int32_t cpl, 
 
 // K2 for the per-launch path: one CTA takes pass p's stop decisions
 // (pga.cpp:89-102), clears the next accumulator slot, publishes the count.
+__device__ void traj_ctl_cta(const PassArgs& a);
 __global__ void k_traj_ctl(PassArgs a) {
-  __shared__ int s_count;
   if (*reinterpret_cast<volatile int32_t*>(a.flag) == 0) return;
+  traj_ctl_cta(a);
+}
+__device__ void traj_ctl_cta(const PassArgs& a) {
+  __shared__ int s_count;
   const int32_t p = a.p_begin;
   const int slot = p % 3, next = (p + 1) % 3;
   if (threadIdx.x == 0) s_count = 0;
@@ -732,11 +755,12 @@ __global__ void k_traj_ctl(PassArgs a) {
     bool stop = false;
     if (a.is_mis) {
       const int32_t t = p - 1;
-      if (t >= 1 && t % a.check_every == 0 && a.viol[slot * a.Bp + b] == 0u) {
+      if (t >= 1 && t % a.check_every == 0 &&
+          *reinterpret_cast<const volatile uint32_t*>(a.viol + slot * a.Bp + b) == 0u) {
         stop = true;
         c = ChainCtl{0, t, MQO_CHECKER_ACCEPTED, (a.base + t) & 1};
       }
-    } else if (a.viol[slot * a.Bp + b] == 0u) {  // max|dx| <= conv_tol
+    } else if (*reinterpret_cast<const volatile uint32_t*>(a.viol + slot * a.Bp + b) == 0u) {  // max|dx| <= conv_tol
       stop = true;
       c = ChainCtl{0, p, MQO_CONVERGED, (a.base + p) & 1};
     }
@@ -1096,6 +1120,12 @@ void launch_groups(const mqo_batch* b, PassArgs& a, int blocks, size_t smem, F f
   a.heavy = a.hblocks = a.lblocks = 0;
 }
 
+// MQO_FUSE_CTL=0: k_traj_ctl as its own launch after every pass (A/B runs)
+const bool g_fuse_ctl = [] {
+  const char* e = std::getenv("MQO_FUSE_CTL");
+  return !(e && *e == '0');
+}();
+
 // Problems up to this many (vertex, chain) cells run the persistent kernel.
 int64_t g_persistent_cells = [] {
   const char* e = std::getenv("MQO_PERSISTENT_CELLS");
@@ -1214,15 +1244,20 @@ void run_trajectories(mqo_batch* b, const mqo_objective& obj, const mqo_optimize
                                            args, smem, b->stream));
     } else {
       if (p == 1) {
+        MQO_CUDA(cudaMemsetAsync(b->d_flag + 3, 0, sizeof(int32_t), b->stream));  // fused-ctl tickets
         MQO_CUDA(cudaMemsetAsync(b->d_viol, 0, sizeof(uint32_t) * 3 * b->Bp, b->stream));
         MQO_CUDA(cudaMemsetAsync(b->d_chg, 0, sizeof(unsigned long long) * 3 * b->Bp, b->stream));
       }
+      // one launch per pass (untiled, or the chain groups fused into one
+      // grid): its last CTA takes the stop decisions
+      a.fuse_ctl = g_fuse_ctl && (a.Qg == b->Q || g_fuse_groups) ? 1 : 0;
       for (int32_t q = p; q < chunk_end; ++q) {
         a.p_begin = q;
         a.p_end = q + 1;
         launch_groups(b, a, blocks, smem, fn);
-        k_traj_ctl<<<1, 256, 0, b->stream>>>(a);
+        if (!a.fuse_ctl) k_traj_ctl<<<1, 256, 0, b->stream>>>(a);
       }
+      a.fuse_ctl = 0;
       MQO_CUDA(cudaGetLastError());
     }
     MQO_CUDA(cudaMemcpyAsync(b->h_flag, b->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost,
