@@ -2127,7 +2127,8 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       if (g_scan_multi) {
         MQO_CUDA(cudaMemsetAsync(d_next, 0, cells, st));
         // candidates per step = 32 warps x C (MQO_SCAN_C = 4 | 8 | 16)
-        auto kern = g_scan_g == 8    ? k_two_scan_multi<32, 8, 8>
+        auto kern = g_scan_g == 8    ? (g_scan_c == 4 ? k_two_scan_multi<32, 4, 8>
+                                                       : k_two_scan_multi<32, 8, 8>)
                     : g_scan_g == 16 ? k_two_scan_multi<32, 8, 16>
                     : g_scan_c == 4  ? k_two_scan_multi<32, 4, 32>
                     : g_scan_c == 16 ? k_two_scan_multi<32, 16, 32>
