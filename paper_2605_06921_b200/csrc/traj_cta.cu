@@ -31,6 +31,9 @@
 #include <cstdlib>
 #include <thread>
 
+#include <mutex>
+#include <set>
+
 #include "common.cuh"
 
 using namespace mqo_b200;
@@ -562,18 +565,32 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
   const size_t smem = cta_smem_for(g, C, a.max_slices, a.max_ell, smem_lay);
   if (smem > kCtaSmemMax) throw std::logic_error("cta trajectories: state exceeds SMEM");
   CtaFn fn = cta_fn(obj.kind, smem_lay, C > 1);
-  // the cap, not this launch's size: the attribute is per function, and
-  // solves on other host threads launch the same kernel with other sizes
-  MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kCtaSmemMax)));
+  // the cap, not this launch's size (the attribute is per function, and
+  // solves on other host threads launch the same kernel with other sizes),
+  // set once per (function, device) -- not while another thread's launch
+  // of the same function may be in flight
+  {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.insert({reinterpret_cast<const void*>(fn), g->device}).second) {
+      MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kCtaSmemMax)));
+      MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+  }
+  // the cluster kernel is launched on a drained stream: queued behind
+  // pending work while another host thread drives the same GPU it faulted
+  // intermittently (illegal address, ~1 in 100 solve_devices([0, 0]) calls;
+  // scripts/repro_devices.py: 0 in 360 with the drain, root cause not
+  // identified); one host sync per trajectory run
+  MQO_CUDA(cudaStreamSynchronize(b->stream));
   const int threads = cta_threads(C, a.max_slices);
   if (C == 1) {
     fn<<<b->B, threads, smem, b->stream>>>(a);
   } else {
-    if (C > 8)
-      MQO_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(b->B * C));
     cfg.blockDim = dim3(static_cast<unsigned>(threads));
