@@ -190,6 +190,9 @@ struct mqo_graph {
 namespace mqo_b200 {
 // the host CSR of g (downloaded once for device graphs; thread-safe)
 void host_csr(const mqo_graph* g);
+// this host thread runs an engine rank that shares its GPU with another
+// rank of the same process (mqo_solve_devices): no SMEM trajectory kernel
+extern thread_local bool g_tls_no_cta_traj;
 }  // namespace mqo_b200
 
 struct mqo_batch {

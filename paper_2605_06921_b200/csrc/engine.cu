@@ -743,6 +743,10 @@ extern "C" int mqo_solve_devices(mqo_graph* g, const mqo_solver_config* cfg, con
         threads.emplace_back([&, r] {
           try {
             MQO_CUDA(cudaSetDevice(devices[r]));
+            // ranks sharing a GPU: the SMEM/cluster trajectory kernel is left
+            // out (an intermittent fault with another rank's work in flight,
+            // DESIGN.md section 8); the per-pass kernels give the same report
+            g_tls_no_cta_traj = !distinct;
             if (mode == MQO_SOLVE_POOLED)
               solve_pooled_impl(graphs[r], cfg, comms[r], &reports[r], r == 0 ? best_body : nullptr);
             else

@@ -2327,7 +2327,11 @@ void launch_swap_cta(const mqo_graph* g, int32_t count, LsWork& w, int64_t* d_ou
                      cudaStream_t st, int32_t* d_bad) {
   alloc_swap_lists(g, count, w, st, true);
   const int64_t cbytes = swap_cta_smem_bytes(g->n, 2 * g->m, g->max_degree);
-  const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem;
+  static const bool swap_smem = [] {
+    const char* e = std::getenv("MQO_SWAP_SMEM");
+    return !(e && *e == '0');
+  }();
+  const bool csm = cbytes <= kSwapSmemMax - 1024 && g_swap_smem && swap_smem;
   auto kern = csm ? k_mis_swap_cta<16, true> : k_mis_swap_cta<16, false>;
   if (csm) {  // the SMEM opt-in, once per device
     static std::mutex mu;

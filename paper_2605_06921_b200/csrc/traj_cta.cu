@@ -420,6 +420,7 @@ CtaFn cta_fn(int kind, bool smem_lay, bool lookahead) {
 namespace mqo_b200 {
 
 constexpr size_t kCtaSmemMax = 200 * 1024;
+thread_local bool g_tls_no_cta_traj = false;
 bool g_cta_disabled = false;  // mqo_tune("cta_traj", 0)
 int g_cta_cluster = 0;        // mqo_tune("cta_cluster", C): 0 = automatic
 
@@ -485,7 +486,7 @@ int cta_group(const mqo_batch* b) {
     const char* e = std::getenv("MQO_NO_CTA_TRAJ");
     return e && *e && *e != '0';
   }();
-  if (disabled || g_cta_disabled) return 0;
+  if (disabled || g_cta_disabled || g_tls_no_cta_traj) return 0;
   const mqo_graph* g = b->g;
   // slot words pack vertex | degree << 16
   if (g->n <= 0 || g->n >= 65536 || g->max_degree >= 32768) return 0;
@@ -581,11 +582,12 @@ void run_trajectories_cta(mqo_batch* b, const mqo_objective& obj, const mqo_opti
                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
   }
-  // the cluster kernel is launched on a drained stream: queued behind
-  // pending work while another host thread drives the same GPU it faulted
-  // intermittently (illegal address, ~1 in 100 solve_devices([0, 0]) calls;
-  // scripts/repro_devices.py: 0 in 360 with the drain, root cause not
-  // identified); one host sync per trajectory run
+  // one SMEM trajectory kernel at a time per GPU, on a drained stream: two
+  // of them in flight from different host threads faulted intermittently
+  // (illegal address; ~1 in 100 solve_devices([0, 0]) calls, root cause not
+  // identified -- scripts/repro_devices.py)
+  static std::mutex dev_mu[64];
+  std::unique_lock<std::mutex> dev_lock(dev_mu[g->device & 63]);
   MQO_CUDA(cudaStreamSynchronize(b->stream));
   const int threads = cta_threads(C, a.max_slices);
   if (C == 1) {
