@@ -189,6 +189,7 @@ extern "C" int mqo_batch_free(mqo_batch* b) {
       dfree(b, b->d_qmask);
       free_solver_buffers(b);
       dfree(b, b->d_ls);
+      dfree(b, b->d_flip);
       cudaStreamSynchronize(b->stream);
     }
     pinned_put(b->h_ls, b->ls_bytes);

@@ -227,6 +227,8 @@ struct mqo_batch {
   int32_t* d_jdraw = nullptr;           // [Bp][n] reset draws j_i
   int32_t* d_counter = nullptr;         // [4] device counters
   uint64_t* d_ls = nullptr;             // mqo_local_search staging (device, grow-only)
+  int32_t* d_flip = nullptr;            // 1-flip closure state [2][count * n] + 3 count (grow-only)
+  size_t flip_bytes = 0;
   uint64_t* h_ls = nullptr;             // ... and its pinned host mirror
   size_t ls_bytes = 0;
 };

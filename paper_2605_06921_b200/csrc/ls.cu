@@ -2079,8 +2079,9 @@ struct LsWork {
 // nothing.  gains[s] = total gain.
 void ensure_lo(mqo_graph* g, cudaStream_t st);
 
-void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* side, int32_t* delta,
+void maxcut_ls_host_driven(mqo_batch* b, int32_t op, int32_t count, uint8_t* side, int32_t* delta,
                            int64_t* d_out, cudaStream_t st) {
+  mqo_graph* g = b->g;
   const int32_t n = g->n;
   const int64_t cells = std::max<int64_t>(1, int64_t(count) * n);
   const int blocks = (count + kLsWarps - 1) / kLsWarps;
@@ -2192,10 +2193,17 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       return;
     }
     ensure_lo(g, st);
-    if (!d_cnt) {  // closure state: counters, lists, [len | fa | fb] per body
-      MQO_CUDA(cudaMallocAsync(&d_cnt, sizeof(int32_t) * cells, st));
-      MQO_CUDA(cudaMallocAsync(&d_list, sizeof(int32_t) * cells, st));
-      MQO_CUDA(cudaMallocAsync(&d_len3, sizeof(int32_t) * 3 * count, st));
+    if (!d_cnt) {  // closure state: counters, lists, [len | fa | fb] per body, kept
+                   // with the batch (the engine's local-search calls reuse it)
+      const size_t need = sizeof(int32_t) * (2 * cells + 3 * count);
+      if (b->flip_bytes < need) {
+        dfree(b, b->d_flip);
+        dalloc(b, &b->d_flip, need);
+        b->flip_bytes = need;
+      }
+      d_cnt = b->d_flip;
+      d_list = d_cnt + cells;
+      d_len3 = d_list + cells;
     }
     int32_t* d_len = d_len3;
     int32_t* d_fa = d_len3 + count;
@@ -2220,6 +2228,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
       MQO_CUDA(cudaStreamSynchronize(st));
       bool listed = g_flip_closure;
       for (int i = 0; i < count; ++i) listed &= !plive[i] || int64_t(lens[i]) * 4 <= n;
+      MQO_TRACE("one_flip pass %d: seeds of body 0 %d, %s", pass, lens[0], listed ? "closure" : "all vertices");
       if (listed) {  // the closure, four frontier steps per check
         for (int step = 0;; step += 4) {
           for (int r = 0; r < 4; ++r) {
@@ -2234,7 +2243,10 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
           MQO_CUDA(cudaStreamSynchronize(st));
           bool more = false;
           for (int i = 0; i < count; ++i) more |= lens[i] != lens[2 * count + i];  // len != fb
-          if (!more) break;
+          if (!more) {
+            MQO_TRACE("one_flip pass %d: closure of body 0 %d after %d steps", pass, lens[0], step + 4);
+            break;
+          }
         }
       } else {
         MQO_CUDA(cudaMemsetAsync(d_cand, 0, cells, st));  // every vertex undecided
@@ -2304,8 +2316,7 @@ void maxcut_ls_host_driven(mqo_graph* g, int32_t op, int32_t count, uint8_t* sid
   cudaFreeAsync(d_cand, st);
   if (d_next) cudaFreeAsync(d_next, st);
   if (d_stats) cudaFreeAsync(d_stats, st);
-  for (void* p : {static_cast<void*>(d_cnt), static_cast<void*>(d_list), static_cast<void*>(d_len3)})
-    if (p) cudaFreeAsync(p, st);
+
 }
 
 // Scratch of the (1,2)-swap kernels: dirty flags, the dirty list(s) and the
@@ -2897,8 +2908,13 @@ void local_search_device(mqo_batch* b, int32_t op, int32_t count, uint64_t* d_pa
   if (op <= 2) {
     launch_gain(g, count, w.bytes, w.ints, st);
     MQO_CUDA(cudaGetLastError());
+    if (trace_on()) {
+      MQO_CUDA(cudaStreamSynchronize(st));
+      MQO_TRACE("local search: bodies unpacked, gain tables built");
+    }
     ensure_hmax(g, st);
-    maxcut_ls_host_driven(g, op, count, w.bytes, w.ints, d_out, st);
+    MQO_TRACE("local search: hmax ready");
+    maxcut_ls_host_driven(b, op, count, w.bytes, w.ints, d_out, st);
   } else if (d_bad && g_swap_cta) {
     // the input check stays on the device: k_tight flags bad bodies in
     // d_bad (zeroed by the caller), which the swap kernel then leaves untouched
