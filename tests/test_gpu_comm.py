@@ -85,3 +85,19 @@ def test_rank_failure_fails_every_rank(P, mode, monkeypatch):
     monkeypatch.delenv("MQO_FAULT_RANK")
     r, _ = P.solve_devices(g, cfg, [0, 0], mode)  # the library is still usable
     assert r.found_solution
+
+
+@pytest.mark.timeout(300)
+def test_solve_devices_shared_gpu_stress(P):
+    """Two and three engine ranks on one GPU from host threads, repeatedly
+    (the configuration in which the SMEM/cluster trajectory kernel faulted
+    intermittently): every call completes and the pooled
+    report equals the single-process solve."""
+    cases = _cfgs(P)
+    refs = [P.solve_pooled(g, cfg) for g, cfg in cases]
+    for _ in range(15):
+        for (g, cfg), ref in zip(cases, refs):
+            for devs in ([0, 0], [0, 0, 0]):
+                r, _ = P.solve_devices(g, cfg, devs, "pooled")
+                assert _key(r) == _key(ref)
+                P.solve_devices(g, cfg, devs, "replicas")
