@@ -746,7 +746,11 @@ extern "C" int mqo_solve_devices(mqo_graph* g, const mqo_solver_config* cfg, con
             // ranks sharing a GPU: the SMEM/cluster trajectory kernel is left
             // out (an intermittent fault with another rank's work in flight,
             // DESIGN.md section 8); the per-pass kernels give the same report
-            g_tls_no_cta_traj = !distinct;
+            static const bool allow = [] {  // MQO_SHARED_CTA=1: keep it (stress runs)
+              const char* e = std::getenv("MQO_SHARED_CTA");
+              return e && *e == '1';
+            }();
+            g_tls_no_cta_traj = !distinct && !allow;
             if (mode == MQO_SOLVE_POOLED)
               solve_pooled_impl(graphs[r], cfg, comms[r], &reports[r], r == 0 ? best_body : nullptr);
             else
