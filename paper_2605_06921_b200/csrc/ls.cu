@@ -571,11 +571,15 @@ __global__ void k_two_cand(const int64_t* __restrict__ off, const int32_t* __res
     const int64_t s = q / n;
     const int32_t v = static_cast<int32_t>(q - s * n);
     if (!live[s]) continue;
-    if (off[v + 1] - off[v] > kCandWarpDeg) continue;  // k_two_cand_heavy
     // mask (may be null): only vertices the last sweep's commits touched can
-    // have become candidates; the rest keep their "no move"
-    cand_all[q] = (!mask_all || mask_all[q]) &&
-                  two_cand(off, nbr, hmax, side_all + s * n, delta_all + s * n, v) ? 1 : 0;
+    // have become candidates; the rest keep their "no move" (tested before
+    // the row is read; k_two_cand_heavy, launched after, rewrites long rows)
+    if (mask_all && !mask_all[q]) {
+      cand_all[q] = 0;
+      continue;
+    }
+    if (off[v + 1] - off[v] > kCandWarpDeg) continue;  // k_two_cand_heavy
+    cand_all[q] = two_cand(off, nbr, hmax, side_all + s * n, delta_all + s * n, v) ? 1 : 0;
   }
 }
 
